@@ -1,0 +1,169 @@
+/*
+ * skc.h -- C-ABI of libskc, the B200-native hot path of direct sparse convolution
+ * (Park et al., "Faster CNNs with Direct Sparse Convolutions and Guided Pruning",
+ * arXiv:1608.01409).  Citations "PAPER.md:<line>" refer to the paper's LaTeX source.
+ *
+ * The problem (Sec. 2.1, Eq. 1): a bank of K filters W [K][C/g][R][S]
+ * applied to an input I [C][H][W] gives O [K][Ho][Wo],
+ *      O(k,y,x) = sum_{c,r,s} W(k,c,r,s) * I(c, y*stride + r - pad, x*stride + s - pad).
+ * Direct sparse convolution (Fig. 2 at :198-218) stores the pruned
+ * weights in CSR, one row per output channel, with each nonzero's column index
+ * pre-encoded as the layout offset f(c,r,s) into the (zero-padded) input, and computes
+ * every output position as that sparse row dotted with the input vector shifted by
+ * f(0,y,x): a sparse-matrix x "virtual" dense-matrix product, no lowering.
+ *
+ * Conventions for every entry point
+ *   - Status: every function returns skc_status (0 = OK, < 0 = error); a thread-local
+ *     message is available from skc_last_error().  No C++ exception crosses the ABI and
+ *     nothing aborts.  Argument/geometry checks happen before any launch.
+ *   - Precision: fp32 data, fp32 FMA accumulation (single precision).
+ *   - Ownership: the caller owns every device buffer (activations, outputs, the plan
+ *     workspace).  libskc NEVER allocates device memory.  A plan owns its host arrays and
+ *     is freed by skc_plan_destroy(), which does not synchronise: the caller must make
+ *     sure no launch using the plan's workspace is still running.
+ *   - Streams: device work is enqueued asynchronously on the caller's stream (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream).  Launch errors are
+ *     returned as SKC_ERR_CUDA; faults during execution surface at the caller's sync.
+ *   - Thread safety: a plan is immutable after skc_plan_upload(); several threads or
+ *     streams may launch with it concurrently.
+ *   - Layouts (all contiguous, fp32):
+ *       input  NCHW            [N][C][H][W]
+ *       padded input           [N][C][Hp][Wp],  Hp = H + 2*pad, Wp = W + 2*pad
+ *       output NCHW            [N][K][Ho][Wo],  Ho = (H+2*pad-R)/stride + 1 (floor), same Wo
+ *   - Device pointers must be 16-byte aligned (TMA bulk copies), else SKC_ERR_ALIGN.
+ */
+#ifndef SKC_H_
+#define SKC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SKC_OK = 0,
+    SKC_ERR_ARG = -1,         /* NULL pointer, negative count, bad enum value          */
+    SKC_ERR_GEOMETRY = -2,    /* Ho/Wo < 1, K or C not divisible by groups, ...         */
+    SKC_ERR_NONFINITE = -3,   /* a weight is NaN or Inf                                 */
+    SKC_ERR_OVERFLOW = -4,    /* an offset or size does not fit the int32 encoding      */
+    SKC_ERR_UNSUPPORTED = -5, /* shape the kernels cannot tile (no CPU fallback exists) */
+    SKC_ERR_ALIGN = -6,       /* device pointer not 16-byte aligned                     */
+    SKC_ERR_STATE = -7,       /* e.g. forward before skc_plan_upload                    */
+    SKC_ERR_CUDA = -8         /* a CUDA runtime call failed                             */
+} skc_status;
+
+typedef struct skc_plan skc_plan; /* opaque */
+
+/* Kernel variants for the conv step.  AUTO picks per geometry. */
+typedef enum {
+    SKC_KERNEL_AUTO = 0,
+    SKC_KERNEL_DIRECT = 1,   /* Fig. 2 statement per lane: one shared-memory read per MAC */
+    SKC_KERNEL_REGTILE = 2   /* register-tiled input window, per-nonzero dispatch        */
+} skc_kernel;
+
+typedef struct {
+    int K, C, R, S, H, W, stride, pad, groups;
+    int Ho, Wo, Hp, Wp;
+    int64_t nnz;                   /* realised nonzeros (the paper's x*|W|)           */
+    size_t padded_elems_per_image; /* C*Hp*Wp                                           */
+    size_t out_elems_per_image;    /* K*Ho*Wo                                           */
+    size_t device_bytes;           /* workspace size skc_plan_upload needs              */
+    int kernel;                    /* skc_kernel chosen (after AUTO resolution)         */
+    int band_rows, chunk_channels, stages, warps, channels_per_warp, pixels_per_lane;
+    size_t smem_bytes;             /* dynamic shared memory per CTA of the conv kernel  */
+} skc_info;
+
+/* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).
+ * w_host: dense pruned weights, host memory, [K][C/groups][R][S] row-major fp32, read only.
+ * A nonzero is any w != 0.0f.  Canonical CSR: rows k = 0..K-1 in natural order, nonzeros in
+ * ascending (c_local, r, s) == ascending colidx, colidx = ((g_k*(C/g) + c_local)*Hp + r)*Wp + s
+ * with g_k = k / (K/groups) (global input channel; R1-R3).  Also builds the
+ * nnz-sorted channel permutation (descending nnz, stable, within each group) and the kernel-
+ * private streams.  *out receives a new plan (host memory only; upload before use).
+ * Errors: SKC_ERR_ARG (NULL), SKC_ERR_GEOMETRY, SKC_ERR_NONFINITE, SKC_ERR_OVERFLOW
+ * (C*Hp*Wp >= 2^31 or nnz >= 2^31), SKC_ERR_UNSUPPORTED (no kernel tiling fits). */
+skc_status skc_pack_csr(const float *w_host, int K, int C, int R, int S, int H, int W,
+                        int stride, int pad, int groups, skc_plan **out);
+
+/* Same as skc_pack_csr, forcing a kernel variant (testing both paths on one shape). */
+skc_status skc_pack_csr_ex(const float *w_host, int K, int C, int R, int S, int H, int W,
+                           int stride, int pad, int groups, int kernel, skc_plan **out);
+
+skc_status skc_plan_info(const skc_plan *plan, skc_info *info);
+
+/* Host views of the canonical CSR (valid until skc_plan_destroy): rowptr[K+1] int32,
+ * colidx[nnz] int32, values[nnz] fp32. */
+skc_status skc_plan_csr(const skc_plan *plan, const int32_t **rowptr, const int32_t **colidx,
+                        const float **values);
+
+/* Host view of the nnz-sorted channel order perm[K] (within-group, descending nnz, ties by
+ * ascending k).  The kernels assign output channels to warps in this order. */
+skc_status skc_plan_perm(const skc_plan *plan, const int32_t **perm);
+
+/* Copy the plan's kernel-private arrays into a caller-owned device workspace of at least
+ * skc_info.device_bytes bytes (16-byte aligned), asynchronously on `stream`.  The host
+ * arrays stay owned by the plan; the workspace must outlive every launch using the plan. */
+skc_status skc_plan_upload(skc_plan *plan, void *d_workspace, size_t bytes, void *stream);
+
+/* a2 -- padded-input layout (R1): d_in [N][C][H][W] ->
+ * d_in_padded [N][C][Hp][Wp], zeros in the pad-wide border, interior copied bit-exactly.
+ * Both device pointers, caller-owned, must not overlap.  N = 0 is a no-op; N < 0 is
+ * SKC_ERR_ARG. */
+skc_status skc_pad_input(const skc_plan *plan, const float *d_in_nchw, float *d_in_padded,
+                         int N, void *stream);
+
+/* a3..a6 -- the sparse conv (PAPER.md:198-208 Fig. 2; :303-316).  d_in_padded as written by
+ * skc_pad_input (or any buffer in that layout, zero border required), d_out [N][K][Ho][Wo]
+ * (fully overwritten, no accumulation into it).  Requires skc_plan_upload first
+ * (else SKC_ERR_STATE).  Deterministic: each output element is accumulated by one thread in
+ * a fixed order, so repeated calls are bitwise identical. */
+skc_status skc_sparse_conv_forward(const skc_plan *plan, const float *d_in_padded,
+                                   float *d_out, int N, void *stream);
+
+/* End-to-end helper used for the host-buffer measurement: H2D copy of h_in (host, ideally
+ * pinned) into d_in, pad, conv, D2H copy of the result into h_out, all on `stream`.
+ * Caller-owned scratch: d_in [N][C][H][W], d_in_padded, d_out.  Returns after enqueueing. */
+skc_status skc_forward_host(const skc_plan *plan, const float *h_in, float *h_out, int N,
+                            float *d_in, float *d_in_padded, float *d_out, void *stream);
+
+/* Layout function f(c,y,x) of the padded input: test hook.
+ * Returns -1 when (c,y,x) is outside [0,C) x [0,Hp) x [0,Wp). */
+int64_t skc_layout_offset(const skc_plan *plan, int c, int y, int x);
+
+void skc_plan_destroy(skc_plan *plan);
+const char *skc_last_error(void);
+
+/* a7 -- roofline performance model, host fp64.
+ *   C = 2*K*(C/g)*R*S*Ho*Wo*batch FLOP; S_A = 4*batch*(C*H*W + K*Ho*Wo) bytes;
+ *   S_W = 4*K*(C/g)*R*S bytes (x batch unless amortised != 0).
+ *   t_dense = C/F; t_sparse_compute = alpha*x*C/F; t_sparse_bw = (S_A + beta*x*S_W)/B;
+ *   speedup = t_dense / max(t_sparse_compute, t_sparse_bw);
+ *   x_hi = 1/alpha (sparse slower than dense above it);
+ *   x_lo = S_A / (alpha*C*B/F - beta*S_W) (bandwidth crossover; +inf if denominator <= 0). */
+typedef struct { double C, S_A, S_W; } skc_layer_cost;
+typedef struct { double F, B, alpha, beta; } skc_platform;
+typedef struct {
+    double t_dense, t_sparse_compute, t_sparse_bw, t_sparse, speedup, effective_flops,
+        actual_flops;
+} skc_projection;
+typedef struct { double x_lo, x_hi; int has_speedup_potential; } skc_window;
+
+skc_status skc_model_layer_cost(int K, int C, int R, int S, int H, int W, int stride, int pad,
+                                int groups, int64_t batch, int amortised, skc_layer_cost *out);
+skc_status skc_model_project(const skc_layer_cost *cost, double x, const skc_platform *p,
+                             skc_projection *out);
+skc_status skc_model_window(const skc_layer_cost *cost, const skc_platform *p, skc_window *out);
+
+/* Device micro-benchmarks that calibrate the B200 roofline (FFMA issue peak and shared-
+ * memory word bandwidth; the analogue of the paper's SGEMM / STREAM calibration,
+ * PAPER.md:531-532).  d_scratch: >= 4 MiB device buffer.  Each writes the elapsed
+ * device milliseconds and the operation count it performed.  Synchronous. */
+skc_status skc_bench_ffma(void *d_scratch, int blocks, int iters, double *ms, double *flops);
+skc_status skc_bench_lds(void *d_scratch, int blocks, int iters, double *ms, double *bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKC_H_ */

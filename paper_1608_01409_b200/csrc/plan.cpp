@@ -1,0 +1,478 @@
+// plan.cpp -- host side of libskc: the C-ABI (include/skc.h), the CSR/offset packer
+// (row a1), plan construction and upload, launch wrappers for the pad (a2) and conv
+// (a3..a6) kernels, and the B200 roofline model (a7).
+//
+// Everything here is host C++17; device memory is never allocated (the caller owns it).
+#include "skc.h"
+#include "skc_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace skc;
+
+namespace {
+
+thread_local std::string g_err;
+
+skc_status fail(skc_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+skc_status ok() {
+    g_err.clear();
+    return SKC_OK;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// The plan
+// ---------------------------------------------------------------------------------------
+struct skc_plan {
+    int K, C, R, S, H, W, stride, pad, groups;
+    int Ho, Wo, Hp, Wp, Kg, Cg;
+
+    // canonical CSR (the checked contract) and the nnz-sorted order
+    std::vector<int32_t> rowptr, colidx, perm;
+    std::vector<float> values;
+
+    // kernel choice + configuration
+    int kernel = SKC_KERNEL_DIRECT;
+    StageGeom sg{};
+    int T = 0, NW = 0, M = 0, cblocks = 0;
+    size_t smem = 0;
+
+    // device image (bytes uploaded verbatim) and the offsets of its arrays
+    std::vector<uint8_t> image;
+    size_t off_nz = 0, off_chunkptr = 0, off_perm = 0;
+
+    void *d_ws = nullptr;  // set by skc_plan_upload
+};
+
+namespace {
+
+const int kDirectT[] = {2, 4, 6, 8, 12, 16};
+constexpr int kDirectNW = 8;              // compute warps per CTA (+1 producer warp)
+constexpr size_t kStageTarget = 24 << 10;  // bytes per stage we aim for
+constexpr size_t kSmemBudget = 112 << 10;  // per CTA, so that >= 2 CTAs fit an SM
+
+skc_status check_geometry(int K, int C, int R, int S, int H, int W, int stride, int pad,
+                          int groups) {
+    if (K < 1 || C < 1 || R < 1 || S < 1 || H < 1 || W < 1 || stride < 1 || pad < 0 ||
+        groups < 1)
+        return fail(SKC_ERR_GEOMETRY, "non-positive dimension (K=%d C=%d R=%d S=%d H=%d W=%d "
+                    "stride=%d pad=%d groups=%d)", K, C, R, S, H, W, stride, pad, groups);
+    if (C % groups || K % groups)
+        return fail(SKC_ERR_GEOMETRY, "K=%d and C=%d must be divisible by groups=%d", K, C,
+                    groups);
+    if (H + 2 * pad < R || W + 2 * pad < S)
+        return fail(SKC_ERR_GEOMETRY, "kernel %dx%d larger than padded input %dx%d", R, S,
+                    H + 2 * pad, W + 2 * pad);
+    const int64_t plane = int64_t(H + 2 * pad) * (W + 2 * pad);
+    if (plane * C >= (int64_t(1) << 31))
+        return fail(SKC_ERR_OVERFLOW, "C*Hp*Wp = %lld does not fit int32 offsets",
+                    (long long)(plane * C));
+    return SKC_OK;
+}
+
+// Pick the direct kernel's band height, pixels per lane, channel chunk and warp layout.
+skc_status configure_direct(skc_plan *p) {
+    const int Ho = p->Ho, Wo = p->Wo;
+    // (1) bands x pixels-per-lane: maximise lane utilisation Ho*Wo / (nb*32*T)
+    double best_util = -1;
+    int best_nb = 0, best_T = 0;
+    for (int nb = 1; nb <= Ho; ++nb) {
+        const int BH = (Ho + nb - 1) / nb;
+        if ((Ho + BH - 1) / BH != nb) continue;  // same BH as a smaller nb
+        const int need = (BH * Wo + 31) / 32;
+        int T = 0;
+        for (int t : kDirectT)
+            if (t >= need) { T = t; break; }
+        if (!T) continue;
+        const double util = double(Ho) * Wo / (double(nb) * 32 * T);
+        if (util > best_util + 1e-9) { best_util = util; best_nb = nb; best_T = T; }
+    }
+    if (!best_T)
+        return fail(SKC_ERR_UNSUPPORTED, "no band fits (Wo=%d too wide for the direct kernel)",
+                    Wo);
+    StageGeom &g = p->sg;
+    g.C = p->C; g.K = p->K; g.Kg = p->Kg; g.Cg = p->Cg; g.Hp = p->Hp; g.Wp = p->Wp;
+    g.Ho = Ho; g.Wo = Wo; g.stride = p->stride;
+    g.BH = (Ho + best_nb - 1) / best_nb;
+    g.nbands = (Ho + g.BH - 1) / g.BH;
+    g.BHin = std::min((g.BH - 1) * p->stride + p->R, p->Hp);
+    g.whole = (g.nbands == 1 && g.BHin == p->Hp) ? 1 : 0;
+    const size_t chan_bytes = size_t(g.BHin) * g.Wp * 4;
+    // (2) channels per stage
+    int CB = int(std::max<size_t>(1, kStageTarget / chan_bytes));
+    CB = std::min(CB, p->Cg);
+    if (CB >= 4) CB -= CB % 4;
+    g.CB = CB;
+    g.nchunks = (p->Cg + CB - 1) / CB;
+    g.stage_floats = int(align_up(size_t(CB) * g.BHin * g.Wp, 4));
+    const size_t stage_bytes = size_t(g.stage_floats) * 4;
+    g.NS = int(std::min<size_t>(4, std::max<size_t>(1, kSmemBudget / stage_bytes)));
+    g.NS = std::min(g.NS, std::max(1, g.nchunks));
+    if (stage_bytes > 200 * 1024)
+        return fail(SKC_ERR_UNSUPPORTED, "one input channel band needs %zu B of shared memory",
+                    stage_bytes);
+    // (3) bulk-copy (TMA) legality: 16-byte aligned sources, sizes and destinations
+    const int64_t plane = int64_t(g.Hp) * g.Wp;
+    bool bulk = (int64_t(g.C) * plane) % 4 == 0 && (int64_t(g.Cg) * plane) % 4 == 0;
+    if (g.whole) {
+        bulk = bulk && (int64_t(CB) * plane) % 4 == 0 &&
+               (int64_t(g.Cg % CB ? g.Cg % CB : CB) * plane) % 4 == 0;
+    } else {
+        bulk = bulk && plane % 4 == 0 && (int64_t(g.BH) * p->stride * g.Wp) % 4 == 0 &&
+               (int64_t(g.BHin) * g.Wp) % 4 == 0;
+        // the last band may copy fewer rows: Hp - row0
+        for (int b = 0; b < g.nbands && bulk; ++b) {
+            const int row0 = b * g.BH * p->stride;
+            const int rows = std::min(g.BHin, g.Hp - row0);
+            bulk = (int64_t(rows) * g.Wp) % 4 == 0;
+        }
+    }
+    g.bulk = bulk ? 1 : 0;
+    p->T = best_T;
+    p->NW = kDirectNW;
+    p->M = std::max(1, std::min(4, 32 / best_T));
+    while (p->M > 1 && p->NW * p->M > p->Kg * 2) p->M /= 2;
+    if (!direct_supported(p->T, p->M))
+        return fail(SKC_ERR_UNSUPPORTED, "no direct kernel instance for T=%d M=%d", p->T, p->M);
+    p->cblocks = (p->Kg + p->NW * p->M - 1) / (p->NW * p->M);
+    p->smem = size_t(g.NS) * stage_bytes + 2 * kMaxStages * sizeof(uint64_t);
+    return SKC_OK;
+}
+
+// Build the device image of the direct kernel: nonzero stream in perm order with offsets
+// re-encoded relative to their stage, per-(channel, chunk) pointers and the permutation.
+skc_status build_direct_image(skc_plan *p) {
+    const StageGeom &g = p->sg;
+    const int64_t nnz = int64_t(p->colidx.size());
+    std::vector<Nz> nz(static_cast<size_t>(nnz));
+    std::vector<int32_t> chunkptr(size_t(p->K) * (g.nchunks + 1));
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    int64_t pos = 0;
+    for (int kp = 0; kp < p->K; ++kp) {
+        const int k = p->perm[kp];
+        const int gk = k / p->Kg;
+        int32_t *cp = &chunkptr[size_t(kp) * (g.nchunks + 1)];
+        int chunk = 0;
+        cp[0] = int32_t(pos);
+        for (int32_t j = p->rowptr[k]; j < p->rowptr[k + 1]; ++j) {
+            const int64_t col = p->colidx[j];
+            const int c_local = int(col / plane) - gk * p->Cg;
+            const int64_t rem = col % plane;
+            const int r = int(rem / p->Wp), s = int(rem % p->Wp);
+            const int ch = c_local / g.CB, cl = c_local % g.CB;
+            while (chunk < ch) cp[++chunk] = int32_t(pos);
+            nz[size_t(pos)].w = p->values[j];
+            nz[size_t(pos)].off = int32_t((int64_t(cl) * g.BHin + r) * g.Wp + s);
+            ++pos;
+        }
+        while (chunk < g.nchunks) cp[++chunk] = int32_t(pos);
+    }
+    p->off_nz = 0;
+    p->off_chunkptr = align_up(size_t(nnz) * sizeof(Nz), 256);
+    p->off_perm = align_up(p->off_chunkptr + chunkptr.size() * 4, 256);
+    const size_t total = align_up(p->off_perm + size_t(p->K) * 4, 256);
+    p->image.assign(total, 0);
+    if (nnz) std::memcpy(p->image.data() + p->off_nz, nz.data(), size_t(nnz) * sizeof(Nz));
+    std::memcpy(p->image.data() + p->off_chunkptr, chunkptr.data(), chunkptr.size() * 4);
+    std::memcpy(p->image.data() + p->off_perm, p->perm.data(), size_t(p->K) * 4);
+    return SKC_OK;
+}
+
+bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------------------
+extern "C" {
+
+const char *skc_last_error(void) { return g_err.c_str(); }
+
+skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, int W,
+                           int stride, int pad, int groups, int kernel, skc_plan **out) {
+    if (!w || !out) return fail(SKC_ERR_ARG, "NULL weights or output pointer");
+    *out = nullptr;
+    if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_REGTILE)
+        return fail(SKC_ERR_ARG, "unknown kernel variant %d", kernel);
+    skc_status st = check_geometry(K, C, R, S, H, W, stride, pad, groups);
+    if (st != SKC_OK) return st;
+    skc_plan *p = new (std::nothrow) skc_plan();
+    if (!p) return fail(SKC_ERR_ARG, "out of host memory");
+    p->K = K; p->C = C; p->R = R; p->S = S; p->H = H; p->W = W;
+    p->stride = stride; p->pad = pad; p->groups = groups;
+    p->Hp = H + 2 * pad; p->Wp = W + 2 * pad;
+    p->Ho = (p->Hp - R) / stride + 1; p->Wo = (p->Wp - S) / stride + 1;
+    p->Kg = K / groups; p->Cg = C / groups;
+
+    // a1: canonical CSR.  Row k scans (c_local, r, s) lexicographically; because r < Hp
+    // and s < Wp the offset is strictly increasing in that order.
+    const size_t per_k = size_t(p->Cg) * R * S;
+    p->rowptr.assign(size_t(K) + 1, 0);
+    size_t nnz = 0;
+    for (int k = 0; k < K; ++k) {
+        const float *wk = w + size_t(k) * per_k;
+        for (size_t i = 0; i < per_k; ++i) {
+            if (!std::isfinite(wk[i])) {
+                delete p;
+                return fail(SKC_ERR_NONFINITE, "weight [%d][%zu] is not finite", k, i);
+            }
+            nnz += (wk[i] != 0.0f);
+        }
+        if (nnz >= (size_t(1) << 31)) {
+            delete p;
+            return fail(SKC_ERR_OVERFLOW, "nnz does not fit int32");
+        }
+        p->rowptr[size_t(k) + 1] = int32_t(nnz);
+    }
+    p->colidx.resize(nnz);
+    p->values.resize(nnz);
+    for (int k = 0; k < K; ++k) {
+        const int gk = k / p->Kg;
+        const float *wk = w + size_t(k) * per_k;
+        size_t j = size_t(p->rowptr[k]);
+        for (int cl = 0; cl < p->Cg; ++cl)
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) {
+                    const float v = wk[(size_t(cl) * R + r) * S + s];
+                    if (v == 0.0f) continue;
+                    p->colidx[j] = int32_t((int64_t(gk * p->Cg + cl) * p->Hp + r) * p->Wp + s);
+                    std::memcpy(&p->values[j], &v, 4);  // bit-exact copy
+                    ++j;
+                }
+    }
+    // nnz-sorted permutation: descending nnz, stable (ties by ascending k), per group
+    p->perm.resize(size_t(K));
+    std::iota(p->perm.begin(), p->perm.end(), 0);
+    for (int g = 0; g < groups; ++g) {
+        auto b = p->perm.begin() + ptrdiff_t(g) * p->Kg;
+        std::stable_sort(b, b + p->Kg, [p](int a, int c) {
+            return p->rowptr[a + 1] - p->rowptr[a] > p->rowptr[c + 1] - p->rowptr[c];
+        });
+    }
+
+    p->kernel = (kernel == SKC_KERNEL_AUTO) ? SKC_KERNEL_DIRECT : kernel;
+    if (p->kernel == SKC_KERNEL_REGTILE) {
+        delete p;
+        return fail(SKC_ERR_UNSUPPORTED, "register-tiled kernel not available in this build");
+    }
+    st = configure_direct(p);
+    if (st == SKC_OK) st = build_direct_image(p);
+    if (st != SKC_OK) {
+        delete p;
+        return st;
+    }
+    *out = p;
+    return ok();
+}
+
+skc_status skc_pack_csr(const float *w, int K, int C, int R, int S, int H, int W, int stride,
+                        int pad, int groups, skc_plan **out) {
+    return skc_pack_csr_ex(w, K, C, R, S, H, W, stride, pad, groups, SKC_KERNEL_AUTO, out);
+}
+
+skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
+    if (!p || !info) return fail(SKC_ERR_ARG, "NULL plan or info");
+    skc_info &i = *info;
+    i.K = p->K; i.C = p->C; i.R = p->R; i.S = p->S; i.H = p->H; i.W = p->W;
+    i.stride = p->stride; i.pad = p->pad; i.groups = p->groups;
+    i.Ho = p->Ho; i.Wo = p->Wo; i.Hp = p->Hp; i.Wp = p->Wp;
+    i.nnz = int64_t(p->colidx.size());
+    i.padded_elems_per_image = size_t(p->C) * p->Hp * p->Wp;
+    i.out_elems_per_image = size_t(p->K) * p->Ho * p->Wo;
+    i.device_bytes = p->image.size();
+    i.kernel = p->kernel;
+    i.band_rows = p->sg.BH; i.chunk_channels = p->sg.CB; i.stages = p->sg.NS;
+    i.warps = p->NW; i.channels_per_warp = p->M; i.pixels_per_lane = p->T;
+    i.smem_bytes = p->smem;
+    return ok();
+}
+
+skc_status skc_plan_csr(const skc_plan *p, const int32_t **rowptr, const int32_t **colidx,
+                        const float **values) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (rowptr) *rowptr = p->rowptr.data();
+    if (colidx) *colidx = p->colidx.data();
+    if (values) *values = p->values.data();
+    return ok();
+}
+
+skc_status skc_plan_perm(const skc_plan *p, const int32_t **perm) {
+    if (!p || !perm) return fail(SKC_ERR_ARG, "NULL plan or perm");
+    *perm = p->perm.data();
+    return ok();
+}
+
+skc_status skc_plan_upload(skc_plan *p, void *d_ws, size_t bytes, void *stream) {
+    if (!p || !d_ws) return fail(SKC_ERR_ARG, "NULL plan or workspace");
+    if (!aligned16(d_ws)) return fail(SKC_ERR_ALIGN, "workspace not 16-byte aligned");
+    if (bytes < p->image.size())
+        return fail(SKC_ERR_ARG, "workspace has %zu bytes, plan needs %zu", bytes,
+                    p->image.size());
+    cudaError_t e = cudaMemcpyAsync(d_ws, p->image.data(), p->image.size(),
+                                    cudaMemcpyHostToDevice, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
+    p->d_ws = d_ws;
+    return ok();
+}
+
+skc_status skc_pad_input(const skc_plan *p, const float *d_in, float *d_pad, int N,
+                         void *stream) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
+    if (N == 0) return ok();
+    if (!d_in || !d_pad) return fail(SKC_ERR_ARG, "NULL device pointer");
+    if (!aligned16(d_in) || !aligned16(d_pad))
+        return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
+    cudaError_t e = launch_pad(d_in, d_pad, N, p->C, p->H, p->W, p->pad, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "pad launch: %s", cudaGetErrorString(e));
+    return ok();
+}
+
+skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *d_out, int N,
+                                   void *stream) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
+    if (!p->d_ws) return fail(SKC_ERR_STATE, "plan not uploaded (call skc_plan_upload)");
+    if (N == 0) return ok();
+    if (!d_in || !d_out) return fail(SKC_ERR_ARG, "NULL device pointer");
+    if (!aligned16(d_in) || !aligned16(d_out))
+        return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
+    const uint8_t *ws = static_cast<const uint8_t *>(p->d_ws);
+    DirectParams dp{};
+    dp.g = p->sg;
+    dp.g.N = N;
+    dp.in = d_in;
+    dp.out = d_out;
+    dp.nz = reinterpret_cast<const Nz *>(ws + p->off_nz);
+    dp.chunkptr = reinterpret_cast<const int32_t *>(ws + p->off_chunkptr);
+    dp.perm = reinterpret_cast<const int32_t *>(ws + p->off_perm);
+    dp.NW = p->NW;
+    dp.M = p->M;
+    dp.cblocks = p->cblocks;
+    cudaError_t e = launch_direct(dp, p->T, p->smem, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "conv launch: %s", cudaGetErrorString(e));
+    return ok();
+}
+
+skc_status skc_forward_host(const skc_plan *p, const float *h_in, float *h_out, int N,
+                            float *d_in, float *d_pad, float *d_out, void *stream) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
+    if (N == 0) return ok();
+    if (!h_in || !h_out) return fail(SKC_ERR_ARG, "NULL host pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t in_bytes = size_t(N) * p->C * p->H * p->W * 4;
+    const size_t out_bytes = size_t(N) * p->K * p->Ho * p->Wo * 4;
+    cudaError_t e = cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "H2D: %s", cudaGetErrorString(e));
+    skc_status s = skc_pad_input(p, d_in, d_pad, N, stream);
+    if (s != SKC_OK) return s;
+    s = skc_sparse_conv_forward(p, d_pad, d_out, N, stream);
+    if (s != SKC_OK) return s;
+    e = cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "D2H: %s", cudaGetErrorString(e));
+    return ok();
+}
+
+int64_t skc_layout_offset(const skc_plan *p, int c, int y, int x) {
+    if (!p || c < 0 || c >= p->C || y < 0 || y >= p->Hp || x < 0 || x >= p->Wp) return -1;
+    return (int64_t(c) * p->Hp + y) * p->Wp + x;
+}
+
+void skc_plan_destroy(skc_plan *p) { delete p; }
+
+// ---------------------------------------------------------------------------------------
+// a7: roofline model
+// ---------------------------------------------------------------------------------------
+skc_status skc_model_layer_cost(int K, int C, int R, int S, int H, int W, int stride, int pad,
+                                int groups, int64_t batch, int amortised, skc_layer_cost *out) {
+    if (!out) return fail(SKC_ERR_ARG, "NULL output");
+    if (batch < 1) return fail(SKC_ERR_ARG, "batch < 1");
+    skc_status st = check_geometry(K, C, R, S, H, W, stride, pad, groups);
+    if (st != SKC_OK) return st;
+    const double Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - S) / stride + 1;
+    const double b = double(batch);
+    out->C = 2.0 * K * (C / groups) * R * S * Ho * Wo * b;
+    out->S_A = 4.0 * b * (double(C) * H * W + K * Ho * Wo);
+    out->S_W = 4.0 * K * (C / groups) * R * S * (amortised ? 1.0 : b);
+    return ok();
+}
+
+skc_status skc_model_project(const skc_layer_cost *c, double x, const skc_platform *pf,
+                             skc_projection *o) {
+    if (!c || !pf || !o) return fail(SKC_ERR_ARG, "NULL argument");
+    if (!(x > 0.0)) return fail(SKC_ERR_ARG, "density x must be > 0");
+    if (!(pf->F > 0) || !(pf->B > 0) || !(pf->alpha > 0))
+        return fail(SKC_ERR_ARG, "platform F, B, alpha must be > 0");
+    o->t_dense = c->C / pf->F;
+    o->t_sparse_compute = pf->alpha * x * c->C / pf->F;
+    o->t_sparse_bw = (c->S_A + pf->beta * x * c->S_W) / pf->B;
+    o->t_sparse = std::max(o->t_sparse_compute, o->t_sparse_bw);
+    o->speedup = o->t_dense / o->t_sparse;
+    o->effective_flops = c->C / o->t_sparse;
+    o->actual_flops = x * c->C / o->t_sparse;
+    return ok();
+}
+
+skc_status skc_model_window(const skc_layer_cost *c, const skc_platform *pf, skc_window *o) {
+    if (!c || !pf || !o) return fail(SKC_ERR_ARG, "NULL argument");
+    if (!(pf->F > 0) || !(pf->B > 0) || !(pf->alpha > 0))
+        return fail(SKC_ERR_ARG, "platform F, B, alpha must be > 0");
+    o->x_hi = 1.0 / pf->alpha;
+    const double denom = pf->alpha * c->C * pf->B / pf->F - pf->beta * c->S_W;
+    if (denom <= 0.0) {
+        o->x_lo = std::numeric_limits<double>::infinity();
+        o->has_speedup_potential = 0;
+        return ok();
+    }
+    o->x_lo = c->S_A / denom;
+    skc_projection pr;
+    skc_model_project(c, std::min(o->x_lo, 1.0), pf, &pr);
+    o->has_speedup_potential = (o->x_lo < o->x_hi && pr.speedup > 1.0) ? 1 : 0;
+    return ok();
+}
+
+skc_status skc_bench_ffma(void *d_scratch, int blocks, int iters, double *ms, double *flops) {
+    if (!d_scratch || !ms || !flops || blocks < 1 || iters < 1)
+        return fail(SKC_ERR_ARG, "bad micro-benchmark arguments");
+    float t = 0;
+    cudaError_t e = bench_ffma(d_scratch, blocks, iters, &t, flops);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "bench_ffma: %s", cudaGetErrorString(e));
+    *ms = t;
+    return ok();
+}
+
+skc_status skc_bench_lds(void *d_scratch, int blocks, int iters, double *ms, double *bytes) {
+    if (!d_scratch || !ms || !bytes || blocks < 1 || iters < 1)
+        return fail(SKC_ERR_ARG, "bad micro-benchmark arguments");
+    float t = 0;
+    cudaError_t e = bench_lds(d_scratch, blocks, iters, &t, bytes);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "bench_lds: %s", cudaGetErrorString(e));
+    *ms = t;
+    return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+"""CPU tests of the C-ABI library (no GPU needed): it loads, exports every symbol
+include/skc.h declares, its host packer is BIT-EXACT against the independent NumPy packer
+(oracle/ref_pack.py) on every config and on random geometries, its model agrees with the
+oracle model, and its argument/geometry errors come back as the documented statuses."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as wl
+from oracle import ref_model
+from oracle.ref_pack import ref_pack
+from paper_1608_01409_b200 import skc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1608_01409_b200 import build
+    build.build()
+    return skc.lib()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "skc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    src = re.sub(r"//.*", "", src)
+    return sorted(set(re.findall(r"\b(skc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    syms = header_symbols()
+    assert len(syms) >= 17
+    for s in syms:
+        assert hasattr(L, s), f"libskc.so does not export {s}"
+    assert sorted(skc.EXPORTS) == syms
+
+
+def assert_pack_equal(plan, ref):
+    rp, ci, va = plan.csr()
+    np.testing.assert_array_equal(rp, ref["rowptr"])
+    np.testing.assert_array_equal(ci, ref["colidx"])
+    np.testing.assert_array_equal(va.view(np.uint32), ref["values"].view(np.uint32))
+    np.testing.assert_array_equal(plan.perm(), ref["perm"])
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
+def test_pack_bit_exact_configs(L, cfg_id):
+    """P-P6 on every BASELINE config layer (config 5 uses config 2's layers)."""
+    cfg = wl.CONFIGS[cfg_id]
+    for li, layer in enumerate(cfg.layers):
+        w = wl.gen_weights(cfg_id, li, layer)
+        plan = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups)
+        assert_pack_equal(plan, ref_pack(w, layer.H, layer.W, layer.pad, layer.groups))
+        info = plan.info()
+        assert info["nnz"] == np.count_nonzero(w)
+        assert (info["Ho"], info["Wo"]) == (layer.Ho, layer.Wo)
+
+
+def test_pack_bit_exact_random(L):
+    """P-P6: 1000 random geometries incl. groups, empty rows, signed zeros, strides."""
+    rng = np.random.default_rng(7)
+    for it in range(1000):
+        layer = wl.random_layer(rng, max_c=12, groups=(1, 2, 3, 4))
+        w, _ = wl.random_tensors(rng, layer, 1)
+        if it % 7 == 0:
+            w[rng.random(w.shape) < 0.5] = -0.0
+        plan = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups)
+        assert_pack_equal(plan, ref_pack(w, layer.H, layer.W, layer.pad, layer.groups))
+
+
+def test_layout_offset_hook(L):
+    """SPEC.md:49-51 through the C-ABI test hook, plus out-of-range = -1."""
+    plan = skc.skc_pack_csr(np.ones((1, 2, 1, 1), np.float32), 3, 3, 1, 0, 1)
+    assert skc.skc_layout_offset(plan, 1, 2, 1) == 16
+    assert skc.skc_layout_offset(plan, 0, 0, 0) == 0
+    assert skc.skc_layout_offset(plan, 2, 0, 0) == -1
+    plan = skc.skc_pack_csr(np.ones((1, 2, 1, 1), np.float32), 3, 3, 1, 1, 1)  # Hp=Wp=5
+    assert skc.skc_layout_offset(plan, 1, 4, 4) == (1 * 5 + 4) * 5 + 4
+    assert skc.skc_layout_offset(plan, 0, 5, 0) == -1
+
+
+def test_errors(L):
+    w = np.ones((4, 2, 3, 3), np.float32)
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pack_csr(w, 5, 5, 1, 1, groups=3)       # K, C not divisible by 3
+    assert e.value.status == -2
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pack_csr(w, 1, 1, 1, 0, 1)              # 3x3 kernel on 1x1 input, no pad
+    assert e.value.status == -2
+    bad = w.copy(); bad[1, 0, 2, 2] = np.nan
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pack_csr(bad, 5, 5, 1, 1, 1)
+    assert e.value.status == -3
+    bad[1, 0, 2, 2] = np.inf
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pack_csr(bad, 5, 5, 1, 1, 1)
+    assert e.value.status == -3
+    with pytest.raises(skc.SkcError) as e:                # C*Hp*Wp >= 2^31
+        skc.skc_pack_csr(np.ones((1, 1, 1, 1), np.float32), 50000, 50000, 1, 0, 1)
+    assert e.value.status == -4
+    plan = skc.skc_pack_csr(w, 5, 5, 1, 1, 1)
+    # forward before upload -> STATE; negative N -> ARG (both before any CUDA call)
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_sparse_conv_forward(plan, 16, 16, 1, 0)
+    assert e.value.status == -7
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_sparse_conv_forward(plan, 16, 16, -1, 0)
+    assert e.value.status == -1
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pad_input(plan, 16, 16, -2, 0)
+    assert e.value.status == -1
+    skc.skc_pad_input(plan, 0, 0, 0, 0)                  # N = 0 is a no-op
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pad_input(plan, 8, 16, 1, 0)             # misaligned device pointer
+    assert e.value.status == -6
+
+
+def test_plan_info_configuration(L):
+    """The direct kernel's tiling for the AlexNet layers: full-image slabs staged with TMA."""
+    for li, layer in enumerate(wl.ALEXNET):
+        w = wl.gen_weights(2, li, layer)
+        info = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups).info()
+        assert info["kernel"] == skc.SKC_KERNEL_DIRECT
+        assert info["smem_bytes"] <= 227 * 1024
+        assert info["pixels_per_lane"] * 32 * -(-layer.Ho // info["band_rows"]) >= layer.Ho * layer.Wo
+
+
+@pytest.mark.parametrize("li", range(4))
+def test_model_matches_oracle_model(L, li):
+    """a7: the C++ model equals the oracle model (both written from PAPER.md Sec. 2.2)."""
+    layer = wl.ALEXNET[li]
+    g = layer.geometry()
+    for batch, am in [(1, False), (256, False), (256, True)]:
+        c = skc.skc_model_layer_cost(**g, batch=batch, amortised=am)
+        r = ref_model.layer_cost(**g, batch=batch, amortised=am)
+        assert c == pytest.approx(r, rel=1e-15)
+        for F, B, a in [(2.15e12, 1.22e11, 3.0), (6.2e10, 1.5e10, 1.2), (6e13, 6.5e12, 4.0)]:
+            for x in (0.01, 0.07, 0.3, 1.0):
+                p = skc.skc_model_project(c, x, F, B, a)
+                q = ref_model.project(r, x, F, B, a)
+                for key in q:
+                    assert p[key] == pytest.approx(q[key], rel=1e-13), key
+            wc, wr = skc.skc_model_window(c, F, B, a), ref_model.window(r, F, B, a)
+            assert wc["x_hi"] == pytest.approx(wr["x_hi"]) and wc["x_lo"] == pytest.approx(wr["x_lo"])
+            assert wc["has_speedup_potential"] == wr["has_speedup_potential"]

@@ -1,0 +1,195 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs.  Tolerance (BASELINE.json north_star): per output element
+|gpu - oracle| <= 1e-4 * sum|w*x|, and exactly 0 where that sum is 0.  Packing is bit-exact
+(tests/test_abi.py); the pad kernel is bitwise equal to numpy.pad."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+from paper_1608_01409_b200 import skc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1608_01409_b200 import build
+    build.build()
+    skc.lib()
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+
+def run_gpu(w, x, layer, kernel=skc.SKC_KERNEL_AUTO, xp_out=False):
+    conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                       layer.groups, kernel)
+    xd = torch.from_numpy(x).cuda()
+    xp = torch.empty(conv.padded_shape(x.shape[0]), device="cuda")
+    out = conv.forward(xd, xp=xp)
+    torch.cuda.synchronize()
+    if xp_out:
+        return out.cpu().numpy(), xp.cpu().numpy(), conv
+    return out.cpu().numpy(), conv
+
+
+def check(out, ref, bound, what=""):
+    assert out.shape == ref.shape, (what, out.shape, ref.shape)
+    err = np.abs(out.astype(np.float64) - ref)
+    zero = bound == 0
+    assert np.all(out[zero] == 0), f"{what}: nonzero where sum|wx| = 0"
+    ratio = np.where(zero, 0.0, err / np.where(zero, 1.0, bound))
+    worst = float(ratio.max()) if ratio.size else 0.0
+    assert worst <= TOL, f"{what}: max err/sum|wx| = {worst:.3e}"
+    return worst
+
+
+def test_pad_bitwise_numpy():
+    """a2 vs the library routine numpy.pad, ragged sizes and pads."""
+    rng = np.random.default_rng(0)
+    for (N, C, H, W, p) in [(1, 1, 1, 1, 1), (3, 5, 7, 9, 2), (2, 96, 27, 27, 2), (4, 256, 13, 13, 1),
+                            (2, 3, 5, 4, 0), (1, 64, 56, 56, 1), (65, 2, 3, 3, 3)]:
+        x = rng.standard_normal((N, C, H, W), dtype=np.float32)
+        x[0, 0, 0, 0] = -0.0
+        layer = wl.Layer("p", 1, C, H, W, 1, 1, 1, p, 1, 0.0, 1.0)
+        plan = skc.skc_pack_csr(np.ones((1, C, 1, 1), np.float32), H, W, 1, p, 1)
+        xd = torch.from_numpy(x).cuda()
+        xp = torch.full((N, C, H + 2 * p, W + 2 * p), float("nan"), device="cuda")
+        skc.skc_pad_input(plan, xd, xp, N)
+        torch.cuda.synchronize()
+        got = xp.cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint32), oracle.pad_ref(x, p).view(np.uint32))
+        del layer
+
+
+def test_worked_example_gpu(golden_dir):
+    import json, os
+    g = json.load(open(os.path.join(golden_dir, "worked_example_conv.json")))
+    x = np.array(g["input_1x1x3x3"], np.float32)
+    w = np.array(g["weight_1x1x2x2"], np.float32)
+    for case in g["cases"]:
+        layer = wl.Layer("we", 1, 1, 3, 3, 2, 2, 1, case["pad"], 1, 0.0, 1.0)
+        out, _ = run_gpu(w, x, layer)
+        np.testing.assert_array_equal(out, np.array(case["out"], np.float32))
+
+
+def test_random_geometries():
+    """SPEC.md:159-163 property suite ranges (+ groups, stride 2): >= 200 random layers."""
+    rng = np.random.default_rng(1)
+    worst = 0.0
+    for it in range(220):
+        layer = wl.random_layer(rng, max_c=32, max_hw=16, rs=(1, 2, 3, 5), groups=(1, 2, 4))
+        N = int(rng.integers(1, 4))
+        w, x = wl.random_tensors(rng, layer, N)
+        out, _ = run_gpu(w, x, layer)
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        worst = max(worst, check(out, ref, bound, f"it{it} {layer}"))
+    print("max err/bound", worst)
+
+
+def test_tiles_and_ragged_tails():
+    """Shapes spanning several channel blocks, stages, bands and lane tails."""
+    rng = np.random.default_rng(2)
+    cases = [
+        wl.Layer("a", 40, 36, 13, 13, 3, 3, 1, 1, 1, 0.9, 1.0),     # K not multiple of 32
+        wl.Layer("b", 70, 50, 27, 27, 5, 5, 1, 2, 2, 0.85, 1.0),    # odd C/g, 2 bands
+        wl.Layer("c", 33, 17, 31, 29, 3, 3, 2, 1, 1, 0.5, 1.0),     # stride 2
+        wl.Layer("d", 64, 64, 56, 56, 3, 3, 1, 1, 1, 0.7, 1.0),     # many bands
+        wl.Layer("e", 24, 96, 7, 7, 3, 3, 1, 1, 1, 0.7, 1.0),       # 49 pixels, tiny T
+        wl.Layer("f", 16, 8, 40, 3, 3, 3, 1, 1, 1, 0.5, 1.0),       # tall and narrow
+        wl.Layer("g", 8, 4, 5, 70, 1, 7, 1, 3, 1, 0.3, 1.0),        # wide rows, 1x7 kernel
+    ]
+    for layer in cases:
+        w, x = wl.random_tensors(rng, layer, 3)
+        out, conv = run_gpu(w, x, layer)
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        check(out, ref, bound, f"{layer} {conv.geom}")
+
+
+def test_edge_cases():
+    rng = np.random.default_rng(3)
+    layer = wl.Layer("z", 20, 12, 9, 9, 3, 3, 1, 1, 2, 0.0, 1.0)
+    _, x = wl.random_tensors(rng, layer, 2)
+    # all-zero weights -> exactly zero output
+    out, _ = run_gpu(np.zeros((20, 6, 3, 3), np.float32), x, layer)
+    assert not out.any()
+    # single nonzero weight
+    w = np.zeros((20, 6, 3, 3), np.float32)
+    w[13, 4, 0, 2] = 1.5
+    out, _ = run_gpu(w, x, layer)
+    ref, bound = oracle.conv2d_fp64(x, w, 1, 1, 2)
+    check(out, ref, bound, "single nnz")
+    # some channels with nnz = 0 among dense ones, x = 1
+    w = rng.standard_normal((20, 6, 3, 3)).astype(np.float32)
+    w[[0, 5, 19]] = 0
+    out, _ = run_gpu(w, x, layer)
+    ref, bound = oracle.conv2d_fp64(x, w, 1, 1, 2)
+    check(out, ref, bound, "empty rows")
+    # N = 0 is a no-op
+    conv = skc.SparseConv2d.from_dense(w, 9, 9, 1, 1, 2)
+    skc.skc_sparse_conv_forward(conv.plan, 0, 0, 0)
+
+
+def test_dense_equals_torch_conv2d_fp32():
+    """P-O7: at 0% sparsity the sparse path equals torch conv2d in FP32 (TF32 off)."""
+    rng = np.random.default_rng(4)
+    layer = wl.Layer("d", 48, 32, 13, 13, 3, 3, 1, 1, 2, 0.0, 1.0)
+    w, x = wl.random_tensors(rng, layer, 4)
+    out, _ = run_gpu(w, x, layer)
+    ref, bound = oracle.conv2d_fp64(x, w, 1, 1, 2)
+    check(out, ref, bound, "dense")
+    t = torch.nn.functional.conv2d(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(),
+                                   padding=1, groups=2).cpu().numpy()
+    check(t, ref, bound, "torch fp32")  # the library routine passes the same bar
+    assert np.max(np.abs(out - t) / np.maximum(bound, 1e-30)) <= 2 * TOL
+
+
+def test_determinism_and_host_path():
+    rng = np.random.default_rng(5)
+    layer = wl.CONFIGS[2].layers[1]
+    w = wl.gen_weights(2, 1, layer)
+    x = wl.gen_input(2, 1, layer, 0, 8)
+    conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups)
+    xd = torch.from_numpy(x).cuda()
+    a = conv.forward(xd).cpu().numpy()
+    b = conv.forward(xd).cpu().numpy()
+    np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+    # end-to-end host-buffer entry point gives the same bits
+    h_in = torch.from_numpy(x).pin_memory()
+    h_out = torch.empty(conv.out_shape(8)).pin_memory()
+    d_in = torch.empty_like(xd)
+    d_pad = torch.empty(conv.padded_shape(8), device="cuda")
+    d_out = torch.empty(conv.out_shape(8), device="cuda")
+    skc.skc_forward_host(conv.plan, h_in, h_out, 8, d_in, d_pad, d_out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(h_out.numpy().view(np.uint32), a.view(np.uint32))
+    del rng
+
+
+def sample_images(N, rng, k):
+    idx = {0, N - 1}
+    while len(idx) < min(k, N):
+        idx.add(int(rng.integers(0, N)))
+    return sorted(idx)
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
+def test_config_parity(cfg_id):
+    """Every BASELINE config layer at its full batch on the GPU, in the launch configuration
+    bench.py times; the oracle checks a seeded sample of images (always first and last)."""
+    cfg = wl.CONFIGS[cfg_id]
+    rng = np.random.default_rng(100 + cfg_id)
+    for li, layer in enumerate(cfg.layers):
+        w = wl.gen_weights(cfg_id, li, layer)
+        x = wl.gen_input(cfg_id, li, layer, 0, cfg.batch)
+        out, conv = run_gpu(w, x, layer)
+        k = 4 if cfg_id != 3 else 2
+        for n in sample_images(cfg.batch, rng, k):
+            ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
+            check(out[n:n + 1], ref, bound, f"cfg{cfg_id} {layer.name} image {n}")
+        assert np.isfinite(out).all()
