@@ -73,6 +73,7 @@ typedef struct {
     int kernel;                    /* skc_kernel chosen (after AUTO resolution)         */
     int band_rows, chunk_channels, stages, warps, channels_per_warp, pixels_per_lane;
     size_t smem_bytes;             /* dynamic shared memory per CTA of the conv kernel  */
+    int lane_mapping;              /* direct kernel: 0 = output pixels, 1 = padded pitch  */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).

@@ -56,7 +56,7 @@ struct skc_plan {
     // kernel choice + configuration
     int kernel = SKC_KERNEL_DIRECT;
     StageGeom sg{};
-    int T = 0, NW = 0, M = 0, cblocks = 0;
+    int T = 0, NW = 0, M = 0, cblocks = 0, pitch = 0;
     size_t smem = 0;
 
     // device image (bytes uploaded verbatim) and the offsets of its arrays
@@ -68,7 +68,7 @@ struct skc_plan {
 
 namespace {
 
-const int kDirectT[] = {2, 4, 6, 8, 12, 16};
+const int kDirectT[] = {2, 4, 6, 7, 8, 12, 14, 16};
 constexpr int kDirectNW = 8;              // compute warps per CTA (+1 producer warp)
 constexpr size_t kStageTarget = 24 << 10;  // bytes per stage we aim for
 constexpr size_t kSmemBudget = 112 << 10;  // per CTA, so that >= 2 CTAs fit an SM
@@ -92,26 +92,65 @@ skc_status check_geometry(int K, int C, int R, int S, int H, int W, int stride, 
     return SKC_OK;
 }
 
-// Pick the direct kernel's band height, pixels per lane, channel chunk and warp layout.
+// Shared-memory wavefronts one warp needs for its T loads of one nonzero (per band), for
+// the natural output-pixel lane mapping: per t, the max number of DISTINCT words that fall
+// in one of the 32 banks (same-word lanes broadcast).
+int natural_wavefronts(int BHcur, int Wo, int Wp, int stride, int T) {
+    int total = 0;
+    const int npix = BHcur * Wo;
+    for (int t = 0; t < T; ++t) {
+        int words[32];
+        for (int l = 0; l < 32; ++l) {
+            const int px = t * 32 + l;
+            words[l] = px < npix ? (px / Wo) * stride * Wp + (px % Wo) * stride : 0;
+        }
+        int worst = 1;
+        for (int b = 0; b < 32; ++b) {
+            int distinct[32], nd = 0;
+            for (int l = 0; l < 32; ++l) {
+                if (((words[l] % 32) + 32) % 32 != b) continue;
+                bool seen = false;
+                for (int i = 0; i < nd; ++i) seen |= distinct[i] == words[l];
+                if (!seen) distinct[nd++] = words[l];
+            }
+            worst = std::max(worst, nd);
+        }
+        total += worst;
+    }
+    return total;
+}
+
+// Pick the direct kernel's lane mapping, band height, pixels per lane, channel chunk and
+// warp layout.  Cost per nonzero per image = shared-memory wavefronts of the T loads of
+// every band + 2 shuffles per band; the cheapest candidate wins (ties: fewer bands).
 skc_status configure_direct(skc_plan *p) {
     const int Ho = p->Ho, Wo = p->Wo;
-    // (1) bands x pixels-per-lane: maximise lane utilisation Ho*Wo / (nb*32*T)
-    double best_util = -1;
-    int best_nb = 0, best_T = 0;
-    for (int nb = 1; nb <= Ho; ++nb) {
-        const int BH = (Ho + nb - 1) / nb;
-        if ((Ho + BH - 1) / BH != nb) continue;  // same BH as a smaller nb
-        const int need = (BH * Wo + 31) / 32;
-        int T = 0;
-        for (int t : kDirectT)
-            if (t >= need) { T = t; break; }
-        if (!T) continue;
-        const double util = double(Ho) * Wo / (double(nb) * 32 * T);
-        if (util > best_util + 1e-9) { best_util = util; best_nb = nb; best_T = T; }
+    double best_cost = 1e300;
+    int best_nb = 0, best_T = 0, best_pitch = 0;
+    for (int pitch = 0; pitch <= (p->stride == 1 ? 1 : 0); ++pitch) {
+        for (int nb = 1; nb <= Ho; ++nb) {
+            const int BH = (Ho + nb - 1) / nb;
+            if ((Ho + BH - 1) / BH != nb) continue;  // same BH as a smaller nb
+            const int slots = BH * (pitch ? p->Wp : Wo);
+            const int need = (slots + 31) / 32;
+            int T = 0;
+            for (int t : kDirectT)
+                if (t >= need) { T = t; break; }
+            if (!T) continue;
+            double cost = 0;
+            for (int b = 0; b < nb; ++b) {
+                const int cur = std::min(BH, Ho - b * BH);
+                cost += 2 + (pitch ? T : natural_wavefronts(cur, Wo, p->Wp, p->stride, T));
+            }
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost; best_nb = nb; best_T = T; best_pitch = pitch;
+            }
+        }
     }
     if (!best_T)
         return fail(SKC_ERR_UNSUPPORTED, "no band fits (Wo=%d too wide for the direct kernel)",
                     Wo);
+    p->pitch = best_pitch;
     StageGeom &g = p->sg;
     g.C = p->C; g.K = p->K; g.Kg = p->Kg; g.Cg = p->Cg; g.Hp = p->Hp; g.Wp = p->Wp;
     g.Ho = Ho; g.Wo = Wo; g.stride = p->stride;
@@ -157,7 +196,10 @@ skc_status configure_direct(skc_plan *p) {
     if (!direct_supported(p->T, p->M))
         return fail(SKC_ERR_UNSUPPORTED, "no direct kernel instance for T=%d M=%d", p->T, p->M);
     p->cblocks = (p->Kg + p->NW * p->M - 1) / (p->NW * p->M);
-    p->smem = size_t(g.NS) * stage_bytes + 2 * kMaxStages * sizeof(uint64_t);
+    // padded-pitch lane slots beyond the band read up to T*32 words past the last channel
+    g.tail_floats = p->pitch ? int(align_up(size_t(p->T) * 32, 4)) : 0;
+    p->smem = size_t(g.NS) * stage_bytes + size_t(g.tail_floats) * 4 +
+              2 * kMaxStages * sizeof(uint64_t);
     return SKC_OK;
 }
 
@@ -307,6 +349,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.band_rows = p->sg.BH; i.chunk_channels = p->sg.CB; i.stages = p->sg.NS;
     i.warps = p->NW; i.channels_per_warp = p->M; i.pixels_per_lane = p->T;
     i.smem_bytes = p->smem;
+    i.lane_mapping = p->pitch;
     return ok();
 }
 
@@ -372,7 +415,7 @@ skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *
     dp.NW = p->NW;
     dp.M = p->M;
     dp.cblocks = p->cblocks;
-    cudaError_t e = launch_direct(dp, p->T, p->smem, (cudaStream_t)stream);
+    cudaError_t e = launch_direct(dp, p->T, p->pitch != 0, p->smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "conv launch: %s", cudaGetErrorString(e));
     return ok();
 }

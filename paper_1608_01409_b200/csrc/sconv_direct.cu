@@ -14,10 +14,16 @@
 //     nnz-sorted channels balance); for each stage it walks its channels' nonzeros of that
 //     channel block, 32 at a time: one coalesced 8-byte load of {w, off} per lane, then the
 //     pair is broadcast with __shfl_sync (reused for every pixel).
-//   - a5: each lane keeps T output pixels of the band in registers (pixel p = t*32 + lane,
-//     so a warp touches 32 consecutive output pixels per t) and performs
+//   - a5: each lane keeps T output pixels of the band in registers and performs
 //     acc[t] = fma(w, stage[off + q_t], acc[t]), q_t = (y*stride)*Wp + x*stride -- exactly
 //     in[off + f(0,y,x)] of Fig. 2, in shared memory.  One shared-memory word per MAC.
+//     Two lane mappings (chosen per shape by plan.cpp's bank-conflict model):
+//       PITCH = false: pixel p = t*32 + lane over the Ho x Wo outputs (no junk lanes, but
+//                      32 consecutive outputs can span > 32 words -> 2-way bank conflicts);
+//       PITCH = true : (stride 1) lane slot p = t*32 + lane over the band in PADDED-row
+//                      coordinates, q_t = p: 32 consecutive words, conflict-free, and the
+//                      T loads use immediate offsets t*128 B; x >= Wo slots are junk (never
+//                      stored).
 //   - a6: coalesced stores of the band rows into out[n][k][y][x] (original channel index).
 // Accumulation order per output element: CSR order (c ascending, then r, s), fixed ->
 // results are bitwise deterministic.
@@ -29,11 +35,12 @@ namespace {
 
 constexpr int kFull = 0xffffffff;
 
-template <int T, int M>
+template <int T, int M, bool PITCH>
 __global__ void __launch_bounds__(288, 1) sconv_direct_kernel(const DirectParams p) {
     extern __shared__ __align__(128) float smem[];
     const StageGeom &g = p.g;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + size_t(g.NS) * g.stage_floats);
+    uint64_t *full =
+        reinterpret_cast<uint64_t *>(smem + size_t(g.NS) * g.stage_floats + g.tail_floats);
     uint64_t *empty = full + kMaxStages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NW = p.NW;
@@ -103,12 +110,14 @@ __global__ void __launch_bounds__(288, 1) sconv_direct_kernel(const DirectParams
 
     // ---------------- compute warps ----------------
     const int npix = BHcur * g.Wo;
-    int q[T];
+    int q[PITCH ? 1 : T];
+    if constexpr (!PITCH) {
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-        const int px = t * 32 + lane;
-        const int yl = px / g.Wo, x = px - yl * g.Wo;
-        q[t] = (px < npix) ? (yl * g.stride * g.Wp + x * g.stride) : 0;
+        for (int t = 0; t < T; ++t) {
+            const int px = t * 32 + lane;
+            const int yl = px / g.Wo, x = px - yl * g.Wo;
+            q[t] = (px < npix) ? (yl * g.stride * g.Wp + x * g.stride) : 0;
+        }
     }
     float acc[M][T];
 #pragma unroll
@@ -140,9 +149,17 @@ __global__ void __launch_bounds__(288, 1) sconv_direct_kernel(const DirectParams
                     for (int j = 0; j < cnt; ++j) {
                         const float w = __int_as_float(__shfl_sync(kFull, pr.x, j));
                         const int off = __shfl_sync(kFull, pr.y, j);
-                        const float *base = sm + off;
+                        if constexpr (PITCH) {
+                            const float *base = sm + off + lane;
 #pragma unroll
-                        for (int t = 0; t < T; ++t) acc[m][t] = fmaf(w, base[q[t]], acc[m][t]);
+                            for (int t = 0; t < T; ++t)
+                                acc[m][t] = fmaf(w, base[t * 32], acc[m][t]);
+                        } else {
+                            const float *base = sm + off;
+#pragma unroll
+                            for (int t = 0; t < T; ++t)
+                                acc[m][t] = fmaf(w, base[q[t]], acc[m][t]);
+                        }
                     }
                 }
             }
@@ -160,16 +177,21 @@ __global__ void __launch_bounds__(288, 1) sconv_direct_kernel(const DirectParams
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 const int px = t * 32 + lane;
-                if (px < npix) o[px] = acc[m][t];
+                if constexpr (PITCH) {
+                    const int yl = px / g.Wp, x = px - yl * g.Wp;
+                    if (yl < BHcur && x < g.Wo) o[yl * g.Wo + x] = acc[m][t];
+                } else {
+                    if (px < npix) o[px] = acc[m][t];
+                }
             }
         }
     }
 }
 
-template <int T, int M>
+template <int T, int M, bool PITCH>
 cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
     static bool attr_set = false;
-    auto fn = sconv_direct_kernel<T, M>;
+    auto fn = sconv_direct_kernel<T, M, PITCH>;
     if (!attr_set) {
         cudaError_t e =
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -183,9 +205,9 @@ cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-#define SKC_DIRECT_CASES(X) \
-    X(2, 1) X(2, 2) X(2, 4) X(4, 1) X(4, 2) X(4, 4) X(6, 1) X(6, 2) X(6, 4) \
-    X(8, 1) X(8, 2) X(8, 4) X(12, 1) X(12, 2) X(16, 1) X(16, 2)
+#define SKC_DIRECT_CASES(X)                                                              \
+    X(2, 1) X(2, 2) X(2, 4) X(4, 1) X(4, 2) X(4, 4) X(6, 1) X(6, 2) X(6, 4) X(7, 1) X(7, 2) \
+    X(7, 4) X(8, 1) X(8, 2) X(8, 4) X(12, 1) X(12, 2) X(14, 1) X(14, 2) X(16, 1) X(16, 2)
 
 }  // namespace
 
@@ -196,9 +218,12 @@ bool direct_supported(int T, int M) {
     return false;
 }
 
-cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st) {
+cudaError_t launch_direct(const DirectParams &p, int T, bool pitch, size_t smem,
+                          cudaStream_t st) {
     if (p.NW != 8) return cudaErrorInvalidValue;
-#define X(t, m) if (T == t && p.M == m) return launch_tm<t, m>(p, smem, st);
+#define X(t, m)                                                      \
+    if (T == t && p.M == m)                                          \
+        return pitch ? launch_tm<t, m, true>(p, smem, st) : launch_tm<t, m, false>(p, smem, st);
     SKC_DIRECT_CASES(X)
 #undef X
     return cudaErrorInvalidValue;

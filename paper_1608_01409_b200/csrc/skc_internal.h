@@ -30,6 +30,7 @@ struct StageGeom {
     int nchunks;    // ceil(Cg / CB)
     int NS;         // stages in the ring
     int stage_floats;  // floats per stage (multiple of 4)
+    int tail_floats;   // slack after the last stage: junk lane slots may read past a stage
     int bulk;       // 1: cp.async.bulk (TMA) staging; 0: LSU copy fallback
     int whole;      // 1: band covers all Hp rows -> one bulk copy per stage
 };
@@ -49,7 +50,8 @@ struct DirectParams {
 // Launchers (defined in the .cu files).  Return cudaError_t of the launch.
 cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int W, int pad,
                        cudaStream_t st);
-cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st);
+cudaError_t launch_direct(const DirectParams &p, int T, bool pitch, size_t smem,
+                          cudaStream_t st);
 bool direct_supported(int T, int M);
 cudaError_t bench_ffma(void *scratch, int blocks, int iters, float *ms, double *flops);
 cudaError_t bench_lds(void *scratch, int blocks, int iters, float *ms, double *bytes);
