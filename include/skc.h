@@ -74,6 +74,8 @@ typedef struct {
     int band_rows, chunk_channels, stages, warps, channels_per_warp, pixels_per_lane;
     size_t smem_bytes;             /* dynamic shared memory per CTA of the conv kernel  */
     int lane_mapping;              /* direct kernel: 0 = output pixels, 1 = padded pitch  */
+    int tile_h, tile_w;            /* regtile kernel: register tile per lane (0: direct)  */
+    int images_per_cta;            /* images staged together in one CTA                   */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).

@@ -19,8 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include"),
           "-I", CSRC]
-SOURCES = ["plan.cpp", "pad.cu", "sconv_direct.cu", "microbench.cu"]
-HEADERS = ["skc_internal.h", "ptx.cuh"]
+SOURCES = ["plan.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu"]
+HEADERS = ["skc_internal.h", "ptx.cuh", "regtile_gen.inc"]
 
 
 def _newer(target: str, deps) -> bool:

@@ -59,9 +59,14 @@ struct skc_plan {
     int T = 0, NW = 0, M = 0, cblocks = 0, pitch = 0;
     size_t smem = 0;
 
+    // register-tiled kernel configuration (kernel == SKC_KERNEL_REGTILE)
+    RegtileParams rp{};
+    RegtileShape rsh{};
+
     // device image (bytes uploaded verbatim) and the offsets of its arrays
     std::vector<uint8_t> image;
     size_t off_nz = 0, off_chunkptr = 0, off_perm = 0;
+    size_t off_stream = 0, off_segoff = 0, off_chan = 0, off_lanemap = 0;
 
     void *d_ws = nullptr;  // set by skc_plan_upload
 };
@@ -242,6 +247,259 @@ skc_status build_direct_image(skc_plan *p) {
     return SKC_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// Register-tiled kernel: configuration and op streams (see sconv_regtile.cu)
+// ---------------------------------------------------------------------------------------
+constexpr int kRtMaxWarps = 12;            // 384 threads at <= 168 registers per thread
+constexpr int kRtRegs = 168;
+constexpr size_t kRtStageTarget = 24 << 10;
+constexpr int kRtStages = 3;
+
+// Shared-memory conflict degree of one warp-wide load whose lane addresses are `addr`
+// (words; -1 = inactive lane reading word 0): max number of distinct words in one bank.
+int conflict_degree(const std::vector<int> &addr) {
+    int worst = 1;
+    for (int b = 0; b < 32; ++b) {
+        std::vector<int> d;
+        for (int a : addr) {
+            const int w = a < 0 ? 0 : a;
+            if ((w & 31) == b && std::find(d.begin(), d.end(), w) == d.end()) d.push_back(w);
+        }
+        worst = std::max(worst, int(d.size()));
+    }
+    return worst;
+}
+
+struct RtCandidate {
+    RegtileShape sh{};
+    int NI = 0, NG = 0, NT = 0, nblocks = 0, CB = 0, NS = 0, img_stride = 0, wf = 1;
+    int ctas_per_sm = 1;
+    std::vector<int32_t> lanemap;
+    double cost = 1e300;
+};
+
+// c-groups (HDR entries) of a task = distinct input channels among its M channels.
+int64_t task_groups(const skc_plan *p, int g, int task, int M) {
+    std::vector<char> seen(size_t(p->Cg), 0);
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    int64_t n = 0;
+    for (int m = 0; m < M; ++m) {
+        const int lp = task * M + m;
+        if (lp >= p->Kg) break;
+        const int k = p->perm[size_t(g) * p->Kg + lp];
+        for (int32_t j = p->rowptr[k]; j < p->rowptr[k + 1]; ++j) {
+            const int cl = int(p->colidx[j] / plane) - g * p->Cg;
+            if (!seen[size_t(cl)]) { seen[size_t(cl)] = 1; ++n; }
+        }
+    }
+    return n;
+}
+
+bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c) {
+    if (p->stride != 1 || sh.R != p->R || sh.S != p->S) return false;
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    if ((int64_t(p->C) * plane) % 4 || (int64_t(p->Cg) * plane) % 4) return false;
+    const int nty = (p->Ho + sh.TY - 1) / sh.TY, ntx = (p->Wo + sh.TX - 1) / sh.TX;
+    const int tiles = nty * ntx;
+    if (ntx > 4096 || nty * sh.TY > 4095) return false;
+    c.sh = sh;
+    c.NI = tiles >= 32 ? 1 : std::max(1, 32 / tiles);
+    const int total = c.NI * tiles;
+    c.NG = (total + 31) / 32;
+    if (c.NG > kRtMaxWarps) return false;
+    // channels per stage: input slab of NI images + the op stream of up to 12 tasks of M
+    // channels (8 B per nonzero), aiming at kRtStageTarget bytes; CB*plane must keep image
+    // slots 16-byte aligned
+    const double density = double(p->colidx.size()) / (double(p->K) * p->Cg * p->R * p->S);
+    const double chan_bytes = double(c.NI) * double(plane) * 4.0 +
+                              8.0 * (kRtMaxWarps * (sh.M * sh.R * sh.S * density + 1.0));
+    int CB = int(std::max(1.0, double(kRtStageTarget) / chan_bytes));
+    CB = std::min(CB, p->Cg);
+    while (CB > 1 && (int64_t(CB) * plane) % 4) --CB;
+    if ((int64_t(CB) * plane) % 4) {
+        CB = 4;  // plane odd: 4 channels always align
+        if (CB > p->Cg) return false;
+    }
+    if (p->Cg % CB && ((int64_t(p->Cg % CB) * plane) % 4)) return false;  // last chunk copy
+    c.CB = CB;
+    // lane map: tiles in (image, tile-row, tile-col) order, 32 per lane group
+    c.lanemap.assign(size_t(c.NG) * 32, -1);
+    for (int i = 0; i < total; ++i) {
+        const int img = i / tiles, rem = i % tiles;
+        const int y0 = (rem / ntx) * sh.TY, x0 = (rem % ntx) * sh.TX;
+        c.lanemap[size_t(i)] = (img << 24) | (y0 << 12) | x0;
+    }
+    // image-slot stride: pad (multiple of 4 words) that minimises window-load bank conflicts
+    const int base = int(align_up(size_t(CB) * size_t(plane), 4));
+    int best_pad = 0, best_wf = 1 << 30;
+    for (int pad = 0; pad < 32; pad += 4) {
+        int wf = 0;
+        for (int g = 0; g < c.NG; ++g) {
+            std::vector<int> addr(32);
+            for (int l = 0; l < 32; ++l) {
+                const int lm = c.lanemap[size_t(g) * 32 + l];
+                addr[l] = lm < 0 ? -1
+                                 : (lm >> 24) * (base + pad) + ((lm >> 12) & 0xfff) * p->Wp +
+                                       (lm & 0xfff);
+            }
+            wf = std::max(wf, conflict_degree(addr));
+        }
+        if (wf < best_wf) { best_wf = wf; best_pad = pad; }
+        if (c.NI == 1) break;  // a single image slot: padding cannot help
+    }
+    c.img_stride = base + best_pad;
+    c.wf = best_wf;
+    // tasks per CTA: keep ~12 warps resident per SM, fill the last block, and prefer more
+    // tasks per CTA (each CTA re-reads its images' slabs: fewer blocks, less L2 traffic)
+    const int tasks = (p->Kg + sh.M - 1) / sh.M;
+    double best = -1;
+    for (int NT = std::min(kRtMaxWarps / c.NG, tasks); NT >= 1; --NT) {
+        const int nb = (tasks + NT - 1) / NT;
+        const int warps = c.NG * NT;
+        const int by_regs = 65536 / (warps * 32 * kRtRegs);
+        if (by_regs < 1) continue;
+        const int resident = std::min(kRtMaxWarps, warps * std::min(by_regs, 2));
+        const double fill = double(tasks) / double(nb * NT);
+        const double score = fill * double(resident) / kRtMaxWarps * (1.0 + 0.05 * NT);
+        if (score > best) { best = score; c.NT = NT; c.nblocks = nb; c.ctas_per_sm = by_regs; }
+    }
+    if (!c.NT) return false;
+    // cost model (clk, whole layer per image): issue slots / 4 vs shared-memory wavefronts
+    const int WR = sh.TY + sh.R - 1, WC = sh.TX + sh.S - 1;
+    double hdr = 0;
+    for (int g = 0; g < p->groups; ++g)
+        for (int t = 0; t < tasks; ++t) hdr += double(task_groups(p, g, t, sh.M));
+    const double ops = double(p->colidx.size());
+    const double per_img = double(c.NG) / double(c.NI);
+    const double issue = (hdr * (WR * WC + WR + 6) + ops * (sh.TY * sh.TX + 9)) * per_img;
+    const double wave = (hdr * (WR * WC * c.wf + 1) + ops) * per_img;
+    c.cost = std::max(issue / 4.0, wave);
+    return true;
+}
+
+skc_status build_regtile(skc_plan *p, const RtCandidate &c) {
+    const RegtileShape &sh = c.sh;
+    const int M = sh.M;
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    const int nchunks = (p->Cg + c.CB - 1) / c.CB;
+    const int tasks = (p->Kg + M - 1) / M;
+    const int nb = c.nblocks, NT = c.NT;
+    const int ncase = M * sh.R * sh.S;
+    std::vector<uint32_t> stream;  // pairs (x, case)
+    std::vector<int32_t> segoff(size_t(p->groups) * nb * nchunks * (NT + 1));
+    std::vector<int32_t> chan(size_t(p->groups) * nb * NT * M, -1);
+    int64_t max_region = 0;
+    // per (group, task): nonzeros of its M channels bucketed by chunk, each bucket sorted by
+    // (c, m, r, s) -- accumulation per output element stays in CSR order (c, r, s)
+    struct Op { int cl, m, rs; float w; };
+    for (int g = 0; g < p->groups; ++g) {
+        for (int b = 0; b < nb; ++b) {
+            std::vector<std::vector<std::vector<Op>>> per(
+                static_cast<size_t>(NT),
+                std::vector<std::vector<Op>>(static_cast<size_t>(nchunks)));
+            for (int t = 0; t < NT; ++t) {
+                const int task = b * NT + t;
+                if (task >= tasks) continue;
+                for (int m = 0; m < M; ++m) {
+                    const int lp = task * M + m;
+                    if (lp >= p->Kg) break;
+                    const int k = p->perm[size_t(g) * p->Kg + lp];
+                    chan[((size_t(g) * nb + b) * NT + t) * M + m] = k;
+                    for (int32_t j = p->rowptr[k]; j < p->rowptr[k + 1]; ++j) {
+                        const int64_t col = p->colidx[j];
+                        const int cl = int(col / plane) - g * p->Cg;
+                        const int64_t rem = col % plane;
+                        const int r = int(rem / p->Wp), s = int(rem % p->Wp);
+                        per[size_t(t)][size_t(cl / c.CB)].push_back(
+                            Op{cl, m, r * sh.S + s, p->values[j]});
+                    }
+                }
+            }
+            for (int i = 0; i < nchunks; ++i) {
+                if (stream.size() % 4) stream.resize(align_up(stream.size(), 4), 0);  // 16 B
+                int32_t *so = &segoff[((size_t(g) * nb + b) * nchunks + i) * (NT + 1)];
+                const int64_t region0 = int64_t(stream.size() / 2);
+                for (int t = 0; t < NT; ++t) {
+                    so[t] = int32_t(stream.size() / 2);
+                    auto &ops = per[size_t(t)][size_t(i)];
+                    std::stable_sort(ops.begin(), ops.end(), [](const Op &a, const Op &b2) {
+                        return a.cl != b2.cl ? a.cl < b2.cl : a.m != b2.m ? a.m < b2.m
+                                                                            : a.rs < b2.rs;
+                    });
+                    int cur = -1;
+                    for (const Op &o : ops) {
+                        if (o.cl != cur) {
+                            cur = o.cl;
+                            stream.push_back(uint32_t((cur - i * c.CB) * plane));
+                            stream.push_back(uint32_t(ncase));  // HDR
+                        }
+                        uint32_t wb;
+                        std::memcpy(&wb, &o.w, 4);
+                        stream.push_back(wb);
+                        stream.push_back(uint32_t(o.m * sh.R * sh.S + o.rs));
+                    }
+                    stream.push_back(0);
+                    stream.push_back(uint32_t(ncase + 1));  // EXIT
+                }
+                so[NT] = int32_t(stream.size() / 2);
+                max_region = std::max(max_region, int64_t(so[NT]) - region0);
+            }
+        }
+    }
+    if (stream.size() / 2 >= (size_t(1) << 31))
+        return fail(SKC_ERR_OVERFLOW, "regtile op stream too large");
+    RegtileParams &rp = p->rp;
+    rp = RegtileParams{};
+    rp.C = p->C; rp.K = p->K; rp.Cg = p->Cg; rp.Kg = p->Kg; rp.Hp = p->Hp; rp.Wp = p->Wp;
+    rp.Ho = p->Ho; rp.Wo = p->Wo; rp.groups = p->groups;
+    rp.NI = c.NI; rp.CB = c.CB; rp.nchunks = nchunks;
+    rp.img_stride = c.img_stride;
+    rp.slab_floats = c.NI * c.img_stride;
+    rp.stream_cap = int(align_up(size_t(max_region) + 2, 2));
+    rp.stage_floats = rp.slab_floats + 2 * rp.stream_cap;
+    rp.NG = c.NG; rp.NT = NT; rp.nblocks = nb;
+    const size_t stage_bytes = size_t(rp.stage_floats) * 4;
+    const int WR = sh.TY + sh.R - 1, WC = sh.TX + sh.S - 1;
+    const size_t tail = align_up(size_t(WR) * p->Wp + WC + 4, 4) * 4;  // junk-tile overrun
+    const size_t fixed = tail + kMaxStages * (sizeof(uint64_t) + sizeof(int));
+    int NS = kRtStages;
+    while (NS > 1 && NS * stage_bytes + fixed > (c.ctas_per_sm >= 2 ? 110 << 10 : 220 << 10))
+        --NS;
+    NS = std::min(NS, nchunks);
+    if (NS * stage_bytes + fixed > (227 << 10))
+        return fail(SKC_ERR_UNSUPPORTED, "regtile stage of %zu B does not fit", stage_bytes);
+    rp.NS = NS;
+    // stages come first; the tail slack sits between the last stage and the barriers
+    p->smem = size_t(NS) * stage_bytes + fixed;
+    p->rsh = sh;
+    p->sg = StageGeom{};
+    p->sg.CB = c.CB; p->sg.NS = NS; p->sg.BH = sh.TY;
+    p->NW = c.NG * NT; p->M = M; p->T = sh.TY * sh.TX;
+    // device image: stream | segoff | chan | lanemap | perm
+    p->off_stream = 0;
+    p->off_segoff = align_up(stream.size() * 4, 256);
+    p->off_chan = align_up(p->off_segoff + segoff.size() * 4, 256);
+    p->off_lanemap = align_up(p->off_chan + chan.size() * 4, 256);
+    p->off_perm = align_up(p->off_lanemap + c.lanemap.size() * 4, 256);
+    const size_t total = align_up(p->off_perm + size_t(p->K) * 4, 256);
+    p->image.assign(total, 0);
+    std::memcpy(p->image.data() + p->off_stream, stream.data(), stream.size() * 4);
+    std::memcpy(p->image.data() + p->off_segoff, segoff.data(), segoff.size() * 4);
+    std::memcpy(p->image.data() + p->off_chan, chan.data(), chan.size() * 4);
+    std::memcpy(p->image.data() + p->off_lanemap, c.lanemap.data(), c.lanemap.size() * 4);
+    std::memcpy(p->image.data() + p->off_perm, p->perm.data(), size_t(p->K) * 4);
+    return SKC_OK;
+}
+
+// Estimated direct-kernel cost on the same scale as RtCandidate::cost (clk per image).
+double direct_cost(const skc_plan *p) {
+    const double nnz = double(p->colidx.size());
+    const int nb = p->sg.nbands;
+    const double issue = nnz * nb * (2.0 * p->T + 6);
+    const double wave = nnz * nb * (p->T + 2.0);
+    return std::max(issue / 4.0, wave);
+}
+
 bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
 }  // namespace
@@ -315,13 +573,38 @@ skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, in
         });
     }
 
-    p->kernel = (kernel == SKC_KERNEL_AUTO) ? SKC_KERNEL_DIRECT : kernel;
-    if (p->kernel == SKC_KERNEL_REGTILE) {
-        delete p;
-        return fail(SKC_ERR_UNSUPPORTED, "register-tiled kernel not available in this build");
+    // kernel choice: the register-tiled kernel when an instantiated tile shape fits and the
+    // cost model prefers it; the direct kernel otherwise (any stride, any R x S)
+    RtCandidate best_rt;
+    if (kernel != SKC_KERNEL_DIRECT) {
+        RegtileShape shapes[32];
+        const int ns = std::min(32, regtile_shapes(shapes, 32));
+        for (int i = 0; i < ns; ++i) {
+            RtCandidate cand;
+            if (regtile_candidate(p, shapes[i], cand) && cand.cost < best_rt.cost)
+                best_rt = cand;
+        }
     }
     st = configure_direct(p);
-    if (st == SKC_OK) st = build_direct_image(p);
+    if (kernel == SKC_KERNEL_REGTILE && best_rt.cost >= 1e300) {
+        delete p;
+        return fail(SKC_ERR_UNSUPPORTED, "no register-tile shape for R=%d S=%d stride=%d "
+                    "(or TMA alignment)", R, S, stride);
+    }
+    if (kernel == SKC_KERNEL_DIRECT && st != SKC_OK) {
+        delete p;
+        return st;
+    }
+    const bool use_rt = best_rt.cost < 1e300 &&
+                        (kernel == SKC_KERNEL_REGTILE || st != SKC_OK ||
+                         best_rt.cost < direct_cost(p));
+    if (use_rt) {
+        p->kernel = SKC_KERNEL_REGTILE;
+        st = build_regtile(p, best_rt);
+    } else if (st == SKC_OK) {
+        p->kernel = SKC_KERNEL_DIRECT;
+        st = build_direct_image(p);
+    }
     if (st != SKC_OK) {
         delete p;
         return st;
@@ -350,6 +633,9 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.warps = p->NW; i.channels_per_warp = p->M; i.pixels_per_lane = p->T;
     i.smem_bytes = p->smem;
     i.lane_mapping = p->pitch;
+    i.tile_h = p->kernel == SKC_KERNEL_REGTILE ? p->rsh.TY : 0;
+    i.tile_w = p->kernel == SKC_KERNEL_REGTILE ? p->rsh.TX : 0;
+    i.images_per_cta = p->kernel == SKC_KERNEL_REGTILE ? p->rp.NI : 1;
     return ok();
 }
 
@@ -404,6 +690,20 @@ skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *
     if (!aligned16(d_in) || !aligned16(d_out))
         return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
     const uint8_t *ws = static_cast<const uint8_t *>(p->d_ws);
+    if (p->kernel == SKC_KERNEL_REGTILE) {
+        RegtileParams rp = p->rp;
+        rp.N = N;
+        rp.in = d_in;
+        rp.out = d_out;
+        rp.stream = reinterpret_cast<const uint2 *>(ws + p->off_stream);
+        rp.segoff = reinterpret_cast<const int32_t *>(ws + p->off_segoff);
+        rp.chan = reinterpret_cast<const int32_t *>(ws + p->off_chan);
+        rp.lanemap = reinterpret_cast<const int32_t *>(ws + p->off_lanemap);
+        cudaError_t e = launch_regtile(rp, p->rsh, p->smem, (cudaStream_t)stream);
+        if (e != cudaSuccess)
+            return fail(SKC_ERR_CUDA, "regtile launch: %s", cudaGetErrorString(e));
+        return ok();
+    }
     DirectParams dp{};
     dp.g = p->sg;
     dp.g.N = N;

@@ -43,7 +43,8 @@ class skc_info(ctypes.Structure):
         ("kernel", ctypes.c_int), ("band_rows", ctypes.c_int), ("chunk_channels", ctypes.c_int),
         ("stages", ctypes.c_int), ("warps", ctypes.c_int), ("channels_per_warp", ctypes.c_int),
         ("pixels_per_lane", ctypes.c_int), ("smem_bytes", ctypes.c_size_t),
-        ("lane_mapping", ctypes.c_int)]
+        ("lane_mapping", ctypes.c_int), ("tile_h", ctypes.c_int), ("tile_w", ctypes.c_int),
+        ("images_per_cta", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -78,7 +78,8 @@ def test_worked_example_gpu(golden_dir):
         np.testing.assert_array_equal(out, np.array(case["out"], np.float32))
 
 
-def test_random_geometries():
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_random_geometries(kernel):
     """SPEC.md:159-163 property suite ranges (+ groups, stride 2): >= 200 random layers."""
     rng = np.random.default_rng(1)
     worst = 0.0
@@ -86,13 +87,49 @@ def test_random_geometries():
         layer = wl.random_layer(rng, max_c=32, max_hw=16, rs=(1, 2, 3, 5), groups=(1, 2, 4))
         N = int(rng.integers(1, 4))
         w, x = wl.random_tensors(rng, layer, N)
-        out, _ = run_gpu(w, x, layer)
+        out, _ = run_gpu(w, x, layer, kernel)
         ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
         worst = max(worst, check(out, ref, bound, f"it{it} {layer}"))
     print("max err/bound", worst)
 
 
-def test_tiles_and_ragged_tails():
+def test_regtile_random_shapes():
+    """The register-tiled kernel forced on random 3x3 / 5x5 stride-1 layers whose padded
+    planes keep the TMA copies aligned: ragged K (not a multiple of M), C/g not a multiple
+    of the chunk, batches that are not a multiple of the images per CTA, tiles that
+    overhang the output, several lane groups, empty channels."""
+    rng = np.random.default_rng(11)
+    n_rt = 0
+    for it in range(120):
+        R = int(rng.choice([3, 5]))
+        g = int(rng.choice([1, 2]))
+        C = g * 4 * int(rng.integers(1, 9))
+        K = g * int(rng.integers(1, 40))
+        H = int(rng.integers(R - 2 if R > 2 else 1, 40))
+        W = int(rng.integers(R - 2 if R > 2 else 1, 40))
+        pad = (R - 1) // 2
+        x_keep = float(rng.choice([1.0, 0.5, 0.1, 0.02]))
+        layer = wl.Layer("rt", K, C, H, W, R, R, 1, pad, g, 1.0 - x_keep, 1.0)
+        if layer.Ho < 1 or layer.Wo < 1:
+            continue
+        N = int(rng.integers(1, 12))
+        w, x = wl.random_tensors(rng, layer, N)
+        if it % 5 == 0:
+            w[rng.integers(0, K)] = 0.0
+        try:
+            out, conv = run_gpu(w, x, layer, skc.SKC_KERNEL_REGTILE)
+        except skc.SkcError as e:
+            assert e.status == -5, e  # unsupported tiling only
+            continue
+        assert conv.geom["kernel"] == skc.SKC_KERNEL_REGTILE
+        n_rt += 1
+        ref, bound = oracle.conv2d_fp64(x, w, 1, pad, g)
+        check(out, ref, bound, f"regtile it{it} {layer} {conv.geom}")
+    assert n_rt >= 80, n_rt
+
+
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_tiles_and_ragged_tails(kernel):
     """Shapes spanning several channel blocks, stages, bands and lane tails."""
     rng = np.random.default_rng(2)
     cases = [
@@ -106,7 +143,7 @@ def test_tiles_and_ragged_tails():
     ]
     for layer in cases:
         w, x = wl.random_tensors(rng, layer, 3)
-        out, conv = run_gpu(w, x, layer)
+        out, conv = run_gpu(w, x, layer, kernel)
         ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
         check(out, ref, bound, f"{layer} {conv.geom}")
 
@@ -149,12 +186,14 @@ def test_dense_equals_torch_conv2d_fp32():
     assert np.max(np.abs(out - t) / np.maximum(bound, 1e-30)) <= 2 * TOL
 
 
-def test_determinism_and_host_path():
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_determinism_and_host_path(kernel):
     rng = np.random.default_rng(5)
     layer = wl.CONFIGS[2].layers[1]
     w = wl.gen_weights(2, 1, layer)
     x = wl.gen_input(2, 1, layer, 0, 8)
-    conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups)
+    conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                       kernel)
     xd = torch.from_numpy(x).cuda()
     a = conv.forward(xd).cpu().numpy()
     b = conv.forward(xd).cpu().numpy()
@@ -178,8 +217,9 @@ def sample_images(N, rng, k):
     return sorted(idx)
 
 
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
 @pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
-def test_config_parity(cfg_id):
+def test_config_parity(cfg_id, kernel):
     """Every BASELINE config layer at its full batch on the GPU, in the launch configuration
     bench.py times; the oracle checks a seeded sample of images (always first and last)."""
     cfg = wl.CONFIGS[cfg_id]
@@ -187,7 +227,7 @@ def test_config_parity(cfg_id):
     for li, layer in enumerate(cfg.layers):
         w = wl.gen_weights(cfg_id, li, layer)
         x = wl.gen_input(cfg_id, li, layer, 0, cfg.batch)
-        out, conv = run_gpu(w, x, layer)
+        out, conv = run_gpu(w, x, layer, kernel)
         k = 4 if cfg_id != 3 else 2
         for n in sample_images(cfg.batch, rng, k):
             ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
