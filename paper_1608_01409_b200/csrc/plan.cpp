@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -250,8 +251,9 @@ skc_status build_direct_image(skc_plan *p) {
 // ---------------------------------------------------------------------------------------
 // Register-tiled kernel: configuration and op streams (see sconv_regtile.cu)
 // ---------------------------------------------------------------------------------------
-constexpr int kRtMaxWarps = 12;            // 384 threads at <= 168 registers per thread
-constexpr int kRtRegs = 168;
+// register cap of a shape's instance (its __launch_bounds__)
+int rt_regs(const RegtileShape &sh) { return std::min(255, 65536 / (32 * sh.nwmax * sh.minb)) & ~7; }
+
 constexpr size_t kRtStageTarget = 24 << 10;
 constexpr int kRtStages = 3;
 
@@ -306,13 +308,13 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
     c.NI = tiles >= 32 ? 1 : std::max(1, 32 / tiles);
     const int total = c.NI * tiles;
     c.NG = (total + 31) / 32;
-    if (c.NG > kRtMaxWarps) return false;
+    if (c.NG > sh.nwmax) return false;
     // channels per stage: input slab of NI images + the op stream of up to 12 tasks of M
     // channels (8 B per nonzero), aiming at kRtStageTarget bytes; CB*plane must keep image
     // slots 16-byte aligned
     const double density = double(p->colidx.size()) / (double(p->K) * p->Cg * p->R * p->S);
     const double chan_bytes = double(c.NI) * double(plane) * 4.0 +
-                              8.0 * (kRtMaxWarps * (sh.M * sh.R * sh.S * density + 1.0));
+                              8.0 * (sh.nwmax * (sh.M * sh.R * sh.S * density + 1.0));
     int CB = int(std::max(1.0, double(kRtStageTarget) / chan_bytes));
     CB = std::min(CB, p->Cg);
     while (CB > 1 && (int64_t(CB) * plane) % 4) --CB;
@@ -349,18 +351,21 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
     }
     c.img_stride = base + best_pad;
     c.wf = best_wf;
-    // tasks per CTA: keep ~12 warps resident per SM, fill the last block, and prefer more
-    // tasks per CTA (each CTA re-reads its images' slabs: fewer blocks, less L2 traffic)
+    // tasks per CTA: keep the most warps resident per SM, fill the last block, and prefer
+    // more tasks per CTA (each CTA re-reads its images' slabs: fewer blocks, less traffic)
     const int tasks = (p->Kg + sh.M - 1) / sh.M;
     double best = -1;
-    for (int NT = std::min(kRtMaxWarps / c.NG, tasks); NT >= 1; --NT) {
+    const char *nt_env = std::getenv("SKC_RT_NT");
+    const int nt_force = nt_env ? std::atoi(nt_env) : 0;
+    for (int NT = std::min(sh.nwmax / c.NG, tasks); NT >= 1; --NT) {
+        if (nt_force > 0 && NT != std::min(nt_force, std::min(sh.nwmax / c.NG, tasks))) continue;
         const int nb = (tasks + NT - 1) / NT;
         const int warps = c.NG * NT;
-        const int by_regs = 65536 / (warps * 32 * kRtRegs);
+        const int by_regs = 65536 / (warps * 32 * rt_regs(sh));
         if (by_regs < 1) continue;
-        const int resident = std::min(kRtMaxWarps, warps * std::min(by_regs, 2));
+        const int resident = std::min(64, warps * std::min(by_regs, 3));
         const double fill = double(tasks) / double(nb * NT);
-        const double score = fill * double(resident) / kRtMaxWarps * (1.0 + 0.05 * NT);
+        const double score = fill * double(resident) * (1.0 + 0.05 * NT);
         if (score > best) { best = score; c.NT = NT; c.nblocks = nb; c.ctas_per_sm = by_regs; }
     }
     if (!c.NT) return false;
@@ -463,7 +468,8 @@ skc_status build_regtile(skc_plan *p, const RtCandidate &c) {
     const size_t tail = align_up(size_t(WR) * p->Wp + WC + 4, 4) * 4;  // junk-tile overrun
     const size_t fixed = tail + kMaxStages * (sizeof(uint64_t) + sizeof(int));
     int NS = kRtStages;
-    while (NS > 1 && NS * stage_bytes + fixed > (c.ctas_per_sm >= 2 ? 110 << 10 : 220 << 10))
+    const size_t smem_cap = (220u << 10) / size_t(std::max(1, std::min(c.ctas_per_sm, 3)));
+    while (NS > 1 && NS * stage_bytes + fixed > smem_cap)
         --NS;
     NS = std::min(NS, nchunks);
     if (NS * stage_bytes + fixed > (227 << 10))
@@ -579,10 +585,26 @@ skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, in
     if (kernel != SKC_KERNEL_DIRECT) {
         RegtileShape shapes[32];
         const int ns = std::min(32, regtile_shapes(shapes, 32));
+        // SKC_RT_SHAPE="R,S,TY,TX,M" restricts the search to one shape (tuning/benchmarks)
+        RegtileShape want{};
+        const char *env = std::getenv("SKC_RT_SHAPE");
+        const bool forced = env && std::sscanf(env, "%d,%d,%d,%d,%d", &want.R, &want.S,
+                                              &want.TY, &want.TX, &want.M) == 5;
+        // SKC_RT_COST=1 prints the cost model of every candidate (tuning aid)
+        const bool verbose = std::getenv("SKC_RT_COST") != nullptr;
         for (int i = 0; i < ns; ++i) {
+            const RegtileShape &sh = shapes[i];
+            if (forced && (sh.R != want.R || sh.S != want.S || sh.TY != want.TY ||
+                           sh.TX != want.TX || sh.M != want.M))
+                continue;
             RtCandidate cand;
-            if (regtile_candidate(p, shapes[i], cand) && cand.cost < best_rt.cost)
-                best_rt = cand;
+            const bool okc = regtile_candidate(p, sh, cand);
+            if (verbose)
+                std::fprintf(stderr, "skc regtile %dx%d tile %dx%d M=%d nw=%d: %s cost %.4g NI=%d "
+                             "NG=%d NT=%d CB=%d wf=%d\n", sh.R, sh.S, sh.TY, sh.TX, sh.M, sh.nwmax,
+                             okc ? "ok" : "n/a", cand.cost, cand.NI, cand.NG, cand.NT, cand.CB,
+                             cand.wf);
+            if (okc && cand.cost < best_rt.cost) best_rt = cand;
         }
     }
     st = configure_direct(p);

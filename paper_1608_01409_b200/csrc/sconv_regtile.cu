@@ -47,8 +47,8 @@ __device__ __forceinline__ void fill_stage(const RegtileParams &p, float *stage,
     if (st_bytes) bulk_g2s(stage + p.slab_floats, p.stream + s0, st_bytes, bar);
 }
 
-template <int R, int S, int TY, int TX, int M>
-__global__ void __launch_bounds__(384, 1) sconv_regtile_kernel(const RegtileParams p) {
+template <int R, int S, int TY, int TX, int M, int NWMAX, int MINB>
+__global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const RegtileParams p) {
     constexpr int WR = TY + R - 1, WC = TX + S - 1;
     extern __shared__ __align__(128) float smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + size_t(p.NS) * p.stage_floats);
@@ -137,10 +137,10 @@ __global__ void __launch_bounds__(384, 1) sconv_regtile_kernel(const RegtilePara
     }
 }
 
-template <int R, int S, int TY, int TX, int M>
+template <int R, int S, int TY, int TX, int M, int NWMAX, int MINB>
 cudaError_t launch_shape(const RegtileParams &p, size_t smem, cudaStream_t st) {
     static bool attr_set = false;
-    auto fn = sconv_regtile_kernel<R, S, TY, TX, M>;
+    auto fn = sconv_regtile_kernel<R, S, TY, TX, M, NWMAX, MINB>;
     if (!attr_set) {
         cudaError_t e =
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -148,7 +148,7 @@ cudaError_t launch_shape(const RegtileParams &p, size_t smem, cudaStream_t st) {
         attr_set = true;
     }
     const int64_t grid = int64_t((p.N + p.NI - 1) / p.NI) * p.groups * p.nblocks;
-    if (grid > 0x7fffffff || p.NG * p.NT * 32 > 384) return cudaErrorInvalidConfiguration;
+    if (grid > 0x7fffffff || p.NG * p.NT > NWMAX) return cudaErrorInvalidConfiguration;
     fn<<<unsigned(grid), p.NG * p.NT * 32, smem, st>>>(p);
     return cudaGetLastError();
 }
@@ -157,8 +157,8 @@ cudaError_t launch_shape(const RegtileParams &p, size_t smem, cudaStream_t st) {
 
 int regtile_shapes(RegtileShape *out, int max) {
     int n = 0;
-#define X(r, s, ty, tx, m) \
-    if (n < max) out[n] = RegtileShape{r, s, ty, tx, m}; \
+#define X(r, s, ty, tx, m, nw, mb) \
+    if (n < max) out[n] = RegtileShape{r, s, ty, tx, m, nw, mb}; \
     ++n;
     SKC_REGTILE_SHAPES(X)
 #undef X
@@ -167,9 +167,10 @@ int regtile_shapes(RegtileShape *out, int max) {
 
 cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_t smem,
                            cudaStream_t st) {
-#define X(r, s, ty, tx, m)                                                            \
-    if (sh.R == r && sh.S == s && sh.TY == ty && sh.TX == tx && sh.M == m)            \
-        return launch_shape<r, s, ty, tx, m>(p, smem, st);
+#define X(r, s, ty, tx, m, nw, mb)                                                    \
+    if (sh.R == r && sh.S == s && sh.TY == ty && sh.TX == tx && sh.M == m &&          \
+        sh.nwmax == nw && sh.minb == mb)                                               \
+        return launch_shape<r, s, ty, tx, m, nw, mb>(p, smem, st);
     SKC_REGTILE_SHAPES(X)
 #undef X
     return cudaErrorInvalidValue;

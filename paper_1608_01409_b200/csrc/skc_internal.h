@@ -72,6 +72,7 @@ struct RegtileParams {
 
 struct RegtileShape {
     int R, S, TY, TX, M;
+    int nwmax, minb;  // __launch_bounds__(nwmax*32, minb): register cap of the instance
 };
 
 // Launchers (defined in the .cu files).  Return cudaError_t of the launch.
