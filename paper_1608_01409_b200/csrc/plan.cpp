@@ -431,26 +431,20 @@ skc_status build_regtile(skc_plan *p, const RtCandidate &c) {
                         return a.cl != b2.cl ? a.cl < b2.cl : a.m != b2.m ? a.m < b2.m
                                                                             : a.rs < b2.rs;
                     });
-                    // the segment's ops {x, case} (HDR before each new input channel) ...
-                    std::vector<std::pair<uint32_t, uint32_t>> seq;
                     int cur = -1;
                     for (const Op &o : ops) {
                         if (o.cl != cur) {
                             cur = o.cl;
-                            seq.emplace_back(uint32_t((cur - i * c.CB) * plane), uint32_t(ncase));
+                            stream.push_back(uint32_t((cur - i * c.CB) * plane));
+                            stream.push_back(uint32_t(ncase));  // HDR
                         }
                         uint32_t wb;
                         std::memcpy(&wb, &o.w, 4);
-                        seq.emplace_back(wb, uint32_t(o.m * sh.R * sh.S + o.rs));
+                        stream.push_back(wb);
+                        stream.push_back(uint32_t(o.m * sh.R * sh.S + o.rs));
                     }
-                    // ... in look-ahead form: {0, case_0}, {x_j, case_(j+1)}, last -> EXIT
-                    const uint32_t exit_case = uint32_t(ncase + 1);
                     stream.push_back(0);
-                    stream.push_back(seq.empty() ? exit_case : seq[0].second);
-                    for (size_t j = 0; j < seq.size(); ++j) {
-                        stream.push_back(seq[j].first);
-                        stream.push_back(j + 1 < seq.size() ? seq[j + 1].second : exit_case);
-                    }
+                    stream.push_back(uint32_t(ncase + 1));  // EXIT
                 }
                 so[NT] = int32_t(stream.size() / 2);
                 max_region = std::max(max_region, int64_t(so[NT]) - region0);
