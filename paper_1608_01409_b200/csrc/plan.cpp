@@ -58,6 +58,7 @@ struct skc_plan {
     int kernel = SKC_KERNEL_DIRECT;
     StageGeom sg{};
     int T = 0, NW = 0, M = 0, cblocks = 0, pitch = 0;
+    double direct_waves = 0;  // smem wavefronts per nonzero per image (all bands)
     size_t smem = 0;
 
     // register-tiled kernel configuration (kernel == SKC_KERNEL_REGTILE)
@@ -157,6 +158,7 @@ skc_status configure_direct(skc_plan *p) {
         return fail(SKC_ERR_UNSUPPORTED, "no band fits (Wo=%d too wide for the direct kernel)",
                     Wo);
     p->pitch = best_pitch;
+    p->direct_waves = best_cost;
     StageGeom &g = p->sg;
     g.C = p->C; g.K = p->K; g.Kg = p->Kg; g.Cg = p->Cg; g.Hp = p->Hp; g.Wp = p->Wp;
     g.Ho = Ho; g.Wo = Wo; g.stride = p->stride;
@@ -369,16 +371,24 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
         if (score > best) { best = score; c.NT = NT; c.nblocks = nb; c.ctas_per_sm = by_regs; }
     }
     if (!c.NT) return false;
-    // cost model (clk, whole layer per image): issue slots / 4 vs shared-memory wavefronts
+    // Cost model, SM-cycles per image summed over SMs (fitted to B200 measurements, see
+    // DESIGN.md "Kernel selection"): every dispatched op costs a(occ) -- the brx.idx dispatch
+    // is latency-bound, so its cost falls with the warps resident per SM -- and every HDR
+    // costs its window's shared-memory wavefronts.
     const int WR = sh.TY + sh.R - 1, WC = sh.TX + sh.S - 1;
     double hdr = 0;
     for (int g = 0; g < p->groups; ++g)
         for (int t = 0; t < tasks; ++t) hdr += double(task_groups(p, g, t, sh.M));
     const double ops = double(p->colidx.size());
     const double per_img = double(c.NG) / double(c.NI);
-    const double issue = (hdr * (WR * WC + WR + 6) + ops * (sh.TY * sh.TX + 9)) * per_img;
-    const double wave = (hdr * (WR * WC * c.wf + 1) + ops) * per_img;
-    c.cost = std::max(issue / 4.0, wave);
+    const double stage_est = double(c.NI) * c.img_stride * 4.0 +
+                             8.0 * c.NT * (c.CB * (sh.M * sh.R * sh.S * density + 1.0) + 2.0);
+    const int warps = c.NG * c.NT;
+    const int by_smem = std::max(1, int((228.0 * 1024) / (kRtStages * stage_est + 1024)));
+    const int ctas = std::min({c.ctas_per_sm, by_smem, 2048 / (warps * 32), 32});
+    const double occ = std::min(64, warps * ctas);
+    const double a = 10.7 * (16.0 / occ) * (16.0 / occ);
+    c.cost = (ops * a + hdr * WR * WC * std::max(1.0, 0.5 * c.wf)) * per_img;
     return true;
 }
 
@@ -499,11 +509,9 @@ skc_status build_regtile(skc_plan *p, const RtCandidate &c) {
 
 // Estimated direct-kernel cost on the same scale as RtCandidate::cost (clk per image).
 double direct_cost(const skc_plan *p) {
-    const double nnz = double(p->colidx.size());
-    const int nb = p->sg.nbands;
-    const double issue = nnz * nb * (2.0 * p->T + 6);
-    const double wave = nnz * nb * (p->T + 2.0);
-    return std::max(issue / 4.0, wave);
+    // shared-memory wavefronts per nonzero per image (T loads + 2 shuffles per band), at the
+    // ~80% wavefront utilisation ncu measured (profiles/r01_ncu_conv3_direct_pitch.json)
+    return double(p->colidx.size()) * p->direct_waves / 0.80;
 }
 
 bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
@@ -619,7 +627,7 @@ skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, in
     }
     const bool use_rt = best_rt.cost < 1e300 &&
                         (kernel == SKC_KERNEL_REGTILE || st != SKC_OK ||
-                         best_rt.cost < direct_cost(p));
+                         best_rt.cost < 0.9 * direct_cost(p));  // prefer direct on near-ties
     if (use_rt) {
         p->kernel = SKC_KERNEL_REGTILE;
         st = build_regtile(p, best_rt);
