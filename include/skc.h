@@ -73,7 +73,7 @@ typedef struct {
     int kernel;                    /* skc_kernel chosen (after AUTO resolution)         */
     int band_rows, chunk_channels, stages, warps, channels_per_warp, pixels_per_lane;
     size_t smem_bytes;             /* dynamic shared memory per CTA of the conv kernel  */
-    int lane_mapping;              /* direct kernel: 0 = output pixels, 1 = padded pitch  */
+    int lane_mapping;              /* direct kernel: images sharing residue-bucketed slots */
     int tile_h, tile_w;            /* regtile kernel: register tile per lane (0: direct)  */
     int images_per_cta;            /* images staged together in one CTA                   */
 } skc_info;

@@ -43,6 +43,16 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
+// Host-side staging geometry of a plan (the kernels receive DirectParams / RegtileParams).
+struct StageGeom {
+    int C, K, Kg, Cg, Hp, Wp, Ho, Wo, stride;
+    int NI;           // images per CTA
+    int BH, BHin, nbands;
+    int CB, nchunks, NS;
+    int chan_stride, img_stride, stage_floats;
+    int bulk, whole;
+};
+
 // ---------------------------------------------------------------------------------------
 // The plan
 // ---------------------------------------------------------------------------------------
@@ -57,7 +67,8 @@ struct skc_plan {
     // kernel choice + configuration
     int kernel = SKC_KERNEL_DIRECT;
     StageGeom sg{};
-    int T = 0, NW = 0, M = 0, cblocks = 0, pitch = 0;
+    int T = 0, NW = 0, M = 0, cblocks = 0;
+    DirectParams dp{};
     double direct_waves = 0;  // smem wavefronts per nonzero per image (all bands)
     size_t smem = 0;
 
@@ -75,7 +86,6 @@ struct skc_plan {
 
 namespace {
 
-const int kDirectT[] = {2, 4, 6, 7, 8, 12, 14, 16};
 constexpr int kDirectNW = 8;              // compute warps per CTA (+1 producer warp)
 constexpr size_t kStageTarget = 24 << 10;  // bytes per stage we aim for
 constexpr size_t kSmemBudget = 112 << 10;  // per CTA, so that >= 2 CTAs fit an SM
@@ -99,153 +109,208 @@ skc_status check_geometry(int K, int C, int R, int S, int H, int W, int stride, 
     return SKC_OK;
 }
 
-// Shared-memory wavefronts one warp needs for its T loads of one nonzero (per band), for
-// the natural output-pixel lane mapping: per t, the max number of DISTINCT words that fall
-// in one of the 32 banks (same-word lanes broadcast).
-int natural_wavefronts(int BHcur, int Wo, int Wp, int stride, int T) {
-    int total = 0;
-    const int npix = BHcur * Wo;
-    for (int t = 0; t < T; ++t) {
-        int words[32];
-        for (int l = 0; l < 32; ++l) {
-            const int px = t * 32 + l;
-            words[l] = px < npix ? (px / Wo) * stride * Wp + (px % Wo) * stride : 0;
-        }
-        int worst = 1;
-        for (int b = 0; b < 32; ++b) {
-            int distinct[32], nd = 0;
-            for (int l = 0; l < 32; ++l) {
-                if (((words[l] % 32) + 32) % 32 != b) continue;
-                bool seen = false;
-                for (int i = 0; i < nd; ++i) seen |= distinct[i] == words[l];
-                if (!seen) distinct[nd++] = words[l];
+// Residue-bucketed pixel slots of one band: pixel (img, yl, x) of the band lives at shared
+// word q = img*IS + yl*stride*Wp + x*stride (relative to its channel's base in image slot 0);
+// lane l gets the pixels with q == l (mod 32), so for any nonzero offset the 32 lanes of a
+// warp load from 32 distinct banks.  Returns T = slots per lane (the largest bucket).
+int band_slots(int NI, int IS, int rows, int Wo, int Wp, int stride,
+               std::vector<std::vector<std::pair<int, int>>> *buckets) {
+    std::vector<std::vector<std::pair<int, int>>> bk(32);
+    for (int img = 0; img < NI; ++img)
+        for (int yl = 0; yl < rows; ++yl)
+            for (int x = 0; x < Wo; ++x) {
+                const int q = img * IS + yl * stride * Wp + x * stride;
+                bk[size_t(q & 31)].emplace_back(q, (img << 24) | (yl << 12) | x);
             }
-            worst = std::max(worst, nd);
-        }
-        total += worst;
-    }
-    return total;
+    size_t T = 0;
+    for (auto &b : bk) T = std::max(T, b.size());
+    if (buckets) *buckets = std::move(bk);
+    return int(T);
 }
 
-// Pick the direct kernel's lane mapping, band height, pixels per lane, channel chunk and
-// warp layout.  Cost per nonzero per image = shared-memory wavefronts of the T loads of
-// every band + 2 shuffles per band; the cheapest candidate wins (ties: fewer bands).
+// Pick the direct kernel's images per CTA (NI), band height, image-slot stride, pixel slots
+// per lane (T), channel chunk and warp layout.  Cost per nonzero per image, in shared-memory
+// wavefronts: bands * (T loads + 1 broadcast) / NI; the cheapest candidate wins.
 skc_status configure_direct(skc_plan *p) {
     const int Ho = p->Ho, Wo = p->Wo;
+    StageGeom &g = p->sg;
+    g = StageGeom{};
+    g.C = p->C; g.K = p->K; g.Kg = p->Kg; g.Cg = p->Cg; g.Hp = p->Hp; g.Wp = p->Wp;
+    g.Ho = Ho; g.Wo = Wo; g.stride = p->stride;
+    if (Wo >= 4096 || Ho >= 4096)
+        return fail(SKC_ERR_UNSUPPORTED, "output %dx%d too large for the direct kernel", Ho, Wo);
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
     double best_cost = 1e300;
-    int best_nb = 0, best_T = 0, best_pitch = 0;
-    for (int pitch = 0; pitch <= (p->stride == 1 ? 1 : 0); ++pitch) {
+    for (int NI = 1; NI <= 4; NI *= 2) {
         for (int nb = 1; nb <= Ho; ++nb) {
             const int BH = (Ho + nb - 1) / nb;
             if ((Ho + BH - 1) / BH != nb) continue;  // same BH as a smaller nb
-            const int slots = BH * (pitch ? p->Wp : Wo);
-            const int need = (slots + 31) / 32;
-            int T = 0;
-            for (int t : kDirectT)
-                if (t >= need) { T = t; break; }
-            if (!T) continue;
-            double cost = 0;
-            for (int b = 0; b < nb; ++b) {
-                const int cur = std::min(BH, Ho - b * BH);
-                cost += 2 + (pitch ? T : natural_wavefronts(cur, Wo, p->Wp, p->stride, T));
-            }
-            if (cost < best_cost - 1e-9) {
-                best_cost = cost; best_nb = nb; best_T = T; best_pitch = pitch;
+            const int BHin = std::min((BH - 1) * p->stride + p->R, p->Hp);
+            const bool whole = nb == 1 && BHin == p->Hp;
+            const int chan_stride = whole ? int(plane) : BHin * p->Wp;
+            const size_t chan_bytes = size_t(NI) * chan_stride * 4;
+            if (chan_bytes > (96u << 10)) continue;
+            int CB = int(std::max<size_t>(1, kStageTarget / chan_bytes));
+            CB = std::min(CB, p->Cg);
+            if (CB >= 4) CB -= CB % 4;
+            const int base_is = int(align_up(size_t(CB) * chan_stride, 4));
+            for (int pad = 0; pad < (NI > 1 ? 32 : 4); pad += 4) {
+                const int IS = base_is + pad;
+                int T = 0;
+                for (int b = 0; b < nb; ++b)
+                    T = std::max(T, band_slots(NI, IS, std::min(BH, Ho - b * BH), Wo, p->Wp,
+                                               p->stride, nullptr));
+                if (T > 16) continue;
+                const double cost = double(nb) * (T + 1) / NI + 1e-3 * NI + 1e-4 * nb;
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    g.NI = NI; g.BH = BH; g.nbands = nb; g.BHin = BHin; g.whole = whole;
+                    g.CB = CB; g.chan_stride = chan_stride; g.img_stride = IS; p->T = T;
+                }
             }
         }
     }
-    if (!best_T)
-        return fail(SKC_ERR_UNSUPPORTED, "no band fits (Wo=%d too wide for the direct kernel)",
-                    Wo);
-    p->pitch = best_pitch;
-    p->direct_waves = best_cost;
-    StageGeom &g = p->sg;
-    g.C = p->C; g.K = p->K; g.Kg = p->Kg; g.Cg = p->Cg; g.Hp = p->Hp; g.Wp = p->Wp;
-    g.Ho = Ho; g.Wo = Wo; g.stride = p->stride;
-    g.BH = (Ho + best_nb - 1) / best_nb;
-    g.nbands = (Ho + g.BH - 1) / g.BH;
-    g.BHin = std::min((g.BH - 1) * p->stride + p->R, p->Hp);
-    g.whole = (g.nbands == 1 && g.BHin == p->Hp) ? 1 : 0;
-    const size_t chan_bytes = size_t(g.BHin) * g.Wp * 4;
-    // (2) channels per stage
-    int CB = int(std::max<size_t>(1, kStageTarget / chan_bytes));
-    CB = std::min(CB, p->Cg);
-    if (CB >= 4) CB -= CB % 4;
-    g.CB = CB;
-    g.nchunks = (p->Cg + CB - 1) / CB;
-    g.stage_floats = int(align_up(size_t(CB) * g.BHin * g.Wp, 4));
-    const size_t stage_bytes = size_t(g.stage_floats) * 4;
-    g.NS = int(std::min<size_t>(4, std::max<size_t>(1, kSmemBudget / stage_bytes)));
-    g.NS = std::min(g.NS, std::max(1, g.nchunks));
-    if (stage_bytes > 200 * 1024)
-        return fail(SKC_ERR_UNSUPPORTED, "one input channel band needs %zu B of shared memory",
-                    stage_bytes);
-    // (3) bulk-copy (TMA) legality: 16-byte aligned sources, sizes and destinations
-    const int64_t plane = int64_t(g.Hp) * g.Wp;
-    bool bulk = (int64_t(g.C) * plane) % 4 == 0 && (int64_t(g.Cg) * plane) % 4 == 0;
+    if (best_cost >= 1e300)
+        return fail(SKC_ERR_UNSUPPORTED, "no band/slot tiling fits the direct kernel (Wo=%d)", Wo);
+    p->direct_waves = double(g.nbands) * (p->T + 1) / g.NI;
+    g.nchunks = (p->Cg + g.CB - 1) / g.CB;
+    // TMA bulk-copy legality: 16-byte aligned sources, destinations and sizes
+    bool bulk = (int64_t(g.C) * plane) % 4 == 0 && (int64_t(g.Cg) * plane) % 4 == 0 &&
+                g.img_stride % 4 == 0;
     if (g.whole) {
-        bulk = bulk && (int64_t(CB) * plane) % 4 == 0 &&
-               (int64_t(g.Cg % CB ? g.Cg % CB : CB) * plane) % 4 == 0;
+        bulk = bulk && (int64_t(g.CB) * plane) % 4 == 0 &&
+               (int64_t(g.Cg % g.CB ? g.Cg % g.CB : g.CB) * plane) % 4 == 0;
     } else {
         bulk = bulk && plane % 4 == 0 && (int64_t(g.BH) * p->stride * g.Wp) % 4 == 0 &&
-               (int64_t(g.BHin) * g.Wp) % 4 == 0;
-        // the last band may copy fewer rows: Hp - row0
+               g.chan_stride % 4 == 0;
         for (int b = 0; b < g.nbands && bulk; ++b) {
             const int row0 = b * g.BH * p->stride;
-            const int rows = std::min(g.BHin, g.Hp - row0);
-            bulk = (int64_t(rows) * g.Wp) % 4 == 0;
+            bulk = (int64_t(std::min(g.BHin, g.Hp - row0)) * g.Wp) % 4 == 0;
         }
     }
     g.bulk = bulk ? 1 : 0;
-    p->T = best_T;
     p->NW = kDirectNW;
-    p->M = std::max(1, std::min(4, 32 / best_T));
+    p->M = p->T <= 8 ? 4 : (p->T <= 16 ? 2 : 1);
     while (p->M > 1 && p->NW * p->M > p->Kg * 2) p->M /= 2;
     if (!direct_supported(p->T, p->M))
         return fail(SKC_ERR_UNSUPPORTED, "no direct kernel instance for T=%d M=%d", p->T, p->M);
     p->cblocks = (p->Kg + p->NW * p->M - 1) / (p->NW * p->M);
-    // padded-pitch lane slots beyond the band read up to T*32 words past the last channel
-    g.tail_floats = p->pitch ? int(align_up(size_t(p->T) * 32, 4)) : 0;
-    p->smem = size_t(g.NS) * stage_bytes + size_t(g.tail_floats) * 4 +
-              2 * kMaxStages * sizeof(uint64_t);
     return SKC_OK;
 }
 
-// Build the device image of the direct kernel: nonzero stream in perm order with offsets
-// re-encoded relative to their stage, per-(channel, chunk) pointers and the permutation.
+// Build the device image of the direct kernel: per (channel block, chunk) stream regions of
+// {w, off} (off relative to the channel's base in image slot 0 of the stage), segment
+// pointers, the channel table and the per-band pixel-slot tables.
 skc_status build_direct_image(skc_plan *p) {
-    const StageGeom &g = p->sg;
-    const int64_t nnz = int64_t(p->colidx.size());
-    std::vector<Nz> nz(static_cast<size_t>(nnz));
-    std::vector<int32_t> chunkptr(size_t(p->K) * (g.nchunks + 1));
+    StageGeom &g = p->sg;
     const int64_t plane = int64_t(p->Hp) * p->Wp;
-    int64_t pos = 0;
-    for (int kp = 0; kp < p->K; ++kp) {
-        const int k = p->perm[kp];
-        const int gk = k / p->Kg;
-        int32_t *cp = &chunkptr[size_t(kp) * (g.nchunks + 1)];
-        int chunk = 0;
-        cp[0] = int32_t(pos);
-        for (int32_t j = p->rowptr[k]; j < p->rowptr[k + 1]; ++j) {
-            const int64_t col = p->colidx[j];
-            const int c_local = int(col / plane) - gk * p->Cg;
-            const int64_t rem = col % plane;
-            const int r = int(rem / p->Wp), s = int(rem % p->Wp);
-            const int ch = c_local / g.CB, cl = c_local % g.CB;
-            while (chunk < ch) cp[++chunk] = int32_t(pos);
-            nz[size_t(pos)].w = p->values[j];
-            nz[size_t(pos)].off = int32_t((int64_t(cl) * g.BHin + r) * g.Wp + s);
-            ++pos;
+    const int nslot = p->NW * p->M;
+    const int gblocks = p->groups * p->cblocks;
+    std::vector<uint32_t> stream;  // pairs
+    std::vector<int32_t> segptr(size_t(gblocks) * g.nchunks * (nslot + 1));
+    std::vector<int32_t> chan(size_t(gblocks) * nslot, -1);
+    // per channel: its nonzeros bucketed by chunk, as {w bits, off}
+    int64_t max_region = 0;
+    for (int gi = 0; gi < p->groups; ++gi) {
+        for (int cb = 0; cb < p->cblocks; ++cb) {
+            const int gb = gi * p->cblocks + cb;
+            std::vector<std::vector<std::vector<std::pair<uint32_t, uint32_t>>>> per(
+                static_cast<size_t>(nslot),
+                std::vector<std::vector<std::pair<uint32_t, uint32_t>>>(
+                    static_cast<size_t>(g.nchunks)));
+            for (int j = 0; j < nslot; ++j) {
+                const int lc = cb * nslot + j;  // channel position inside the group (perm)
+                if (lc >= p->Kg) continue;
+                const int k = p->perm[size_t(gi) * p->Kg + lc];
+                chan[size_t(gb) * nslot + j] = k;
+                for (int32_t e = p->rowptr[k]; e < p->rowptr[k + 1]; ++e) {
+                    const int64_t col = p->colidx[e];
+                    const int cl = int(col / plane) - gi * p->Cg;
+                    const int64_t rem = col % plane;
+                    const int r = int(rem / p->Wp), s = int(rem % p->Wp);
+                    uint32_t wb;
+                    std::memcpy(&wb, &p->values[e], 4);
+                    const int off = (cl % g.CB) * g.chan_stride + r * p->Wp + s;
+                    per[size_t(j)][size_t(cl / g.CB)].emplace_back(wb, uint32_t(off));
+                }
+            }
+            for (int i = 0; i < g.nchunks; ++i) {
+                if (stream.size() % 4) stream.resize(align_up(stream.size(), 4), 0);  // 16 B
+                int32_t *sp = &segptr[(size_t(gb) * g.nchunks + i) * (nslot + 1)];
+                const int64_t r0 = int64_t(stream.size() / 2);
+                for (int j = 0; j < nslot; ++j) {
+                    sp[j] = int32_t(stream.size() / 2);
+                    for (auto &e : per[size_t(j)][size_t(i)]) {
+                        stream.push_back(e.first);
+                        stream.push_back(e.second);
+                    }
+                }
+                sp[nslot] = int32_t(stream.size() / 2);
+                max_region = std::max(max_region, int64_t(sp[nslot]) - r0);
+            }
         }
-        while (chunk < g.nchunks) cp[++chunk] = int32_t(pos);
     }
-    p->off_nz = 0;
-    p->off_chunkptr = align_up(size_t(nnz) * sizeof(Nz), 256);
-    p->off_perm = align_up(p->off_chunkptr + chunkptr.size() * 4, 256);
+    if (stream.size() / 2 >= (size_t(1) << 31))
+        return fail(SKC_ERR_OVERFLOW, "direct stream too large");
+    // pixel-slot tables per band
+    const int T = p->T;
+    std::vector<int32_t> slotq(size_t(g.nbands) * T * 32), slotout(slotq.size());
+    const int64_t img_elems = int64_t(p->K) * p->Ho * p->Wo;
+    if (img_elems * g.NI >= (int64_t(1) << 31))
+        return fail(SKC_ERR_OVERFLOW, "output too large for int32 slot offsets");
+    for (int b = 0; b < g.nbands; ++b) {
+        std::vector<std::vector<std::pair<int, int>>> bk;
+        band_slots(g.NI, g.img_stride, std::min(g.BH, p->Ho - b * g.BH), p->Wo, p->Wp,
+                   p->stride, &bk);
+        for (int t = 0; t < T; ++t)
+            for (int l = 0; l < 32; ++l) {
+                const size_t o = (size_t(b) * T + t) * 32 + l;
+                if (size_t(t) < bk[size_t(l)].size()) {
+                    const int q = bk[size_t(l)][size_t(t)].first;
+                    const int code = bk[size_t(l)][size_t(t)].second;
+                    const int img = code >> 24, yl = (code >> 12) & 0xfff, x = code & 0xfff;
+                    slotq[o] = q;
+                    slotout[o] = int32_t(img * img_elems + int64_t(yl) * p->Wo + x);
+                } else {
+                    slotq[o] = l;  // empty slot: a conflict-free dummy read, never stored
+                    slotout[o] = -1;
+                }
+            }
+    }
+    g.NS = 1;
+    const int stream_cap = int(align_up(size_t(max_region) + 2, 2));
+    const int slab = g.NI * g.img_stride;
+    g.stage_floats = slab + 2 * stream_cap + 32;  // +32: empty slots read off + lane
+    const size_t stage_bytes = size_t(g.stage_floats) * 4;
+    g.NS = int(std::min<size_t>(4, std::max<size_t>(1, kSmemBudget / stage_bytes)));
+    g.NS = std::min(g.NS, std::max(1, g.nchunks));
+    if (size_t(g.NS) * stage_bytes + 2 * kMaxStages * 8 > (227u << 10))
+        return fail(SKC_ERR_UNSUPPORTED, "direct stage of %zu B does not fit", stage_bytes);
+    p->smem = size_t(g.NS) * stage_bytes + 2 * kMaxStages * sizeof(uint64_t);
+    p->dp = DirectParams{};
+    DirectParams &d = p->dp;
+    d.C = p->C; d.K = p->K; d.Kg = p->Kg; d.Cg = p->Cg; d.Hp = p->Hp; d.Wp = p->Wp;
+    d.Ho = p->Ho; d.Wo = p->Wo; d.stride = p->stride; d.groups = p->groups;
+    d.NI = g.NI; d.BH = g.BH; d.BHin = g.BHin; d.nbands = g.nbands; d.CB = g.CB;
+    d.nchunks = g.nchunks; d.NS = g.NS; d.chan_stride = g.chan_stride;
+    d.img_stride = g.img_stride; d.slab_floats = slab; d.stream_cap = stream_cap;
+    d.stage_floats = g.stage_floats; d.bulk = g.bulk; d.whole = g.whole;
+    d.NW = p->NW; d.M = p->M; d.cblocks = p->cblocks;
+    // device image: stream | segptr | chan | slotq | slotout | perm
+    p->off_stream = 0;
+    p->off_segoff = align_up(stream.size() * 4, 256);
+    p->off_chan = align_up(p->off_segoff + segptr.size() * 4, 256);
+    p->off_lanemap = align_up(p->off_chan + chan.size() * 4, 256);      // slotq
+    p->off_chunkptr = align_up(p->off_lanemap + slotq.size() * 4, 256);  // slotout
+    p->off_perm = align_up(p->off_chunkptr + slotout.size() * 4, 256);
     const size_t total = align_up(p->off_perm + size_t(p->K) * 4, 256);
     p->image.assign(total, 0);
-    if (nnz) std::memcpy(p->image.data() + p->off_nz, nz.data(), size_t(nnz) * sizeof(Nz));
-    std::memcpy(p->image.data() + p->off_chunkptr, chunkptr.data(), chunkptr.size() * 4);
+    if (!stream.empty())
+        std::memcpy(p->image.data() + p->off_stream, stream.data(), stream.size() * 4);
+    std::memcpy(p->image.data() + p->off_segoff, segptr.data(), segptr.size() * 4);
+    std::memcpy(p->image.data() + p->off_chan, chan.data(), chan.size() * 4);
+    std::memcpy(p->image.data() + p->off_lanemap, slotq.data(), slotq.size() * 4);
+    std::memcpy(p->image.data() + p->off_chunkptr, slotout.data(), slotout.size() * 4);
     std::memcpy(p->image.data() + p->off_perm, p->perm.data(), size_t(p->K) * 4);
     return SKC_OK;
 }
@@ -662,10 +727,10 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.band_rows = p->sg.BH; i.chunk_channels = p->sg.CB; i.stages = p->sg.NS;
     i.warps = p->NW; i.channels_per_warp = p->M; i.pixels_per_lane = p->T;
     i.smem_bytes = p->smem;
-    i.lane_mapping = p->pitch;
+    i.lane_mapping = p->kernel == SKC_KERNEL_DIRECT ? p->sg.NI : 0;
     i.tile_h = p->kernel == SKC_KERNEL_REGTILE ? p->rsh.TY : 0;
     i.tile_w = p->kernel == SKC_KERNEL_REGTILE ? p->rsh.TX : 0;
-    i.images_per_cta = p->kernel == SKC_KERNEL_REGTILE ? p->rp.NI : 1;
+    i.images_per_cta = p->kernel == SKC_KERNEL_REGTILE ? p->rp.NI : p->sg.NI;
     return ok();
 }
 
@@ -734,18 +799,16 @@ skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *
             return fail(SKC_ERR_CUDA, "regtile launch: %s", cudaGetErrorString(e));
         return ok();
     }
-    DirectParams dp{};
-    dp.g = p->sg;
-    dp.g.N = N;
+    DirectParams dp = p->dp;
+    dp.N = N;
     dp.in = d_in;
     dp.out = d_out;
-    dp.nz = reinterpret_cast<const Nz *>(ws + p->off_nz);
-    dp.chunkptr = reinterpret_cast<const int32_t *>(ws + p->off_chunkptr);
-    dp.perm = reinterpret_cast<const int32_t *>(ws + p->off_perm);
-    dp.NW = p->NW;
-    dp.M = p->M;
-    dp.cblocks = p->cblocks;
-    cudaError_t e = launch_direct(dp, p->T, p->pitch != 0, p->smem, (cudaStream_t)stream);
+    dp.stream = reinterpret_cast<const uint2 *>(ws + p->off_stream);
+    dp.segptr = reinterpret_cast<const int32_t *>(ws + p->off_segoff);
+    dp.chan = reinterpret_cast<const int32_t *>(ws + p->off_chan);
+    dp.slotq = reinterpret_cast<const int32_t *>(ws + p->off_lanemap);
+    dp.slotout = reinterpret_cast<const int32_t *>(ws + p->off_chunkptr);
+    cudaError_t e = launch_direct(dp, p->T, p->smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "conv launch: %s", cudaGetErrorString(e));
     return ok();
 }

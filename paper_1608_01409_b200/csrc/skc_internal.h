@@ -17,34 +17,31 @@ struct Nz {
     int32_t off;
 };
 
-// Geometry of the staging pipeline shared by both conv kernels.
-//  - A work item is (image n, output-row band, block of output channels of one group).
-//  - Input channels of the group are staged CB at a time ("column blocking")
-//    into a ring of NS shared-memory stages; each stage holds CB channels x BHin rows x Wp.
-struct StageGeom {
-    int N, C, K, Kg, Cg, Hp, Wp, Ho, Wo, stride;
-    int BH;         // output rows per band
-    int BHin;       // input rows staged per band = (BH-1)*stride + R
-    int nbands;
-    int CB;         // input channels per stage
-    int nchunks;    // ceil(Cg / CB)
-    int NS;         // stages in the ring
-    int stage_floats;  // floats per stage (multiple of 4)
-    int tail_floats;   // slack after the last stage: junk lane slots may read past a stage
-    int bulk;       // 1: cp.async.bulk (TMA) staging; 0: LSU copy fallback
-    int whole;      // 1: band covers all Hp rows -> one bulk copy per stage
-};
-
+// Direct kernel (sconv_direct.cu).  CTA = (group of NI images, output-row band, block of
+// NW*M output channels of one conv group); NW compute warps + 1 producer warp.  The
+// producer stages CB input channels of the band for the NI images, plus the (w, off) stream
+// of the block's channels for that chunk, per stage of an NS-deep mbarrier ring.  Each lane
+// owns T output-pixel "slots" (slotq/slotout, built on the host): slot (t, lane) reads shared
+// word off + slotq[t][lane], and slotq[t][lane] == lane (mod 32), so every load of a warp
+// touches 32 distinct banks whatever the nonzero's offset.
 struct DirectParams {
-    StageGeom g;
-    const float *in;       // padded input [N][C][Hp][Wp]
-    float *out;            // [N][K][Ho][Wo]
-    const Nz *nz;          // streams in perm order, chunk-major inside each row
-    const int32_t *chunkptr;  // [K][nchunks+1] absolute indices into nz
-    const int32_t *perm;   // perm position -> output channel
-    int NW;                // compute warps per CTA
-    int M;                 // channels per warp
-    int cblocks;           // channel blocks per group = ceil(Kg / (NW*M))
+    const float *in;          // padded input [N][C][Hp][Wp]
+    float *out;               // [N][K][Ho][Wo]
+    const uint2 *stream;      // {w bits, off} per nonzero, regions per (block, chunk)
+    const int32_t *segptr;    // [gblocks][nchunks][NW*M + 1] absolute uint2 index
+    const int32_t *chan;      // [gblocks][NW*M] output channel (slot j = m*NW + warp) or -1
+    const int32_t *slotq;     // [nbands][T][32] smem word offset of the slot (or lane: empty)
+    const int32_t *slotout;   // [nbands][T][32] img*K*Ho*Wo + yl*Wo + x, or -1 (empty)
+    int N, C, K, Kg, Cg, Hp, Wp, Ho, Wo, stride, groups;
+    int NI, BH, BHin, nbands, CB, nchunks, NS;
+    int chan_stride;          // floats between channels inside an image slot
+    int img_stride;           // floats between image slots (multiple of 4)
+    int slab_floats;          // NI * img_stride
+    int stream_cap;           // uint2 entries of a stage's stream area
+    int stage_floats;         // slab_floats + 2 * stream_cap
+    int bulk;                 // 1: TMA bulk copies; 0: LSU copy fallback (misaligned planes)
+    int whole;                // band = all Hp rows: one copy per image per chunk
+    int NW, M, cblocks;
 };
 
 // Register-tiled kernel (sconv_regtile.cu).  A CTA = (group of NI images, block of NT
@@ -78,8 +75,7 @@ struct RegtileShape {
 // Launchers (defined in the .cu files).  Return cudaError_t of the launch.
 cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int W, int pad,
                        cudaStream_t st);
-cudaError_t launch_direct(const DirectParams &p, int T, bool pitch, size_t smem,
-                          cudaStream_t st);
+cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st);
 bool direct_supported(int T, int M);
 cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_t smem,
                            cudaStream_t st);
