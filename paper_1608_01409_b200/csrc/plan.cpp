@@ -236,17 +236,24 @@ skc_status build_direct_image(skc_plan *p) {
             }
             for (int i = 0; i < g.nchunks; ++i) {
                 if (stream.size() % 4) stream.resize(align_up(stream.size(), 4), 0);  // 16 B
+                // region = [segment table: nslot+1 int32 offsets (entries, region-relative),
+                //            padded to whole uint2] [ {w, off} entries of slot 0, 1, ... ]
                 int32_t *sp = &segptr[(size_t(gb) * g.nchunks + i) * (nslot + 1)];
-                const int64_t r0 = int64_t(stream.size() / 2);
-                for (int j = 0; j < nslot; ++j) {
-                    sp[j] = int32_t(stream.size() / 2);
+                const size_t r0 = stream.size() / 2;
+                const size_t hdr = size_t(nslot + 2) / 2;
+                stream.resize(stream.size() + 2 * hdr, 0);
+                for (int j = 0; j <= nslot; ++j) {
+                    const size_t at = stream.size() / 2;
+                    stream[2 * r0 + size_t(j)] = uint32_t(at - r0);
+                    sp[j] = int32_t(at);
+                    if (j == nslot) break;
                     for (auto &e : per[size_t(j)][size_t(i)]) {
                         stream.push_back(e.first);
                         stream.push_back(e.second);
                     }
                 }
-                sp[nslot] = int32_t(stream.size() / 2);
-                max_region = std::max(max_region, int64_t(sp[nslot]) - r0);
+                sp[0] = int32_t(r0);  // region start (the producer copies from here)
+                max_region = std::max(max_region, int64_t(stream.size() / 2 - r0));
             }
         }
     }
@@ -498,9 +505,14 @@ skc_status build_regtile(skc_plan *p, const RtCandidate &c) {
             for (int i = 0; i < nchunks; ++i) {
                 if (stream.size() % 4) stream.resize(align_up(stream.size(), 4), 0);  // 16 B
                 int32_t *so = &segoff[((size_t(g) * nb + b) * nchunks + i) * (NT + 1)];
+                // region = [segment table: NT+1 int32 region-relative entry offsets, padded
+                //            to whole uint2] [segment of task 0] [task 1] ...
                 const int64_t region0 = int64_t(stream.size() / 2);
+                const size_t hdr = size_t(NT + 2) / 2;
+                stream.resize(stream.size() + 2 * hdr, 0);
                 for (int t = 0; t < NT; ++t) {
                     so[t] = int32_t(stream.size() / 2);
+                    stream[2 * size_t(region0) + size_t(t)] = uint32_t(so[t] - region0);
                     auto &ops = per[size_t(t)][size_t(i)];
                     std::stable_sort(ops.begin(), ops.end(), [](const Op &a, const Op &b2) {
                         return a.cl != b2.cl ? a.cl < b2.cl : a.m != b2.m ? a.m < b2.m
@@ -522,6 +534,8 @@ skc_status build_regtile(skc_plan *p, const RtCandidate &c) {
                     stream.push_back(uint32_t(ncase + 1));  // EXIT
                 }
                 so[NT] = int32_t(stream.size() / 2);
+                stream[2 * size_t(region0) + size_t(NT)] = uint32_t(so[NT] - region0);
+                so[0] = int32_t(region0);  // region start (fill_stage copies from here)
                 max_region = std::max(max_region, int64_t(so[NT]) - region0);
             }
         }

@@ -13,7 +13,8 @@
 //     LSU copies by the same warp.  Padding is already materialised (skc_pad_input).
 //   - a4: warp w owns channel slots j = m*NW + w (perm order, so nnz-sorted channels
 //     interleave across warps); per nonzero ONE broadcast LDS.64 of {w, off} from the staged
-//     stream ("reused for every pixel").
+//     stream ("reused for every pixel").  Each staged region starts with
+//     its segment table (region-relative entry offsets of every slot).
 //   - a5: each lane owns T pixel slots; slot (t, lane) sits at shared word slotq[t][lane],
 //     chosen on the host so that slotq[t][lane] == lane (mod 32): acc[m][t] += w *
 //     stage[off + slotq[t]] touches 32 distinct banks for ANY off -- in[off + f(0,y,x)] of
@@ -129,12 +130,11 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
         mbar_wait(&full[s], uint32_t(i / p.NS) & 1u);
         const float *sm = smem + size_t(s) * p.stage_floats;
         const uint2 *st = reinterpret_cast<const uint2 *>(sm + p.slab_floats);
-        const int32_t *sp = p.segptr + (int64_t(gb) * p.nchunks + i) * (nslot + 1);
-        const int32_t base = __ldg(sp);
+        const int *seg = reinterpret_cast<const int *>(st);  // staged segment table
 #pragma unroll
         for (int m = 0; m < M; ++m) {
             const int j = m * NW + warp;
-            const int b = __ldg(sp + j) - base, e = __ldg(sp + j + 1) - base;
+            const int b = seg[j], e = seg[j + 1];
 #pragma unroll 2
             for (int idx = b; idx < e; ++idx) {
                 const uint2 pr = st[idx];  // same address in every lane: broadcast

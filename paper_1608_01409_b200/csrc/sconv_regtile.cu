@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
         const int s = i % p.NS;
         float *stage = smem + size_t(s) * p.stage_floats;
         mbar_wait(&full[s], uint32_t(i / p.NS) & 1u);
-        const int32_t *so = p.segoff + (int64_t(bidx) * p.nchunks + i) * (p.NT + 1);
-        const int32_t off = __ldg(so + t) - __ldg(so);
+        // staged segment table: region-relative entry offset of this warp's task
+        const int32_t off = reinterpret_cast<const int32_t *>(stage + p.slab_floats)[t];
         // the warp's segment: HDR / FMA ops ... EXIT, dispatched in registers (regtile_gen.inc)
         rt_dispatch<R, S, TY, TX, M>(acc, win, smem_u32(stage + p.slab_floats) + uint32_t(off) * 8u,
                                      smem_u32(stage + lbase), wp4);
