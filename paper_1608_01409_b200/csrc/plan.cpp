@@ -128,6 +128,28 @@ int band_slots(int NI, int IS, int rows, int Wo, int Wp, int stride,
     return int(T);
 }
 
+// TMA bulk-copy legality of a direct-kernel staging layout: 16-byte aligned sources,
+// destinations and sizes for every (image, chunk, band) copy.
+bool bulk_legal(const skc_plan *p, int NI, int BH, int BHin, int nbands, bool whole, int CB,
+                int chan_stride, int IS) {
+    (void)NI;
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    bool bulk = (int64_t(p->C) * plane) % 4 == 0 && (int64_t(p->Cg) * plane) % 4 == 0 &&
+                IS % 4 == 0;
+    if (whole) {
+        bulk = bulk && (int64_t(CB) * plane) % 4 == 0 &&
+               (int64_t(p->Cg % CB ? p->Cg % CB : CB) * plane) % 4 == 0;
+    } else {
+        bulk = bulk && plane % 4 == 0 && (int64_t(BH) * p->stride * p->Wp) % 4 == 0 &&
+               chan_stride % 4 == 0;
+        for (int b = 0; b < nbands && bulk; ++b) {
+            const int row0 = b * BH * p->stride;
+            bulk = (int64_t(std::min(BHin, p->Hp - row0)) * p->Wp) % 4 == 0;
+        }
+    }
+    return bulk;
+}
+
 // Pick the direct kernel's images per CTA (NI), band height, image-slot stride, pixel slots
 // per lane (T), channel chunk and warp layout.  Cost per nonzero per image, in shared-memory
 // wavefronts: bands * (T loads + 1 broadcast) / NI; the cheapest candidate wins.
@@ -161,7 +183,16 @@ skc_status configure_direct(skc_plan *p) {
                     T = std::max(T, band_slots(NI, IS, std::min(BH, Ho - b * BH), Wo, p->Wp,
                                                p->stride, nullptr));
                 if (T > 16) continue;
-                const double cost = double(nb) * (T + 1) / NI + 1e-3 * NI + 1e-4 * nb;
+                // per nonzero and image: T loads + 1 broadcast per band (wavefront-cycles)
+                double cost = double(nb) * (T + 1) / NI + 1e-3 * NI + 1e-4 * nb;
+                if (!bulk_legal(p, NI, BH, BHin, nb, whole, CB, chan_stride, IS)) {
+                    // cp.async fallback: ~8 cycles per 32 staged words, repeated by every
+                    // channel block; expressed per nonzero of the layer
+                    const int M = T <= 8 ? 4 : 2;
+                    const double blocks = std::ceil(double(p->Kg) / (kDirectNW * M)) * p->groups;
+                    const double words = double(nb) * BHin * p->Wp * p->C * blocks;
+                    cost += words / 32.0 * 8.0 / std::max<double>(1.0, double(p->colidx.size()));
+                }
                 if (cost < best_cost) {
                     best_cost = cost;
                     g.NI = NI; g.BH = BH; g.nbands = nb; g.BHin = BHin; g.whole = whole;
@@ -174,20 +205,8 @@ skc_status configure_direct(skc_plan *p) {
         return fail(SKC_ERR_UNSUPPORTED, "no band/slot tiling fits the direct kernel (Wo=%d)", Wo);
     p->direct_waves = double(g.nbands) * (p->T + 1) / g.NI;
     g.nchunks = (p->Cg + g.CB - 1) / g.CB;
-    // TMA bulk-copy legality: 16-byte aligned sources, destinations and sizes
-    bool bulk = (int64_t(g.C) * plane) % 4 == 0 && (int64_t(g.Cg) * plane) % 4 == 0 &&
-                g.img_stride % 4 == 0;
-    if (g.whole) {
-        bulk = bulk && (int64_t(g.CB) * plane) % 4 == 0 &&
-               (int64_t(g.Cg % g.CB ? g.Cg % g.CB : g.CB) * plane) % 4 == 0;
-    } else {
-        bulk = bulk && plane % 4 == 0 && (int64_t(g.BH) * p->stride * g.Wp) % 4 == 0 &&
-               g.chan_stride % 4 == 0;
-        for (int b = 0; b < g.nbands && bulk; ++b) {
-            const int row0 = b * g.BH * p->stride;
-            bulk = (int64_t(std::min(g.BHin, g.Hp - row0)) * g.Wp) % 4 == 0;
-        }
-    }
+    const bool bulk = bulk_legal(p, g.NI, g.BH, g.BHin, g.nbands, g.whole, g.CB, g.chan_stride,
+                                 g.img_stride);
     g.bulk = bulk ? 1 : 0;
     p->NW = kDirectNW;
     p->M = p->T <= 8 ? 4 : (p->T <= 16 ? 2 : 1);

@@ -50,6 +50,19 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// 4-byte asynchronous global -> shared copy (LDGSTS), completion tracked per thread.
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+
+// Arrive on `bar` once all of this thread's prior cp.async copies have completed; the
+// arrival is pre-counted in the barrier's initial count (.noinc).
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
 // Division by a runtime-constant divisor d (1 <= d < 2^31) for n < 2^31: q = (mulhi(n,m)+n)>>s.
 struct FastDiv {
     uint32_t d, m, s;

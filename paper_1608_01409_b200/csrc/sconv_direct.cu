@@ -9,8 +9,9 @@
 //   - a3: the producer warp stages CB input channels of the band for the NI images, and the
 //     block's (w, off) stream for that chunk, into a ring of NS shared-memory stages with TMA
 //     bulk copies (cp.async.bulk ... mbarrier::complete_tx) -- column blocking.
-//     Consumers release a stage with an mbarrier arrive.  Misaligned planes fall back to
-//     LSU copies by the same warp.  Padding is already materialised (skc_pad_input).
+//     Consumers release a stage with an mbarrier arrive.  Planes that are not 16-byte
+//     multiples fall back to 4-byte cp.async copies that complete on the same barrier.
+//     Padding is already materialised (skc_pad_input).
 //   - a4: warp w owns channel slots j = m*NW + w (perm order, so nnz-sorted channels
 //     interleave across warps); per nonzero ONE broadcast LDS.64 of {w, off} from the staged
 //     stream ("reused for every pixel").  Each staged region starts with
@@ -58,6 +59,13 @@ __device__ __forceinline__ void produce(const DirectParams &p, float *dst, uint6
         }
         if (lane == 0 && len) bulk_g2s(sdst, p.stream + s0, uint32_t(len) * 8u, bar);
     } else {
+        // planes not 16-byte aligned: 4-byte cp.async copies by all 32 lanes, each lane's
+        // completion arriving on the stage barrier (initial count 33 = 32 lanes + lane 0's
+        // expect_tx for the stream region, which is always 16-byte aligned)
+        if (lane == 0) {
+            mbar_arrive_expect_tx(bar, uint32_t(len) * 8u);
+            if (len) bulk_g2s(sdst, p.stream + s0, uint32_t(len) * 8u, bar);
+        }
         const int cnt = rows * p.Wp;
         for (int j = 0; j < nimg; ++j) {
             const float *src = p.in + (int64_t(n0 + j) * p.C + int64_t(gi) * p.Cg + c0) * plane +
@@ -65,13 +73,9 @@ __device__ __forceinline__ void produce(const DirectParams &p, float *dst, uint6
             float *d = dst + j * p.img_stride;
             for (int c = 0; c < cn; ++c)
                 for (int e = lane; e < cnt; e += 32)
-                    d[c * p.chan_stride + e] = __ldg(src + int64_t(c) * plane + e);
+                    cp_async4(d + c * p.chan_stride + e, src + int64_t(c) * plane + e);
         }
-        uint2 *sd = reinterpret_cast<uint2 *>(sdst);
-        for (int e = lane; e < len; e += 32) sd[e] = __ldg(p.stream + s0 + e);
-        __threadfence_block();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar);
+        cp_async_mbar_arrive(bar);
     }
 }
 
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.NS; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], p.bulk ? 1 : 33);
             mbar_init(&empty[s], NW);
         }
         mbar_fence_init();
