@@ -76,7 +76,8 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
-    def __enter__(self):
+    def start(self):
+        """Launch nvidia-smi and wait (<= 5 s) for its first sample, before timing starts."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
@@ -84,8 +85,21 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5 and self.proc.poll() is None:
+                time.sleep(0.01)
         except (FileNotFoundError, OSError):
             self.proc = None
+        return self
+
+    def mark(self):
+        """Start of the timed region: only samples after this count."""
+        self.lines.clear()
+
+    def __enter__(self):
+        if self.proc is None:
+            self.start()
+        self.mark()
         return self
 
     def _read(self):
@@ -245,6 +259,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             if evs is not None:
                 evs[2 * i + 2].record(stream)
 
+    clk = ClockSampler(local_rank).start()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -255,7 +270,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with clk:
         for _ in range(args.steps):
             flush.fill_(1)  # L2 flush between timed steps (outside the events)
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
