@@ -250,7 +250,7 @@ skc_status build_direct_image(skc_plan *p) {
                     uint32_t wb;
                     std::memcpy(&wb, &p->values[e], 4);
                     const int off = (cl % g.CB) * g.chan_stride + r * p->Wp + s;
-                    per[size_t(j)][size_t(cl / g.CB)].emplace_back(wb, uint32_t(off));
+                    per[size_t(j)][size_t(cl / g.CB)].emplace_back(wb, uint32_t(off) * 4u);
                 }
             }
             for (int i = 0; i < g.nchunks; ++i) {

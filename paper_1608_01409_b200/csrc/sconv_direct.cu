@@ -29,6 +29,12 @@
 namespace skc {
 namespace {
 
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 // Producer: stage chunk i (input band of NI images + the block's stream region) into `dst`.
 __device__ __forceinline__ void produce(const DirectParams &p, float *dst, uint64_t *bar, int i,
                                         int n0, int gi, int gb, int row0, int lane) {
@@ -122,11 +128,14 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
     const int32_t *sq = p.slotq + (int64_t(band) * T) * 32 + lane;
 #pragma unroll
     for (int t = 0; t < T; ++t) q[t] = __ldg(sq + t * 32);
-    float acc[M][T];
+    // accumulators as float2 pairs of slots: one packed FFMA2 (fma.rn.f32x2, sm_100) per two
+    // slots -- two independent round-to-nearest FMAs, bit-identical to two fmaf()
+    constexpr int T2 = (T + 1) / 2;
+    float2 acc[M][T2];
 #pragma unroll
     for (int m = 0; m < M; ++m)
 #pragma unroll
-        for (int t = 0; t < T; ++t) acc[m][t] = 0.0f;
+        for (int t = 0; t < T2; ++t) acc[m][t] = make_float2(0.0f, 0.0f);
     const int nslot = NW * M;
 
     for (int i = 0; i < p.nchunks; ++i) {
@@ -134,6 +143,10 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
         mbar_wait(&full[s], uint32_t(i / p.NS) & 1u);
         const float *sm = smem + size_t(s) * p.stage_floats;
         const uint2 *st = reinterpret_cast<const uint2 *>(sm + p.slab_floats);
+        uint32_t qb[T];  // shared byte address of every slot in this stage
+        const uint32_t sbase = smem_u32(sm);
+#pragma unroll
+        for (int t = 0; t < T; ++t) qb[t] = sbase + uint32_t(q[t]) * 4u;
         const int *seg = reinterpret_cast<const int *>(st);  // staged segment table
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -143,9 +156,14 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
             for (int idx = b; idx < e; ++idx) {
                 const uint2 pr = st[idx];  // same address in every lane: broadcast
                 const float w = __uint_as_float(pr.x);
-                const float *src = sm + int(pr.y);
+                const float2 w2 = make_float2(w, w);
+                const uint32_t ob = pr.y;  // byte offset of (c, r, s) in the stage
 #pragma unroll
-                for (int t = 0; t < T; ++t) acc[m][t] = fmaf(w, src[q[t]], acc[m][t]);
+                for (int u = 0; u < T2; ++u) {
+                    const float a = lds_f32(qb[2 * u] + ob);
+                    const float b = (2 * u + 1 < T) ? lds_f32(qb[2 * u + 1] + ob) : 0.0f;
+                    acc[m][u] = __ffma2_rn(w2, make_float2(a, b), acc[m][u]);
+                }
             }
         }
         __syncwarp();
@@ -164,7 +182,8 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             const int off = __ldg(so + t * 32);
-            if (off >= 0 && off / img_elems < nimg) o[off] = acc[m][t];
+            const float v = (t & 1) ? acc[m][t / 2].y : acc[m][t / 2].x;
+            if (off >= 0 && off / img_elems < nimg) o[off] = v;
         }
     }
 }
