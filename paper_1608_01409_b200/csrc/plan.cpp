@@ -210,6 +210,9 @@ skc_status configure_direct(skc_plan *p) {
     g.bulk = bulk ? 1 : 0;
     p->NW = kDirectNW;
     p->M = p->T <= 8 ? 4 : (p->T <= 16 ? 2 : 1);
+    // tuning overrides (benchmarks): SKC_DIRECT_NW (compute warps, 1..16), SKC_DIRECT_M
+    if (const char *e = std::getenv("SKC_DIRECT_NW")) p->NW = std::max(1, std::min(16, std::atoi(e)));
+    if (const char *e = std::getenv("SKC_DIRECT_M")) p->M = std::max(1, std::min(4, std::atoi(e)));
     while (p->M > 1 && p->NW * p->M > p->Kg * 2) p->M /= 2;
     if (!direct_supported(p->T, p->M))
         return fail(SKC_ERR_UNSUPPORTED, "no direct kernel instance for T=%d M=%d", p->T, p->M);

@@ -208,9 +208,9 @@ cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
 #define SKC_DIRECT_CASES(X) \
     X(1, 1) X(1, 2) X(1, 4) X(2, 1) X(2, 2) X(2, 4) X(3, 1) X(3, 2) X(3, 4) X(4, 1) \
     X(4, 2) X(4, 4) X(5, 1) X(5, 2) X(5, 4) X(6, 1) X(6, 2) X(6, 4) X(7, 1) X(7, 2) \
-    X(7, 4) X(8, 1) X(8, 2) X(8, 4) X(9, 1) X(9, 2) X(10, 1) X(10, 2) X(11, 1) X(11, 2) \
-    X(12, 1) X(12, 2) X(13, 1) X(13, 2) X(14, 1) X(14, 2) X(15, 1) X(15, 2) X(16, 1) \
-    X(16, 2)
+    X(7, 4) X(8, 1) X(8, 2) X(8, 4) X(9, 1) X(9, 2) X(9, 4) X(10, 1) X(10, 2) X(10, 4) \
+    X(11, 1) X(11, 2) X(11, 4) X(12, 1) X(12, 2) X(12, 4) X(13, 1) X(13, 2) X(13, 4) \
+    X(14, 1) X(14, 2) X(14, 4) X(15, 1) X(15, 2) X(15, 4) X(16, 1) X(16, 2) X(16, 4)
 
 }  // namespace
 
