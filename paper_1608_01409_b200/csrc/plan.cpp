@@ -420,32 +420,62 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
     }
     if (p->Cg % CB && ((int64_t(p->Cg % CB) * plane) % 4)) return false;  // last chunk copy
     c.CB = CB;
-    // lane map: tiles in (image, tile-row, tile-col) order, 32 per lane group
-    c.lanemap.assign(size_t(c.NG) * 32, -1);
-    for (int i = 0; i < total; ++i) {
-        const int img = i / tiles, rem = i % tiles;
-        const int y0 = (rem / ntx) * sh.TY, x0 = (rem % ntx) * sh.TX;
-        c.lanemap[size_t(i)] = (img << 24) | (y0 << 12) | x0;
-    }
-    // image-slot stride: pad (multiple of 4 words) that minimises window-load bank conflicts
+    // Lane map.  Every window load of a warp reads word (tile base + const), so its bank
+    // conflicts are those of the tile bases mod 32.  Tiles are dealt to lane groups greedily
+    // by bank (a tile goes to the group where its bank is least used), for each candidate
+    // image-slot padding; the layout with the fewest conflicts wins.
     const int base = int(align_up(size_t(CB) * size_t(plane), 4));
-    int best_pad = 0, best_wf = 1 << 30;
-    for (int pad = 0; pad < 32; pad += 4) {
+    int best_wf = 1 << 30;
+    for (int pad = 0; pad < (c.NI > 1 ? 32 : 4); pad += 4) {
+        const int IS = base + pad;
+        std::vector<int32_t> lm(size_t(c.NG) * 32, -1);
+        std::vector<std::vector<int>> used(size_t(c.NG), std::vector<int>(32, 0));
+        std::vector<int> fill(size_t(c.NG), 0);
+        // visit tiles bank by bank, fullest bank first, so each bank's tiles spread across
+        // the groups (achieves max_b ceil(count_b / NG) whenever the capacities allow)
+        std::vector<int> order(static_cast<size_t>(total)), bank_of(static_cast<size_t>(total));
+        std::vector<int> cnt(32, 0);
+        for (int i = 0; i < total; ++i) {
+            const int img = i / tiles, rem = i % tiles;
+            bank_of[size_t(i)] = (img * IS + (rem / ntx) * sh.TY * p->Wp + (rem % ntx) * sh.TX) & 31;
+            cnt[size_t(bank_of[size_t(i)])]++;
+            order[size_t(i)] = i;
+        }
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b2) {
+            const int ba = bank_of[size_t(a)], bb = bank_of[size_t(b2)];
+            return cnt[size_t(ba)] != cnt[size_t(bb)] ? cnt[size_t(ba)] > cnt[size_t(bb)] : ba < bb;
+        });
+        for (int i : order) {
+            const int img = i / tiles, rem = i % tiles;
+            const int y0 = (rem / ntx) * sh.TY, x0 = (rem % ntx) * sh.TX;
+            const int bank = bank_of[size_t(i)];
+            int gbest = -1;
+            for (int g = 0; g < c.NG; ++g) {
+                if (fill[size_t(g)] >= 32) continue;
+                if (gbest < 0 || used[size_t(g)][size_t(bank)] < used[size_t(gbest)][size_t(bank)] ||
+                    (used[size_t(g)][size_t(bank)] == used[size_t(gbest)][size_t(bank)] &&
+                     fill[size_t(g)] < fill[size_t(gbest)]))
+                    gbest = g;
+            }
+            used[size_t(gbest)][size_t(bank)]++;
+            lm[size_t(gbest) * 32 + size_t(fill[size_t(gbest)]++)] = (img << 24) | (y0 << 12) | x0;
+        }
+        // idle lanes duplicate lane 0's tile (same word: a broadcast, never a conflict) and
+        // carry the idle flag (bit 30) so the epilogue skips them
+        for (int g = 0; g < c.NG; ++g)
+            for (int l = fill[size_t(g)]; l < 32; ++l)
+                lm[size_t(g) * 32 + size_t(l)] = (1 << 30) | lm[size_t(g) * 32];
         int wf = 0;
         for (int g = 0; g < c.NG; ++g) {
             std::vector<int> addr(32);
             for (int l = 0; l < 32; ++l) {
-                const int lm = c.lanemap[size_t(g) * 32 + l];
-                addr[l] = lm < 0 ? -1
-                                 : (lm >> 24) * (base + pad) + ((lm >> 12) & 0xfff) * p->Wp +
-                                       (lm & 0xfff);
+                const int v = lm[size_t(g) * 32 + l] & ~(1 << 30);
+                addr[size_t(l)] = ((v >> 24) & 0x3f) * IS + ((v >> 12) & 0xfff) * p->Wp + (v & 0xfff);
             }
             wf = std::max(wf, conflict_degree(addr));
         }
-        if (wf < best_wf) { best_wf = wf; best_pad = pad; }
-        if (c.NI == 1) break;  // a single image slot: padding cannot help
+        if (wf < best_wf) { best_wf = wf; c.img_stride = IS; c.lanemap = lm; }
     }
-    c.img_stride = base + best_pad;
     c.wf = best_wf;
     // tasks per CTA: keep the most warps resident per SM, fill the last block, and prefer
     // more tasks per CTA (each CTA re-reads its images' slabs: fewer blocks, less traffic)

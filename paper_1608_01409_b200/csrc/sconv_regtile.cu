@@ -75,10 +75,13 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
     __syncthreads();
 
     const int lg = warp % p.NG, t = warp / p.NG;
+    // lanemap: (img << 24) | (y0 << 12) | x0; bit 30 marks an idle lane (it mirrors an
+    // active lane's tile so its loads broadcast instead of conflicting, and stores nothing)
     const int lm = __ldg(p.lanemap + lg * 32 + lane);
-    const int img = lm >= 0 ? (lm >> 24) : 0;
-    const int y0 = lm >= 0 ? ((lm >> 12) & 0xfff) : 0;
-    const int x0 = lm >= 0 ? (lm & 0xfff) : 0;
+    const bool idle = (lm >> 30) & 1;
+    const int img = (lm >> 24) & 0x3f;
+    const int y0 = (lm >> 12) & 0xfff;
+    const int x0 = lm & 0xfff;
     const int lbase = img * p.img_stride + y0 * p.Wp + x0;
 
     float acc[M][TY][TX];
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
     }
 
     // a6: epilogue
-    if (lm < 0 || n0 + img >= p.N) return;
+    if (idle || n0 + img >= p.N) return;
     const int *ch = p.chan + (int64_t(bidx) * p.NT + t) * M;
 #pragma unroll
     for (int m = 0; m < M; ++m) {

@@ -57,7 +57,7 @@ struct RegtileParams {
     const uint2 *stream;     // op streams
     const int32_t *segoff;   // [groups*nblocks][nchunks][NT+1] absolute uint2 index
     const int32_t *chan;     // [groups*nblocks][NT][M] output channel or -1
-    const int32_t *lanemap;  // [NG][32] (img << 24) | (y0 << 12) | x0, or -1
+    const int32_t *lanemap;  // [NG][32] (img << 24) | (y0 << 12) | x0; bit 30 = idle lane
     int N, C, K, Cg, Kg, Hp, Wp, Ho, Wo, groups;
     int NI, CB, nchunks, NS;
     int img_stride;          // floats between image slots of a stage (multiple of 4)
