@@ -125,9 +125,14 @@ skc_status skc_pad_input(const skc_plan *plan, const float *d_in_nchw, float *d_
 skc_status skc_sparse_conv_forward(const skc_plan *plan, const float *d_in_padded,
                                    float *d_out, int N, void *stream);
 
-/* End-to-end helper used for the host-buffer measurement: H2D copy of h_in (host, ideally
- * pinned) into d_in, pad, conv, D2H copy of the result into h_out, all on `stream`.
- * Caller-owned scratch: d_in [N][C][H][W], d_in_padded, d_out.  Returns after enqueueing. */
+/* End-to-end entry with HOST buffers (the host-buffer measurement): h_in [N][C][H][W] ->
+ * h_out [N][K][Ho][Wo] (host memory; pinned for asynchronous overlap).  The batch is cut
+ * into image chunks; the H2D copy of a chunk, pad + conv of the previous one (on `stream`)
+ * and the D2H copy of the one before run concurrently on two internal copy streams.  The
+ * call returns after enqueueing; `stream` completes after the last D2H copy.  Caller-owned
+ * device scratch for the whole batch: d_in [N][C][H][W], d_in_padded, d_out.  Requires
+ * skc_plan_upload.  Errors: as skc_pad_input / skc_sparse_conv_forward, SKC_ERR_CUDA for
+ * stream/copy failures. */
 skc_status skc_forward_host(const skc_plan *plan, const float *h_in, float *h_out, int N,
                             float *d_in, float *d_in_padded, float *d_out, void *stream);
 

@@ -884,19 +884,63 @@ skc_status skc_forward_host(const skc_plan *p, const float *h_in, float *h_out, 
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
     if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
     if (N == 0) return ok();
-    if (!h_in || !h_out) return fail(SKC_ERR_ARG, "NULL host pointer");
+    if (!h_in || !h_out || !d_in || !d_pad || !d_out) return fail(SKC_ERR_ARG, "NULL pointer");
+    if (!p->d_ws) return fail(SKC_ERR_STATE, "plan not uploaded (call skc_plan_upload)");
+    // Pipeline over image chunks: H2D of chunk i+1 and D2H of chunk i-1 (two copy streams)
+    // overlap pad + conv of chunk i on the caller's stream; the caller's stream finally
+    // waits for the last D2H, so completion semantics are those of one stream.
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t in_bytes = size_t(N) * p->C * p->H * p->W * 4;
-    const size_t out_bytes = size_t(N) * p->K * p->Ho * p->Wo * 4;
-    cudaError_t e = cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "H2D: %s", cudaGetErrorString(e));
-    skc_status s = skc_pad_input(p, d_in, d_pad, N, stream);
-    if (s != SKC_OK) return s;
-    s = skc_sparse_conv_forward(p, d_pad, d_out, N, stream);
-    if (s != SKC_OK) return s;
-    e = cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "D2H: %s", cudaGetErrorString(e));
-    return ok();
+    const size_t in_img = size_t(p->C) * p->H * p->W;
+    const size_t pad_img = size_t(p->C) * p->Hp * p->Wp;
+    const size_t out_img = size_t(p->K) * p->Ho * p->Wo;
+    // chunks: a few per call, whole images, >= 8 images each
+    int nchunk = std::max(1, std::min(8, N / 8));
+    const int per = (N + nchunk - 1) / nchunk;
+    nchunk = (N + per - 1) / per;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev(size_t(2 * nchunk + 2), nullptr);
+    cudaError_t e = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
+    for (auto &x : ev)
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    skc_status result = SKC_OK;
+    if (e != cudaSuccess) result = fail(SKC_ERR_CUDA, "forward_host setup: %s", cudaGetErrorString(e));
+    // order the copies after whatever the caller already queued on its stream
+    if (result == SKC_OK) {
+        e = cudaEventRecord(ev[size_t(2 * nchunk)], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_in, ev[size_t(2 * nchunk)], 0);
+        if (e != cudaSuccess) result = fail(SKC_ERR_CUDA, "forward_host: %s", cudaGetErrorString(e));
+    }
+    for (int c = 0; c < nchunk && result == SKC_OK; ++c) {
+        const int n0 = c * per, n = std::min(per, N - n0);
+        e = cudaMemcpyAsync(d_in + n0 * in_img, h_in + n0 * in_img, n * in_img * 4,
+                            cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[size_t(2 * c)], s_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[size_t(2 * c)], 0);
+        if (e != cudaSuccess) { result = fail(SKC_ERR_CUDA, "H2D: %s", cudaGetErrorString(e)); break; }
+        result = skc_pad_input(p, d_in + n0 * in_img, d_pad + n0 * pad_img, n, stream);
+        if (result == SKC_OK)
+            result = skc_sparse_conv_forward(p, d_pad + n0 * pad_img, d_out + n0 * out_img, n, stream);
+        if (result != SKC_OK) break;
+        e = cudaEventRecord(ev[size_t(2 * c + 1)], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, ev[size_t(2 * c + 1)], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out + n0 * out_img, d_out + n0 * out_img, n * out_img * 4,
+                                cudaMemcpyDeviceToHost, s_out);
+        if (e != cudaSuccess) { result = fail(SKC_ERR_CUDA, "D2H: %s", cudaGetErrorString(e)); break; }
+    }
+    if (s_out) {
+        // the caller's stream completes only after the last D2H
+        cudaError_t e2 = cudaEventRecord(ev[size_t(2 * nchunk + 1)], s_out);
+        if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, ev[size_t(2 * nchunk + 1)], 0);
+        if (e2 != cudaSuccess && result == SKC_OK)
+            result = fail(SKC_ERR_CUDA, "forward_host join: %s", cudaGetErrorString(e2));
+    }
+    for (auto &x : ev)
+        if (x) cudaEventDestroy(x);  // deferred by the runtime until the event completes
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    return result == SKC_OK ? ok() : result;
 }
 
 int64_t skc_layout_offset(const skc_plan *p, int c, int y, int x) {

@@ -198,15 +198,20 @@ def test_determinism_and_host_path(kernel):
     a = conv.forward(xd).cpu().numpy()
     b = conv.forward(xd).cpu().numpy()
     np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
-    # end-to-end host-buffer entry point gives the same bits
-    h_in = torch.from_numpy(x).pin_memory()
-    h_out = torch.empty(conv.out_shape(8)).pin_memory()
-    d_in = torch.empty_like(xd)
-    d_pad = torch.empty(conv.padded_shape(8), device="cuda")
-    d_out = torch.empty(conv.out_shape(8), device="cuda")
-    skc.skc_forward_host(conv.plan, h_in, h_out, 8, d_in, d_pad, d_out)
-    torch.cuda.synchronize()
-    np.testing.assert_array_equal(h_out.numpy().view(np.uint32), a.view(np.uint32))
+    # end-to-end host-buffer entry point (chunk-pipelined over 2 copy streams, ragged last
+    # chunk) gives the same bits as the device path
+    n = 37
+    x2 = wl.gen_input(2, 1, layer, 0, n)
+    ref = conv.forward(torch.from_numpy(x2).cuda()).cpu().numpy()
+    h_in = torch.from_numpy(x2).pin_memory()
+    h_out = torch.full(conv.out_shape(n), float("nan")).pin_memory()
+    d_in = torch.empty(x2.shape, device="cuda")
+    d_pad = torch.empty(conv.padded_shape(n), device="cuda")
+    d_out = torch.empty(conv.out_shape(n), device="cuda")
+    skc.skc_forward_host(conv.plan, h_in, h_out, n, d_in, d_pad, d_out)
+    torch.cuda.current_stream().synchronize()
+    np.testing.assert_array_equal(h_out.numpy().view(np.uint32), ref.view(np.uint32))
+    np.testing.assert_array_equal(ref[:8].view(np.uint32), a.view(np.uint32))
     del rng
 
 
