@@ -140,6 +140,14 @@ skc_status skc_forward_host(const skc_plan *plan, const float *h_in, float *h_ou
  * Returns -1 when (c,y,x) is outside [0,C) x [0,Hp) x [0,Wp). */
 int64_t skc_layout_offset(const skc_plan *plan, int c, int y, int x);
 
+/* Static self-check of a plan (host only, no GPU): every kernel-private index the kernels
+ * will dereference -- shared-memory windows and pixel slots against the stage and allocation
+ * bounds, segment tables, op-stream structure (HDR before FMA ops, EXIT last) -- and that the
+ * kernel streams decode back EXACTLY to the canonical CSR (each nonzero once, same weight
+ * bits) and every output element is written exactly once.  SKC_OK or SKC_ERR_STATE with the
+ * first violation in skc_last_error(). */
+skc_status skc_plan_verify(const skc_plan *plan);
+
 void skc_plan_destroy(skc_plan *plan);
 const char *skc_last_error(void);
 

@@ -16,6 +16,7 @@
 #include <new>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <vector>
 
 using namespace skc;
@@ -813,6 +814,228 @@ skc_status skc_plan_perm(const skc_plan *p, const int32_t **perm) {
     if (!p || !perm) return fail(SKC_ERR_ARG, "NULL plan or perm");
     *perm = p->perm.data();
     return ok();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// Plan verifier: a static check of every kernel-private index the kernels dereference, and
+// an exact round trip of the kernel streams back to the canonical CSR.
+// ---------------------------------------------------------------------------------------
+namespace {
+
+struct NzKey {
+    int k, c, r, s;
+    uint32_t wbits;
+    bool operator<(const NzKey &o) const {
+        return std::tie(k, c, r, s, wbits) < std::tie(o.k, o.c, o.r, o.s, o.wbits);
+    }
+    bool operator==(const NzKey &o) const {
+        return k == o.k && c == o.c && r == o.r && s == o.s && wbits == o.wbits;
+    }
+};
+
+std::vector<NzKey> csr_keys(const skc_plan *p) {
+    std::vector<NzKey> v;
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    for (int k = 0; k < p->K; ++k)
+        for (int32_t j = p->rowptr[k]; j < p->rowptr[k + 1]; ++j) {
+            const int64_t col = p->colidx[j];
+            uint32_t wb;
+            std::memcpy(&wb, &p->values[j], 4);
+            v.push_back(NzKey{k, int(col / plane), int(col % plane / p->Wp), int(col % p->Wp), wb});
+        }
+    std::sort(v.begin(), v.end());
+    return v;
+}
+
+template <class T>
+const T *img_ptr(const skc_plan *p, size_t off) {
+    return reinterpret_cast<const T *>(p->image.data() + off);
+}
+
+skc_status verify_direct(const skc_plan *p) {
+    const DirectParams &d = p->dp;
+    const int nslot = d.NW * d.M, T = p->T;
+    const int gblocks = p->groups * d.cblocks;
+    const int32_t *segptr = img_ptr<int32_t>(p, p->off_segoff);
+    const int32_t *chan = img_ptr<int32_t>(p, p->off_chan);
+    const int32_t *slotq = img_ptr<int32_t>(p, p->off_lanemap);
+    const int32_t *slotout = img_ptr<int32_t>(p, p->off_chunkptr);
+    const uint32_t *stream = img_ptr<uint32_t>(p, p->off_stream);
+    const size_t stream_entries = p->off_segoff / 8;
+    // channel table: every output channel exactly once, in its own conv group
+    std::vector<int> seen(size_t(p->K), 0);
+    for (int gb = 0; gb < gblocks; ++gb)
+        for (int j = 0; j < nslot; ++j) {
+            const int k = chan[size_t(gb) * nslot + j];
+            if (k < -1 || k >= p->K) return fail(SKC_ERR_STATE, "verify: channel %d out of range", k);
+            if (k >= 0 && (seen[size_t(k)]++ || k / p->Kg != gb / d.cblocks))
+                return fail(SKC_ERR_STATE, "verify: channel %d placed twice or in the wrong group", k);
+        }
+    for (int k = 0; k < p->K; ++k)
+        if (!seen[size_t(k)]) return fail(SKC_ERR_STATE, "verify: channel %d never computed", k);
+    // slots: reads stay inside the stage, outputs cover every (image, y, x) exactly once
+    int qmax = 0;
+    const int64_t img_elems = int64_t(p->K) * p->Ho * p->Wo;
+    for (int b = 0; b < d.nbands; ++b) {
+        const int rows = std::min(d.BH, p->Ho - b * d.BH);
+        std::vector<int> cover(size_t(d.NI) * rows * p->Wo, 0);
+        for (int t = 0; t < T; ++t)
+            for (int l = 0; l < 32; ++l) {
+                const size_t o = (size_t(b) * T + t) * 32 + l;
+                const int q = slotq[o], out = slotout[o];
+                if ((q & 31) != l) return fail(SKC_ERR_STATE, "verify: slot bank %d != lane %d", q & 31, l);
+                if (q < 0) return fail(SKC_ERR_STATE, "verify: negative slot offset");
+                qmax = std::max(qmax, q);
+                if (out < 0) continue;
+                const int img = int(out / img_elems), rem = int(out % img_elems);
+                const int yl = rem / p->Wo, x = rem % p->Wo;
+                if (img >= d.NI || yl >= rows)
+                    return fail(SKC_ERR_STATE, "verify: slot output out of the band");
+                if (q != img * d.img_stride + yl * p->stride * p->Wp + x * p->stride)
+                    return fail(SKC_ERR_STATE, "verify: slot reads the wrong input pixel");
+                cover[(size_t(img) * rows + yl) * p->Wo + x]++;
+            }
+        for (int v : cover)
+            if (v != 1) return fail(SKC_ERR_STATE, "verify: output pixel covered %d times", v);
+    }
+    // streams: segment tables, bounds of every read, exact round trip to the CSR
+    std::vector<NzKey> got;
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    for (int gb = 0; gb < gblocks; ++gb)
+        for (int i = 0; i < d.nchunks; ++i) {
+            const int32_t *sp = segptr + (size_t(gb) * d.nchunks + i) * (nslot + 1);
+            const int32_t r0 = sp[0], r1 = sp[nslot];
+            if (r0 < 0 || r1 < r0 || size_t(r1) > stream_entries || (r0 & 1))
+                return fail(SKC_ERR_STATE, "verify: bad stream region");
+            if (((r1 - r0 + 1) & ~1) > d.stream_cap)
+                return fail(SKC_ERR_STATE, "verify: stream region exceeds the stage capacity");
+            const int32_t *hdr = reinterpret_cast<const int32_t *>(stream + 2 * size_t(r0));
+            for (int j = 0; j < nslot; ++j) {
+                const int b0 = hdr[j], b1 = hdr[j + 1];
+                if (b0 < (nslot + 2) / 2 || b1 < b0 || r0 + b1 > r1)
+                    return fail(SKC_ERR_STATE, "verify: bad segment table");
+                const int k = chan[size_t(gb) * nslot + j];
+                if (k < 0 && b1 > b0) return fail(SKC_ERR_STATE, "verify: ops for an empty slot");
+                for (int e = b0; e < b1; ++e) {
+                    const uint32_t wb = stream[2 * size_t(r0 + e)];
+                    const uint32_t ob = stream[2 * size_t(r0 + e) + 1];
+                    if (ob & 3) return fail(SKC_ERR_STATE, "verify: misaligned offset");
+                    const int off = int(ob / 4);
+                    if (off + qmax >= d.stage_floats)
+                        return fail(SKC_ERR_STATE, "verify: read beyond the stage");
+                    const int cl = off / d.chan_stride, rem = off % d.chan_stride;
+                    if (cl >= d.CB || i * d.CB + cl >= p->Cg)
+                        return fail(SKC_ERR_STATE, "verify: channel outside the chunk");
+                    got.push_back(NzKey{k, (k / p->Kg) * p->Cg + i * d.CB + cl, rem / p->Wp,
+                                        rem % p->Wp, wb});
+                }
+            }
+        }
+    (void)plane;
+    std::sort(got.begin(), got.end());
+    if (got != csr_keys(p)) return fail(SKC_ERR_STATE, "verify: direct streams != canonical CSR");
+    return SKC_OK;
+}
+
+skc_status verify_regtile(const skc_plan *p) {
+    const RegtileParams &r = p->rp;
+    const RegtileShape &sh = p->rsh;
+    const int M = sh.M, ncase = M * sh.R * sh.S;
+    const int WR = sh.TY + sh.R - 1, WC = sh.TX + sh.S - 1;
+    const int gblocks = p->groups * r.nblocks;
+    const int64_t plane = int64_t(p->Hp) * p->Wp;
+    const int32_t *segoff = img_ptr<int32_t>(p, p->off_segoff);
+    const int32_t *chan = img_ptr<int32_t>(p, p->off_chan);
+    const int32_t *lanemap = img_ptr<int32_t>(p, p->off_lanemap);
+    const uint32_t *stream = img_ptr<uint32_t>(p, p->off_stream);
+    const size_t stream_entries = p->off_segoff / 8;
+    std::vector<int> seen(size_t(p->K), 0);
+    for (int gb = 0; gb < gblocks; ++gb)
+        for (int j = 0; j < r.NT * M; ++j) {
+            const int k = chan[size_t(gb) * r.NT * M + j];
+            if (k < -1 || k >= p->K) return fail(SKC_ERR_STATE, "verify: channel %d out of range", k);
+            if (k >= 0 && (seen[size_t(k)]++ || k / p->Kg != gb / r.nblocks))
+                return fail(SKC_ERR_STATE, "verify: channel %d placed twice or in the wrong group", k);
+        }
+    for (int k = 0; k < p->K; ++k)
+        if (!seen[size_t(k)]) return fail(SKC_ERR_STATE, "verify: channel %d never computed", k);
+    // lane map: every output pixel of the NI images in exactly one active lane's tile
+    std::vector<int> cover(size_t(r.NI) * p->Ho * p->Wo, 0);
+    int lb_max = 0;
+    for (int g = 0; g < r.NG; ++g)
+        for (int l = 0; l < 32; ++l) {
+            const int v = lanemap[g * 32 + l];
+            const bool idle = (v >> 30) & 1;
+            const int img = (v >> 24) & 0x3f, y0 = (v >> 12) & 0xfff, x0 = v & 0xfff;
+            if (img >= r.NI) return fail(SKC_ERR_STATE, "verify: lane image out of range");
+            lb_max = std::max(lb_max, img * r.img_stride + y0 * p->Wp + x0);
+            if (idle) continue;
+            for (int ty = 0; ty < sh.TY; ++ty)
+                for (int tx = 0; tx < sh.TX; ++tx)
+                    if (y0 + ty < p->Ho && x0 + tx < p->Wo)
+                        cover[(size_t(img) * p->Ho + y0 + ty) * p->Wo + x0 + tx]++;
+        }
+    for (int v : cover)
+        if (v != 1) return fail(SKC_ERR_STATE, "verify: output pixel covered %d times", v);
+    // op streams
+    const int64_t alloc_floats = int64_t(p->smem / 4);
+    std::vector<NzKey> got;
+    for (int gb = 0; gb < gblocks; ++gb)
+        for (int i = 0; i < r.nchunks; ++i) {
+            const int32_t *so = segoff + (size_t(gb) * r.nchunks + i) * (r.NT + 1);
+            const int32_t r0 = so[0], r1 = so[r.NT];
+            if (r0 < 0 || r1 < r0 || size_t(r1) > stream_entries || (r0 & 1))
+                return fail(SKC_ERR_STATE, "verify: bad stream region");
+            if (((r1 - r0 + 1) & ~1) > r.stream_cap)
+                return fail(SKC_ERR_STATE, "verify: stream region exceeds the stage capacity");
+            const int32_t *hdr = reinterpret_cast<const int32_t *>(stream + 2 * size_t(r0));
+            for (int t = 0; t < r.NT; ++t) {
+                const int b0 = hdr[t], b1 = (t + 1 < r.NT) ? hdr[t + 1] : r1 - r0;
+                if (b0 < (r.NT + 2) / 2 || b1 <= b0 || r0 + b1 > r1)
+                    return fail(SKC_ERR_STATE, "verify: bad segment table");
+                int cbase = -1;
+                for (int e = b0; e < b1; ++e) {
+                    const uint32_t x = stream[2 * size_t(r0 + e)];
+                    const uint32_t c = stream[2 * size_t(r0 + e) + 1];
+                    const bool last = e + 1 == b1;
+                    if (c == uint32_t(ncase + 1)) {
+                        if (!last) return fail(SKC_ERR_STATE, "verify: EXIT before the end");
+                        continue;
+                    }
+                    if (last) return fail(SKC_ERR_STATE, "verify: segment without EXIT");
+                    if (c == uint32_t(ncase)) {  // HDR: window of channel x in every lane
+                        if (int64_t(x) % plane || int64_t(x) / plane >= r.CB)
+                            return fail(SKC_ERR_STATE, "verify: HDR channel offset");
+                        const int64_t hi = int64_t(r.NS - 1) * r.stage_floats + lb_max + x +
+                                           int64_t(WR - 1) * p->Wp + WC - 1;
+                        if (hi >= alloc_floats) return fail(SKC_ERR_STATE, "verify: window beyond smem");
+                        cbase = int(x);
+                        continue;
+                    }
+                    if (c >= uint32_t(ncase)) return fail(SKC_ERR_STATE, "verify: bad case %u", c);
+                    if (cbase < 0) return fail(SKC_ERR_STATE, "verify: FMA op before any HDR");
+                    const int m = int(c) / (sh.R * sh.S), rr = (int(c) / sh.S) % sh.R, ss = int(c) % sh.S;
+                    const int k = chan[(size_t(gb) * r.NT + t) * M + m];
+                    if (k < 0) return fail(SKC_ERR_STATE, "verify: op for an empty channel slot");
+                    got.push_back(NzKey{k, (k / p->Kg) * p->Cg + i * r.CB + int(cbase / plane), rr, ss, x});
+                }
+            }
+        }
+    std::sort(got.begin(), got.end());
+    if (got != csr_keys(p)) return fail(SKC_ERR_STATE, "verify: regtile streams != canonical CSR");
+    return SKC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+skc_status skc_plan_verify(const skc_plan *p) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    const skc_status st = p->kernel == SKC_KERNEL_REGTILE ? verify_regtile(p) : verify_direct(p);
+    return st == SKC_OK ? ok() : st;
 }
 
 skc_status skc_plan_upload(skc_plan *p, void *d_ws, size_t bytes, void *stream) {

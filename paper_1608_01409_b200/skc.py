@@ -26,7 +26,8 @@ STATUS = {0: "SKC_OK", -1: "SKC_ERR_ARG", -2: "SKC_ERR_GEOMETRY", -3: "SKC_ERR_N
 EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "skc_plan_perm",
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
-           "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds")
+           "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
+           "skc_plan_verify")
 
 
 class SkcError(RuntimeError):
@@ -87,6 +88,7 @@ def lib():
             "skc_pack_csr": [_P] + [_I] * 9 + [ctypes.POINTER(_P)],
             "skc_pack_csr_ex": [_P] + [_I] * 10 + [ctypes.POINTER(_P)],
             "skc_plan_info": [_P, ctypes.POINTER(skc_info)],
+            "skc_plan_verify": [_P],
             "skc_plan_csr": [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
             "skc_plan_perm": [_P, ctypes.POINTER(_P)],
             "skc_plan_upload": [_P, _P, ctypes.c_size_t, _P],
@@ -202,6 +204,11 @@ def skc_pack_csr(w: np.ndarray, H: int, W: int, stride: int = 1, pad: int = 0, g
     _check(lib().skc_pack_csr_ex(w.ctypes.data, K, Cg * groups, R, S, H, W, stride, pad, groups,
                                  kernel, ctypes.byref(h)))
     return Plan(h.value)
+
+
+def skc_plan_verify(plan: Plan):
+    """Static self-check of the plan's kernel-private data (raises SkcError on a violation)."""
+    _check(lib().skc_plan_verify(plan.handle))
 
 
 def skc_plan_upload(plan: Plan, workspace, stream=None):

@@ -146,3 +146,48 @@ def test_model_matches_oracle_model(L, li):
             wc, wr = skc.skc_model_window(c, F, B, a), ref_model.window(r, F, B, a)
             assert wc["x_hi"] == pytest.approx(wr["x_hi"]) and wc["x_lo"] == pytest.approx(wr["x_lo"])
             assert wc["has_speedup_potential"] == wr["has_speedup_potential"]
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
+def test_plan_verify_configs(L, cfg_id):
+    """Every config layer, both kernels: kernel-private indices in bounds, the kernel streams
+    decode exactly to the canonical CSR, every output written exactly once."""
+    cfg = wl.CONFIGS[cfg_id]
+    for li, layer in enumerate(cfg.layers):
+        w = wl.gen_weights(cfg_id, li, layer)
+        for kern in (skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT, skc.SKC_KERNEL_REGTILE):
+            try:
+                plan = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad,
+                                        layer.groups, kern)
+            except skc.SkcError as e:
+                assert kern == skc.SKC_KERNEL_REGTILE and e.status == -5
+                continue
+            skc.skc_plan_verify(plan)
+
+
+def test_plan_verify_random(L):
+    """400 random geometries (strides, groups, ragged sizes, empty rows), both kernels."""
+    rng = np.random.default_rng(21)
+    n_rt = 0
+    for it in range(400):
+        if it % 2:
+            layer = wl.random_layer(rng, max_c=24, max_hw=30, rs=(1, 2, 3, 5), groups=(1, 2, 4))
+        else:  # register-tile friendly: 3x3 / 5x5, stride 1, TMA-aligned planes
+            R = int(rng.choice([3, 5]))
+            g = int(rng.choice([1, 2]))
+            layer = wl.Layer("rt", g * int(rng.integers(1, 30)), g * 4 * int(rng.integers(1, 7)),
+                             int(rng.integers(1, 40)), int(rng.integers(1, 40)), R, R, 1,
+                             (R - 1) // 2, g, float(rng.choice([0.0, 0.5, 0.9, 0.98])), 1.0)
+        w, _ = wl.random_tensors(rng, layer, 1)
+        if it % 9 == 0:
+            w[rng.integers(0, layer.K)] = 0.0
+        for kern in (skc.SKC_KERNEL_DIRECT, skc.SKC_KERNEL_REGTILE):
+            try:
+                plan = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad,
+                                        layer.groups, kern)
+            except skc.SkcError as e:
+                assert kern == skc.SKC_KERNEL_REGTILE and e.status == -5, e
+                continue
+            n_rt += kern == skc.SKC_KERNEL_REGTILE
+            skc.skc_plan_verify(plan)
+    assert n_rt >= 20

@@ -29,6 +29,7 @@ def cuda():
 def run_gpu(w, x, layer, kernel=skc.SKC_KERNEL_AUTO, xp_out=False):
     conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
                                        layer.groups, kernel)
+    skc.skc_plan_verify(conv.plan)
     xd = torch.from_numpy(x).cuda()
     xp = torch.empty(conv.padded_shape(x.shape[0]), device="cuda")
     out = conv.forward(xd, xp=xp)
@@ -238,3 +239,19 @@ def test_config_parity(cfg_id, kernel):
             ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
             check(out[n:n + 1], ref, bound, f"cfg{cfg_id} {layer.name} image {n}")
         assert np.isfinite(out).all()
+
+
+def test_config5_batch4096_sampled():
+    """BASELINE.json configs[4]: config 2's layers at batch 4096 (one GPU's worth of the
+    sharded job at P = 1), in the launch configuration bench.py uses; the oracle checks a
+    seeded sample of images of every layer (first, last, and two inside)."""
+    cfg = wl.CONFIGS[5]
+    rng = np.random.default_rng(105)
+    for li, layer in enumerate(cfg.layers):
+        w = wl.gen_weights(5, li, layer)
+        x = wl.gen_input(5, li, layer, 0, cfg.batch)
+        out, conv = run_gpu(w, x, layer)
+        for n in sample_images(cfg.batch, rng, 4):
+            ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
+            check(out[n:n + 1], ref, bound, f"cfg5 {layer.name} image {n}")
+        del out, x
