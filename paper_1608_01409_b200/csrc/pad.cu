@@ -10,6 +10,9 @@
 namespace skc {
 namespace {
 
+constexpr int kPadVec = 4;    // outputs per vector (float4 store)
+constexpr int kPadUnroll = 4; // vectors per thread per iteration: 16 loads in flight
+
 __global__ void __launch_bounds__(256) pad_kernel(const float *__restrict__ in,
                                                   float *__restrict__ out, int C, int H, int W,
                                                   int pad, int Wp, uint32_t per_img,
@@ -17,30 +20,41 @@ __global__ void __launch_bounds__(256) pad_kernel(const float *__restrict__ in,
     const int64_t n = blockIdx.y;
     const float *src = in + n * int64_t(C) * H * W;
     float *dst = out + n * int64_t(per_img);
-    const uint32_t stride = gridDim.x * blockDim.x * 4u;
-    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4u; i0 < per_img;
-         i0 += stride) {
-        float v[4];
+    const uint32_t span = blockDim.x * kPadVec;  // outputs covered by one vector round
+    const uint32_t stride = gridDim.x * span * kPadUnroll;
+    for (uint32_t base = blockIdx.x * span * kPadUnroll + threadIdx.x * kPadVec; base < per_img;
+         base += stride) {
+        float v[kPadUnroll][kPadVec];
+        // all loads first (independent), then the stores
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t i = i0 + k;
-            v[k] = 0.0f;
-            if (i < per_img) {
-                const uint32_t plane = fdiv(i, div_plane);
-                const uint32_t rem = i - plane * div_plane.d;
-                const uint32_t yy = fdiv(rem, div_wp);
-                const int y = int(yy) - pad;
-                const int x = int(rem - yy * uint32_t(Wp)) - pad;
-                if (y >= 0 && y < H && x >= 0 && x < W)
-                    v[k] = __ldg(src + (int64_t(plane) * H + y) * W + x);
+        for (int u = 0; u < kPadUnroll; ++u) {
+            const uint32_t i0 = base + u * span;
+#pragma unroll
+            for (int k = 0; k < kPadVec; ++k) {
+                const uint32_t i = i0 + k;
+                v[u][k] = 0.0f;
+                if (i < per_img) {
+                    const uint32_t plane = fdiv(i, div_plane);
+                    const uint32_t rem = i - plane * div_plane.d;
+                    const uint32_t yy = fdiv(rem, div_wp);
+                    const int y = int(yy) - pad;
+                    const int x = int(rem - yy * uint32_t(Wp)) - pad;
+                    if (y >= 0 && y < H && x >= 0 && x < W)
+                        v[u][k] = __ldg(src + (int64_t(plane) * H + y) * W + x);
+                }
             }
         }
-        if (vec4 && i0 + 3 < per_img) {
-            *reinterpret_cast<float4 *>(dst + i0) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (i0 + k < per_img) dst[i0 + k] = v[k];
+        for (int u = 0; u < kPadUnroll; ++u) {
+            const uint32_t i0 = base + u * span;
+            if (vec4 && i0 + 3 < per_img) {
+                *reinterpret_cast<float4 *>(dst + i0) =
+                    make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kPadVec; ++k)
+                    if (i0 + k < per_img) dst[i0 + k] = v[u][k];
+            }
         }
     }
 }
@@ -52,7 +66,7 @@ cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     const uint32_t per_img = uint32_t(int64_t(C) * Hp * Wp);
     const int threads = 256;
-    int64_t bx = (int64_t(per_img) + threads * 4 - 1) / (threads * 4);
+    int64_t bx = (int64_t(per_img) + threads * 16 - 1) / (threads * 16);
     bx = bx > 4096 ? 4096 : bx;
     for (int64_t n0 = 0; n0 < N; n0 += 65535) {
         const int64_t nn = (N - n0) < 65535 ? (N - n0) : 65535;
