@@ -125,6 +125,18 @@ skc_status skc_pad_input(const skc_plan *plan, const float *d_in_nchw, float *d_
 skc_status skc_sparse_conv_forward(const skc_plan *plan, const float *d_in_padded,
                                    float *d_out, int N, void *stream);
 
+/* Row f1 -- the same convolution with a fused epilogue (the layout
+ * function makes writing into another layout legitimate):
+ *     d_out[n][k][y + out_pad][x + out_pad] = act(conv(n, k, y, x) + bias[k])
+ * d_bias: device [K] fp32 or NULL (no bias); relu: 0 (identity) or 1 (max(., 0));
+ * d_out: [N][K][Ho + 2*out_pad][Wo + 2*out_pad] -- with out_pad equal to the next layer's pad
+ * this IS the next layer's padded input, so no skc_pad_input pass is needed.  Only the
+ * interior is written: the caller zero-fills the halo once (e.g. at allocation).
+ * out_pad in [0, 64]; otherwise as skc_sparse_conv_forward. */
+skc_status skc_sparse_conv_forward_ex(const skc_plan *plan, const float *d_in_padded,
+                                      float *d_out, int N, const float *d_bias, int relu,
+                                      int out_pad, void *stream);
+
 /* End-to-end entry with HOST buffers (the host-buffer measurement): h_in [N][C][H][W] ->
  * h_out [N][K][Ho][Wo] (host memory; pinned for asynchronous overlap).  The batch is cut
  * into image chunks; the H2D copy of a chunk, pad + conv of the previous one (on `stream`)

@@ -285,9 +285,6 @@ skc_status build_direct_image(skc_plan *p) {
     // pixel-slot tables per band
     const int T = p->T;
     std::vector<int32_t> slotq(size_t(g.nbands) * T * 32), slotout(slotq.size());
-    const int64_t img_elems = int64_t(p->K) * p->Ho * p->Wo;
-    if (img_elems * g.NI >= (int64_t(1) << 31))
-        return fail(SKC_ERR_OVERFLOW, "output too large for int32 slot offsets");
     for (int b = 0; b < g.nbands; ++b) {
         std::vector<std::vector<std::pair<int, int>>> bk;
         band_slots(g.NI, g.img_stride, std::min(g.BH, p->Ho - b * g.BH), p->Wo, p->Wp,
@@ -298,9 +295,8 @@ skc_status build_direct_image(skc_plan *p) {
                 if (size_t(t) < bk[size_t(l)].size()) {
                     const int q = bk[size_t(l)][size_t(t)].first;
                     const int code = bk[size_t(l)][size_t(t)].second;
-                    const int img = code >> 24, yl = (code >> 12) & 0xfff, x = code & 0xfff;
                     slotq[o] = q;
-                    slotout[o] = int32_t(img * img_elems + int64_t(yl) * p->Wo + x);
+                    slotout[o] = code;  // (img << 24) | (yl << 12) | x
                 } else {
                     slotq[o] = l;  // empty slot: a conflict-free dummy read, never stored
                     slotout[o] = -1;
@@ -877,7 +873,6 @@ skc_status verify_direct(const skc_plan *p) {
         if (!seen[size_t(k)]) return fail(SKC_ERR_STATE, "verify: channel %d never computed", k);
     // slots: reads stay inside the stage, outputs cover every (image, y, x) exactly once
     int qmax = 0;
-    const int64_t img_elems = int64_t(p->K) * p->Ho * p->Wo;
     for (int b = 0; b < d.nbands; ++b) {
         const int rows = std::min(d.BH, p->Ho - b * d.BH);
         std::vector<int> cover(size_t(d.NI) * rows * p->Wo, 0);
@@ -889,8 +884,7 @@ skc_status verify_direct(const skc_plan *p) {
                 if (q < 0) return fail(SKC_ERR_STATE, "verify: negative slot offset");
                 qmax = std::max(qmax, q);
                 if (out < 0) continue;
-                const int img = int(out / img_elems), rem = int(out % img_elems);
-                const int yl = rem / p->Wo, x = rem % p->Wo;
+                const int img = out >> 24, yl = (out >> 12) & 0xfff, x = out & 0xfff;
                 if (img >= d.NI || yl >= rows)
                     return fail(SKC_ERR_STATE, "verify: slot output out of the band");
                 if (q != img * d.img_stride + yl * p->stride * p->Wp + x * p->stride)
@@ -1064,9 +1058,13 @@ skc_status skc_pad_input(const skc_plan *p, const float *d_in, float *d_pad, int
     return ok();
 }
 
-skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *d_out, int N,
-                                   void *stream) {
+skc_status skc_sparse_conv_forward_ex(const skc_plan *p, const float *d_in, float *d_out,
+                                      int N, const float *d_bias, int relu, int out_pad,
+                                      void *stream) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (out_pad < 0 || out_pad > 64) return fail(SKC_ERR_ARG, "out_pad = %d outside [0, 64]", out_pad);
+    if (relu != 0 && relu != 1) return fail(SKC_ERR_ARG, "relu must be 0 or 1");
+    const Epilogue epi{d_bias, relu, out_pad};
     if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
     if (!p->d_ws) return fail(SKC_ERR_STATE, "plan not uploaded (call skc_plan_upload)");
     if (N == 0) return ok();
@@ -1083,6 +1081,7 @@ skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *
         rp.segoff = reinterpret_cast<const int32_t *>(ws + p->off_segoff);
         rp.chan = reinterpret_cast<const int32_t *>(ws + p->off_chan);
         rp.lanemap = reinterpret_cast<const int32_t *>(ws + p->off_lanemap);
+        rp.epi = epi;
         cudaError_t e = launch_regtile(rp, p->rsh, p->smem, (cudaStream_t)stream);
         if (e != cudaSuccess)
             return fail(SKC_ERR_CUDA, "regtile launch: %s", cudaGetErrorString(e));
@@ -1097,9 +1096,15 @@ skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *
     dp.chan = reinterpret_cast<const int32_t *>(ws + p->off_chan);
     dp.slotq = reinterpret_cast<const int32_t *>(ws + p->off_lanemap);
     dp.slotout = reinterpret_cast<const int32_t *>(ws + p->off_chunkptr);
+    dp.epi = epi;
     cudaError_t e = launch_direct(dp, p->T, p->smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "conv launch: %s", cudaGetErrorString(e));
     return ok();
+}
+
+skc_status skc_sparse_conv_forward(const skc_plan *p, const float *d_in, float *d_out, int N,
+                                   void *stream) {
+    return skc_sparse_conv_forward_ex(p, d_in, d_out, N, nullptr, 0, 0, stream);
 }
 
 skc_status skc_forward_host(const skc_plan *p, const float *h_in, float *h_out, int N,

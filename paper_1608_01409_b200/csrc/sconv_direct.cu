@@ -20,7 +20,9 @@
 //     chosen on the host so that slotq[t][lane] == lane (mod 32): acc[m][t] += w *
 //     stage[off + slotq[t]] touches 32 distinct banks for ANY off -- in[off + f(0,y,x)] of
 //     Fig. 2 at one shared-memory wavefront per 32 MACs, without junk columns.
-//   - a6: stores to out[n][k][y][x] at the original channel index (slotout tables).
+//   - a6: stores to out[n][k][y][x] at the original channel index (slotout tables); with
+//     the fused epilogue (f1) out = act(acc + bias[k]) lands in the interior of the next
+//     layer's zero-padded layout.
 // Accumulation order per output element: CSR order (c ascending, then r, s) -> bitwise
 // deterministic results.
 #include "ptx.cuh"
@@ -170,20 +172,27 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 
-    // a6: epilogue
+    // a6: epilogue (optionally fused bias + ReLU into the next layer's padded layout)
     const int nimg = min(p.NI, p.N - n0);
-    const int64_t img_elems = int64_t(p.K) * p.Ho * p.Wo;
+    const int opad = p.epi.opad;
+    const int Hop = p.Ho + 2 * opad, Wop = p.Wo + 2 * opad;
     const int32_t *so = p.slotout + (int64_t(band) * T) * 32 + lane;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
         const int k = __ldg(p.chan + int64_t(gb) * nslot + m * NW + warp);
         if (k < 0) continue;
-        float *o = p.out + (int64_t(n0) * p.K + k) * p.Ho * p.Wo + int64_t(band) * p.BH * p.Wo;
+        const float bias = p.epi.bias ? __ldg(p.epi.bias + k) : 0.0f;
+        float *o = p.out + (int64_t(n0) * p.K + k) * Hop * Wop +
+                   int64_t(band * p.BH + opad) * Wop + opad;
 #pragma unroll
         for (int t = 0; t < T; ++t) {
-            const int off = __ldg(so + t * 32);
-            const float v = (t & 1) ? acc[m][t / 2].y : acc[m][t / 2].x;
-            if (off >= 0 && off / img_elems < nimg) o[off] = v;
+            const int code = __ldg(so + t * 32);
+            float v = (t & 1) ? acc[m][t / 2].y : acc[m][t / 2].x;
+            v += bias;
+            if (p.epi.relu) v = fmaxf(v, 0.0f);
+            const int img = code >> 24;
+            if (code >= 0 && img < nimg)
+                o[int64_t(img) * p.K * Hop * Wop + ((code >> 12) & 0xfff) * Wop + (code & 0xfff)] = v;
         }
     }
 }

@@ -122,20 +122,25 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
         }
     }
 
-    // a6: epilogue
+    // a6: epilogue (optionally fused bias + ReLU into the next layer's padded layout)
     if (idle || n0 + img >= p.N) return;
+    const int opad = p.epi.opad;
+    const int Hop = p.Ho + 2 * opad, Wop = p.Wo + 2 * opad;
     const int *ch = p.chan + (int64_t(bidx) * p.NT + t) * M;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
         const int k = __ldg(ch + m);
         if (k < 0) continue;
-        float *o = p.out + (int64_t(n0 + img) * p.K + k) * p.Ho * p.Wo;
+        const float bias = p.epi.bias ? __ldg(p.epi.bias + k) : 0.0f;
+        float *o = p.out + (int64_t(n0 + img) * p.K + k) * Hop * Wop + int64_t(opad) * Wop + opad;
 #pragma unroll
         for (int ty = 0; ty < TY; ++ty)
 #pragma unroll
             for (int tx = 0; tx < TX; ++tx) {
                 const int y = y0 + ty, x = x0 + tx;
-                if (y < p.Ho && x < p.Wo) o[y * p.Wo + x] = acc[m][ty][tx];
+                float v = acc[m][ty][tx] + bias;
+                if (p.epi.relu) v = fmaxf(v, 0.0f);
+                if (y < p.Ho && x < p.Wo) o[y * Wop + x] = v;
             }
     }
 }

@@ -17,6 +17,15 @@ struct Nz {
     int32_t off;
 };
 
+// Fused epilogue (row f1): out = act(acc + bias[k]) written into an output with an opad-wide
+// halo, i.e. directly in the zero-padded input layout of the next layer (the halo itself is
+// never written: the caller zero-fills it once).
+struct Epilogue {
+    const float *bias;  // [K] or nullptr
+    int relu;           // 1: max(., 0)
+    int opad;           // output halo width (0: plain NCHW output)
+};
+
 // Direct kernel (sconv_direct.cu).  CTA = (group of NI images, output-row band, block of
 // NW*M output channels of one conv group); NW compute warps + 1 producer warp.  The
 // producer stages CB input channels of the band for the NI images, plus the (w, off) stream
@@ -31,7 +40,7 @@ struct DirectParams {
     const int32_t *segptr;    // [gblocks][nchunks][NW*M + 1] absolute uint2 index
     const int32_t *chan;      // [gblocks][NW*M] output channel (slot j = m*NW + warp) or -1
     const int32_t *slotq;     // [nbands][T][32] smem word offset of the slot (or lane: empty)
-    const int32_t *slotout;   // [nbands][T][32] img*K*Ho*Wo + yl*Wo + x, or -1 (empty)
+    const int32_t *slotout;   // [nbands][T][32] (img << 24) | (yl << 12) | x, or -1 (empty)
     int N, C, K, Kg, Cg, Hp, Wp, Ho, Wo, stride, groups;
     int NI, BH, BHin, nbands, CB, nchunks, NS;
     int chan_stride;          // floats between channels inside an image slot
@@ -42,6 +51,7 @@ struct DirectParams {
     int bulk;                 // 1: TMA bulk copies; 0: LSU copy fallback (misaligned planes)
     int whole;                // band = all Hp rows: one copy per image per chunk
     int NW, M, cblocks;
+    Epilogue epi;
 };
 
 // Register-tiled kernel (sconv_regtile.cu).  A CTA = (group of NI images, block of NT
@@ -65,6 +75,7 @@ struct RegtileParams {
     int stream_cap;          // uint2 entries per stage stream area (incl. slack)
     int stage_floats;        // slab_floats + 2 * stream_cap
     int NG, NT, nblocks;
+    Epilogue epi;
 };
 
 struct RegtileShape {

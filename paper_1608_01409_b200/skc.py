@@ -27,7 +27,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
-           "skc_plan_verify")
+           "skc_plan_verify", "skc_sparse_conv_forward_ex")
 
 
 class SkcError(RuntimeError):
@@ -94,6 +94,7 @@ def lib():
             "skc_plan_upload": [_P, _P, ctypes.c_size_t, _P],
             "skc_pad_input": [_P, _P, _P, _I, _P],
             "skc_sparse_conv_forward": [_P, _P, _P, _I, _P],
+            "skc_sparse_conv_forward_ex": [_P, _P, _P, _I, _P, _I, _I, _P],
             "skc_forward_host": [_P, _P, _P, _I, _P, _P, _P, _P],
             "skc_model_layer_cost": [_I] * 9 + [ctypes.c_int64, _I, ctypes.POINTER(skc_layer_cost)],
             "skc_model_project": [ctypes.POINTER(skc_layer_cost), ctypes.c_double,
@@ -224,6 +225,14 @@ def skc_sparse_conv_forward(plan: Plan, d_in_padded, d_out, N: int, stream=None)
     """a3..a6: the direct sparse convolution (CUDA kernel)."""
     _check(lib().skc_sparse_conv_forward(plan.handle, _dptr(d_in_padded), _dptr(d_out), int(N),
                                          _stream(stream)))
+
+
+def skc_sparse_conv_forward_ex(plan: Plan, d_in_padded, d_out, N: int, d_bias=None,
+                               relu: bool = False, out_pad: int = 0, stream=None):
+    """f1: conv + bias + ReLU written into the interior of an out_pad-wide padded output."""
+    _check(lib().skc_sparse_conv_forward_ex(plan.handle, _dptr(d_in_padded), _dptr(d_out), int(N),
+                                            _dptr(d_bias) if d_bias is not None else None,
+                                            int(bool(relu)), int(out_pad), _stream(stream)))
 
 
 def skc_forward_host(plan: Plan, h_in, h_out, N: int, d_in, d_pad, d_out, stream=None):

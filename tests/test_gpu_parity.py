@@ -255,3 +255,84 @@ def test_config5_batch4096_sampled():
             ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
             check(out[n:n + 1], ref, bound, f"cfg5 {layer.name} image {n}")
         del out, x
+
+
+def check_epi(out, ref, bound, bias, relu, what=""):
+    """Reading R16 (DESIGN.md): with a fused bias the per-element scale is sum|w*x| + |b|;
+    ReLU is 1-Lipschitz, so the oracle's act(ref + b) carries the same bound."""
+    b = bias.reshape(1, -1, 1, 1).astype(np.float64)
+    exp = ref + b
+    if relu:
+        exp = np.maximum(exp, 0.0)
+    scale = bound + np.abs(b)
+    err = np.abs(out.astype(np.float64) - exp)
+    zero = scale == 0
+    assert np.all(out[zero] == 0), what
+    worst = float(np.max(np.where(zero, 0.0, err / np.where(zero, 1.0, scale))))
+    assert worst <= TOL, f"{what}: max err/scale {worst:.3e}"
+
+
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_DIRECT, skc.SKC_KERNEL_REGTILE])
+def test_fused_epilogue(kernel):
+    """f1: conv + bias + ReLU written into the interior of an out_pad-wide halo; the halo is
+    never touched (pre-filled sentinel survives)."""
+    rng = np.random.default_rng(31)
+    cases = [wl.Layer("e1", 20, 16, 13, 13, 3, 3, 1, 1, 2, 0.9, 1.0),
+             wl.Layer("e2", 24, 8, 27, 27, 5, 5, 1, 2, 2, 0.85, 1.0),
+             wl.Layer("e3", 9, 4, 9, 11, 3, 3, 1, 1, 1, 0.5, 1.0)]
+    for layer in cases:
+        w, x = wl.random_tensors(rng, layer, 3)
+        bias = rng.standard_normal(layer.K).astype(np.float32)
+        try:
+            conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                               layer.groups, kernel)
+        except skc.SkcError as e:
+            assert e.status == -5
+            continue
+        skc.skc_plan_verify(conv.plan)
+        xp = torch.empty(conv.padded_shape(3), device="cuda")
+        skc.skc_pad_input(conv.plan, torch.from_numpy(x).cuda(), xp, 3)
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        db = torch.from_numpy(bias).cuda()
+        for relu in (False, True):
+            for op in (0, 1, 2):
+                out = torch.full((3, layer.K, layer.Ho + 2 * op, layer.Wo + 2 * op), 7.0,
+                                 device="cuda")
+                skc.skc_sparse_conv_forward_ex(conv.plan, xp, out, 3, db, relu, op)
+                torch.cuda.synchronize()
+                o = out.cpu().numpy()
+                inner = o[:, :, op:op + layer.Ho, op:op + layer.Wo]
+                check_epi(inner, ref, bound, bias, relu, f"{layer.name} relu={relu} pad={op}")
+                halo = o.copy()
+                halo[:, :, op:op + layer.Ho, op:op + layer.Wo] = 7.0
+                assert np.all(halo == 7.0), "halo written"
+
+
+def test_chain_conv3_to_conv5_no_pad_pass():
+    """f1 in use: AlexNet conv3 -> conv4 -> conv5 (13x13, pad 1, ReLU between) where each
+    layer writes bias + ReLU straight into the next layer's zero-padded input; every layer is
+    checked against the oracle fed with exactly the GPU's input to that layer."""
+    cfg = wl.CONFIGS[2]
+    N = 16
+    rng = np.random.default_rng(33)
+    layers = [cfg.layers[1], cfg.layers[2], cfg.layers[3]]
+    convs = [skc.SparseConv2d.from_dense(wl.gen_weights(2, i + 1, L), L.H, L.W, L.stride, L.pad,
+                                         L.groups) for i, L in enumerate(layers)]
+    biases = [(0.1 * rng.standard_normal(L.K)).astype(np.float32) for L in layers]
+    x = wl.gen_input(2, 1, layers[0], 0, N)
+    xp = torch.empty(convs[0].padded_shape(N), device="cuda")
+    skc.skc_pad_input(convs[0].plan, torch.from_numpy(x).cuda(), xp, N)
+    for i, (L, conv, b) in enumerate(zip(layers, convs, biases)):
+        last = i == len(layers) - 1
+        op = 0 if last else layers[i + 1].pad
+        nxt = torch.zeros((N, L.K, L.Ho + 2 * op, L.Wo + 2 * op), device="cuda")
+        skc.skc_sparse_conv_forward_ex(conv.plan, xp, nxt, N, torch.from_numpy(b).cuda(), True, op)
+        torch.cuda.synchronize()
+        xin = xp.cpu().numpy()[:, :, L.pad:L.pad + L.H, L.pad:L.pad + L.W]
+        ref, bound = oracle.conv2d_fp64(np.ascontiguousarray(xin), wl.gen_weights(2, i + 1, L),
+                                        L.stride, L.pad, L.groups)
+        o = nxt.cpu().numpy()[:, :, op:op + L.Ho, op:op + L.Wo]
+        check_epi(o, ref, bound, b, True, f"chain {L.name}")
+        if not last:
+            assert not nxt.cpu().numpy()[:, :, :op, :].any()  # halo still zero
+        xp = nxt
