@@ -125,6 +125,17 @@ skc_status skc_pad_input(const skc_plan *plan, const float *d_in_nchw, float *d_
 skc_status skc_sparse_conv_forward(const skc_plan *plan, const float *d_in_padded,
                                    float *d_out, int N, void *stream);
 
+/* Row f3 -- lowering for the comparison baseline "sparse convolution with lowering"
+ * (PAPER.md:272-284; Fig. 3's "conv5 lowered", :413-414): d_lowered[n][(c*R + r)*S + s][y][x]
+ * = in[n][c][y*stride + r - pad][x*stride + s - pad] (zero outside), i.e. the C*R*S x Ho*Wo
+ * lowered matrix per image (R*S-fold replication of the input).  The geometry is the plan's.
+ * Sparse conv with lowering = this + a 1x1 plan over the lowered tensor (weights reshaped
+ * [K][C/g*R*S][1][1], same groups), whose CSR visits the nonzeros in the same (c, r, s)
+ * order, so the two paths agree bit for bit.  Errors: SKC_ERR_ARG, SKC_ERR_OVERFLOW
+ * (C*R*S*Ho*Wo >= 2^31). */
+skc_status skc_im2col(const skc_plan *plan, const float *d_in_nchw, float *d_lowered, int N,
+                      void *stream);
+
 /* Row f1 -- the same convolution with a fused epilogue (the layout
  * function makes writing into another layout legitimate):
  *     d_out[n][k][y + out_pad][x + out_pad] = act(conv(n, k, y, x) + bias[k])

@@ -59,7 +59,51 @@ __global__ void __launch_bounds__(256) pad_kernel(const float *__restrict__ in,
     }
 }
 
+// Row f3: lowering (im2col) for the comparison baseline.
+// L[n][(c*R + r)*S + s][y][x] = in[n][c][y*stride + r - pad][x*stride + s - pad] (0 outside):
+// one thread per lowered element, coalesced writes, per-image grid.y, 32-bit magic division.
+__global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ in,
+                                                     float *__restrict__ out, int C, int H,
+                                                     int W, int R, int S, int stride, int pad,
+                                                     int Wo, uint32_t per_img, FastDiv div_howo,
+                                                     FastDiv div_wo, FastDiv div_rs,
+                                                     FastDiv div_s) {
+    const int64_t n = blockIdx.y;
+    const float *src = in + n * int64_t(C) * H * W;
+    float *dst = out + n * int64_t(per_img);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < per_img;
+         i += gridDim.x * blockDim.x) {
+        const uint32_t crs = fdiv(i, div_howo);
+        const uint32_t pix = i - crs * div_howo.d;
+        const uint32_t y = fdiv(pix, div_wo), x = pix - y * uint32_t(Wo);
+        const uint32_t c = fdiv(crs, div_rs), rs = crs - c * div_rs.d;
+        const uint32_t r = fdiv(rs, div_s), s = rs - r * uint32_t(S);
+        const int yi = int(y) * stride + int(r) - pad, xi = int(x) * stride + int(s) - pad;
+        float v = 0.0f;
+        if (yi >= 0 && yi < H && xi >= 0 && xi < W) v = __ldg(src + (int64_t(c) * H + yi) * W + xi);
+        dst[i] = v;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
+                          int S, int stride, int pad, int Ho, int Wo, cudaStream_t st) {
+    const uint32_t per_img = uint32_t(int64_t(C) * R * S * Ho * Wo);
+    int64_t bx = (int64_t(per_img) + 255) / 256;
+    bx = bx > 4096 ? 4096 : bx;
+    for (int64_t n0 = 0; n0 < N; n0 += 65535) {
+        const int64_t nn = (N - n0) < 65535 ? (N - n0) : 65535;
+        const dim3 grid{static_cast<unsigned>(bx), static_cast<unsigned>(nn), 1u};
+        im2col_kernel<<<grid, 256, 0, st>>>(in + n0 * int64_t(C) * H * W,
+                                            out + n0 * int64_t(per_img), C, H, W, R, S, stride,
+                                            pad, Wo, per_img, make_fastdiv(uint32_t(Ho * Wo)),
+                                            make_fastdiv(uint32_t(Wo)),
+                                            make_fastdiv(uint32_t(R * S)),
+                                            make_fastdiv(uint32_t(S)));
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int W, int pad,
                        cudaStream_t st) {

@@ -1058,6 +1058,20 @@ skc_status skc_pad_input(const skc_plan *p, const float *d_in, float *d_pad, int
     return ok();
 }
 
+skc_status skc_im2col(const skc_plan *p, const float *d_in, float *d_lowered, int N,
+                      void *stream) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
+    if (N == 0) return ok();
+    if (!d_in || !d_lowered) return fail(SKC_ERR_ARG, "NULL device pointer");
+    if (int64_t(p->C) * p->R * p->S * p->Ho * p->Wo >= (int64_t(1) << 31))
+        return fail(SKC_ERR_OVERFLOW, "lowered image does not fit int32 indexing");
+    cudaError_t e = launch_im2col(d_in, d_lowered, N, p->C, p->H, p->W, p->R, p->S, p->stride,
+                                  p->pad, p->Ho, p->Wo, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "im2col launch: %s", cudaGetErrorString(e));
+    return ok();
+}
+
 skc_status skc_sparse_conv_forward_ex(const skc_plan *p, const float *d_in, float *d_out,
                                       int N, const float *d_bias, int relu, int out_pad,
                                       void *stream) {

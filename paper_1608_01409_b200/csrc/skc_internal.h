@@ -86,6 +86,8 @@ struct RegtileShape {
 // Launchers (defined in the .cu files).  Return cudaError_t of the launch.
 cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int W, int pad,
                        cudaStream_t st);
+cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
+                          int S, int stride, int pad, int Ho, int Wo, cudaStream_t st);
 cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st);
 bool direct_supported(int T, int M);
 cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_t smem,

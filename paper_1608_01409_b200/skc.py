@@ -27,7 +27,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
-           "skc_plan_verify", "skc_sparse_conv_forward_ex")
+           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col")
 
 
 class SkcError(RuntimeError):
@@ -95,6 +95,7 @@ def lib():
             "skc_pad_input": [_P, _P, _P, _I, _P],
             "skc_sparse_conv_forward": [_P, _P, _P, _I, _P],
             "skc_sparse_conv_forward_ex": [_P, _P, _P, _I, _P, _I, _I, _P],
+            "skc_im2col": [_P, _P, _P, _I, _P],
             "skc_forward_host": [_P, _P, _P, _I, _P, _P, _P, _P],
             "skc_model_layer_cost": [_I] * 9 + [ctypes.c_int64, _I, ctypes.POINTER(skc_layer_cost)],
             "skc_model_project": [ctypes.POINTER(skc_layer_cost), ctypes.c_double,
@@ -233,6 +234,36 @@ def skc_sparse_conv_forward_ex(plan: Plan, d_in_padded, d_out, N: int, d_bias=No
     _check(lib().skc_sparse_conv_forward_ex(plan.handle, _dptr(d_in_padded), _dptr(d_out), int(N),
                                             _dptr(d_bias) if d_bias is not None else None,
                                             int(bool(relu)), int(out_pad), _stream(stream)))
+
+
+def skc_im2col(plan: Plan, d_in, d_lowered, N: int, stream=None):
+    """f3: lowered (im2col) tensor [N][C*R*S][Ho][Wo] of an NCHW input (CUDA kernel)."""
+    _check(lib().skc_im2col(plan.handle, _dptr(d_in), _dptr(d_lowered), int(N), _stream(stream)))
+
+
+class LoweredSparseConv2d:
+    """f3 baseline: im2col + CSR SpMDM (the direct kernel run as a 1x1 conv over the lowered
+    tensor).  Same weights, same nonzero order as SparseConv2d -> identical results."""
+
+    def __init__(self, w: np.ndarray, H: int, W: int, stride=1, pad=0, groups=1,
+                 kernel=SKC_KERNEL_DIRECT, device="cuda"):
+        K, Cg, R, S = w.shape
+        self.geom_plan = skc_pack_csr(w, H, W, stride, pad, groups, SKC_KERNEL_DIRECT)
+        g = self.geom_plan.info()
+        self.Ho, self.Wo, self.K, self.CRS = g["Ho"], g["Wo"], K, g["C"] * R * S
+        w1 = np.ascontiguousarray(w.reshape(K, Cg * R * S, 1, 1))
+        self.conv = SparseConv2d.from_dense(w1, self.Ho, self.Wo, 1, 0, groups, kernel, device)
+
+    def lowered_shape(self, N):
+        return (N, self.CRS, self.Ho, self.Wo)
+
+    def forward(self, x, lowered=None, out=None, stream=None):
+        import torch
+        N = x.shape[0]
+        if lowered is None:
+            lowered = torch.empty(self.lowered_shape(N), dtype=torch.float32, device=x.device)
+        skc_im2col(self.geom_plan, x, lowered, N, stream)
+        return self.conv.forward_padded(lowered, out, stream)
 
 
 def skc_forward_host(plan: Plan, h_in, h_out, N: int, d_in, d_pad, d_out, stream=None):

@@ -336,3 +336,38 @@ def test_chain_conv3_to_conv5_no_pad_pass():
         if not last:
             assert not nxt.cpu().numpy()[:, :, :op, :].any()  # halo still zero
         xp = nxt
+
+
+def test_im2col_equals_unfold():
+    """f3: the lowering kernel equals the library routine torch.nn.functional.unfold
+    (same (c, r, s) row order), bitwise."""
+    rng = np.random.default_rng(41)
+    for (N, C, H, W, R, st, p) in [(2, 3, 7, 9, 3, 1, 1), (1, 8, 13, 13, 3, 1, 1),
+                                   (2, 4, 27, 27, 5, 1, 2), (3, 2, 11, 10, 3, 2, 0)]:
+        x = rng.standard_normal((N, C, H, W), dtype=np.float32)
+        plan = skc.skc_pack_csr(np.ones((1, C, R, R), np.float32), H, W, st, p, 1)
+        g = plan.info()
+        low = torch.empty((N, C * R * R, g["Ho"], g["Wo"]), device="cuda")
+        skc.skc_im2col(plan, torch.from_numpy(x).cuda(), low, N)
+        torch.cuda.synchronize()
+        ref = torch.nn.functional.unfold(torch.from_numpy(x), R, padding=p, stride=st)
+        np.testing.assert_array_equal(low.cpu().numpy().reshape(ref.shape).view(np.uint32),
+                                      ref.numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("li", [0, 1, 2, 3])
+def test_lowered_equals_direct(li):
+    """f3: sparse conv WITH lowering (im2col + SpMDM) gives bit-for-bit the direct sparse
+    convolution's result (same nonzero order), and passes the oracle bar."""
+    L = wl.CONFIGS[2].layers[li]
+    w = wl.gen_weights(2, li, L)
+    x = wl.gen_input(2, li, L, 0, 4)
+    direct, _ = run_gpu(w, x, L, skc.SKC_KERNEL_DIRECT)
+    low = skc.LoweredSparseConv2d(w, L.H, L.W, L.stride, L.pad, L.groups)
+    skc.skc_plan_verify(low.conv.plan)
+    out = low.forward(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    np.testing.assert_array_equal(o.view(np.uint32), direct.view(np.uint32))
+    ref, bound = oracle.conv2d_fp64(x, w, L.stride, L.pad, L.groups)
+    check(o, ref, bound, f"lowered {L.name}")
