@@ -94,6 +94,15 @@ skc_status skc_pack_csr(const float *w_host, int K, int C, int R, int S, int H, 
 skc_status skc_pack_csr_ex(const float *w_host, int K, int C, int R, int S, int H, int W,
                            int stride, int pad, int groups, int kernel, skc_plan **out);
 
+/* Row f2 -- sparse fully connected layer as SpMDM: Y[M x B] = W[M x K] .
+ * X[K x B] with W dense-pruned on the host (row-major [M][K]) and X, Y device row-major (the
+ * batch is the fast axis -- SpMDM's dense operand).  This is exactly the 1x1 convolution of
+ * one image with K channels of 1 x B pixels (the virtual dense matrix degenerates to X), so
+ * the plan runs on the same kernels: skc_plan_upload, then
+ * skc_sparse_conv_forward(plan, X, Y, 1, stream) (X needs no padding; or _ex for bias+ReLU).
+ * The plan is specific to B.  Errors: as skc_pack_csr_ex. */
+skc_status skc_pack_fc(const float *w_host, int M, int K, int B, int kernel, skc_plan **out);
+
 skc_status skc_plan_info(const skc_plan *plan, skc_info *info);
 
 /* Host views of the canonical CSR (valid until skc_plan_destroy): rowptr[K+1] int32,

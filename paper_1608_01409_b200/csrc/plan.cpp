@@ -71,6 +71,7 @@ struct skc_plan {
     int T = 0, NW = 0, M = 0, cblocks = 0;
     DirectParams dp{};
     double direct_waves = 0;  // smem wavefronts per nonzero per image (all bands)
+    int max_ni = 4;           // images per CTA the direct kernel may stage (FC: 1)
     size_t smem = 0;
 
     // register-tiled kernel configuration (kernel == SKC_KERNEL_REGTILE)
@@ -164,7 +165,7 @@ skc_status configure_direct(skc_plan *p) {
         return fail(SKC_ERR_UNSUPPORTED, "output %dx%d too large for the direct kernel", Ho, Wo);
     const int64_t plane = int64_t(p->Hp) * p->Wp;
     double best_cost = 1e300;
-    for (int NI = 1; NI <= 4; NI *= 2) {
+    for (int NI = 1; NI <= p->max_ni; NI *= 2) {
         for (int nb = 1; nb <= Ho; ++nb) {
             const int BH = (Ho + nb - 1) / nb;
             if ((Ho + BH - 1) / BH != nb) continue;  // same BH as a smaller nb
@@ -653,8 +654,16 @@ extern "C" {
 
 const char *skc_last_error(void) { return g_err.c_str(); }
 
+static skc_status pack_common(const float *w, int K, int C, int R, int S, int H, int W, int stride,
+                       int pad, int groups, int kernel, int max_ni, skc_plan **out);
+
 skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, int W,
                            int stride, int pad, int groups, int kernel, skc_plan **out) {
+    return pack_common(w, K, C, R, S, H, W, stride, pad, groups, kernel, 4, out);
+}
+
+static skc_status pack_common(const float *w, int K, int C, int R, int S, int H, int W, int stride,
+                       int pad, int groups, int kernel, int max_ni, skc_plan **out) {
     if (!w || !out) return fail(SKC_ERR_ARG, "NULL weights or output pointer");
     *out = nullptr;
     if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_REGTILE)
@@ -668,6 +677,7 @@ skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, in
     p->Hp = H + 2 * pad; p->Wp = W + 2 * pad;
     p->Ho = (p->Hp - R) / stride + 1; p->Wo = (p->Wp - S) / stride + 1;
     p->Kg = K / groups; p->Cg = C / groups;
+    p->max_ni = max_ni;
 
     // a1: canonical CSR.  Row k scans (c_local, r, s) lexicographically; because r < Hp
     // and s < Wp the offset is strictly increasing in that order.
@@ -774,6 +784,14 @@ skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, in
 skc_status skc_pack_csr(const float *w, int K, int C, int R, int S, int H, int W, int stride,
                         int pad, int groups, skc_plan **out) {
     return skc_pack_csr_ex(w, K, C, R, S, H, W, stride, pad, groups, SKC_KERNEL_AUTO, out);
+}
+
+skc_status skc_pack_fc(const float *w, int M, int K, int B, int kernel, skc_plan **out) {
+    // Y[M x B] = W[M x K] X[K x B] is the 1x1 convolution of one "image" with K channels of
+    // 1 x B pixels: PAPER.md:318-329 (sparse FC layers as SpMDM)
+    if (B < 1) return fail(SKC_ERR_GEOMETRY, "batch B = %d < 1", B);
+    // one "image" per call: never stage more than one image per CTA
+    return pack_common(w, M, K, 1, 1, 1, B, 1, 0, 1, kernel, 1, out);
 }
 
 skc_status skc_plan_info(const skc_plan *p, skc_info *info) {

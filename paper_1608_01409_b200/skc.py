@@ -27,7 +27,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
-           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col")
+           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc")
 
 
 class SkcError(RuntimeError):
@@ -96,6 +96,7 @@ def lib():
             "skc_sparse_conv_forward": [_P, _P, _P, _I, _P],
             "skc_sparse_conv_forward_ex": [_P, _P, _P, _I, _P, _I, _I, _P],
             "skc_im2col": [_P, _P, _P, _I, _P],
+            "skc_pack_fc": [_P, _I, _I, _I, _I, ctypes.POINTER(_P)],
             "skc_forward_host": [_P, _P, _P, _I, _P, _P, _P, _P],
             "skc_model_layer_cost": [_I] * 9 + [ctypes.c_int64, _I, ctypes.POINTER(skc_layer_cost)],
             "skc_model_project": [ctypes.POINTER(skc_layer_cost), ctypes.c_double,
@@ -239,6 +240,33 @@ def skc_sparse_conv_forward_ex(plan: Plan, d_in_padded, d_out, N: int, d_bias=No
 def skc_im2col(plan: Plan, d_in, d_lowered, N: int, stream=None):
     """f3: lowered (im2col) tensor [N][C*R*S][Ho][Wo] of an NCHW input (CUDA kernel)."""
     _check(lib().skc_im2col(plan.handle, _dptr(d_in), _dptr(d_lowered), int(N), _stream(stream)))
+
+
+def skc_pack_fc(w: np.ndarray, batch: int, kernel: int = SKC_KERNEL_AUTO) -> Plan:
+    """f2: pruned FC weights float32 [M, K] -> plan for Y[M x B] = W X[K x B] (B = batch)."""
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    M, K = w.shape
+    h = _P()
+    _check(lib().skc_pack_fc(w.ctypes.data, M, K, int(batch), kernel, ctypes.byref(h)))
+    return Plan(h.value)
+
+
+class SparseLinear:
+    """f2: a pruned FC layer on the GPU, Y[M x B] = W[M x K] X[K x B] (batch-minor layout)."""
+
+    def __init__(self, w: np.ndarray, batch: int, kernel=SKC_KERNEL_AUTO, device="cuda"):
+        self.plan = skc_pack_fc(w, batch, kernel)
+        self.plan.upload(device)
+        self.M, self.K, self.B = w.shape[0], w.shape[1], int(batch)
+
+    def forward(self, x, out=None, bias=None, relu=False, stream=None):
+        import torch
+        if tuple(x.shape) != (self.K, self.B):
+            raise ValueError(f"expected X of shape {(self.K, self.B)}")
+        if out is None:
+            out = torch.empty((self.M, self.B), dtype=torch.float32, device=x.device)
+        skc_sparse_conv_forward_ex(self.plan, x, out, 1, bias, relu, 0, stream)
+        return out
 
 
 class LoweredSparseConv2d:

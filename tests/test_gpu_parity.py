@@ -371,3 +371,31 @@ def test_lowered_equals_direct(li):
     np.testing.assert_array_equal(o.view(np.uint32), direct.view(np.uint32))
     ref, bound = oracle.conv2d_fp64(x, w, L.stride, L.pad, L.groups)
     check(o, ref, bound, f"lowered {L.name}")
+
+
+def test_sparse_fc_alexnet():
+    """f2: AlexNet fc6-fc8 (90% sparse) at batch 256 as SpMDM through skc_pack_fc against
+    the library routine numpy float64 matmul; scale = |W| |X| per output element."""
+    for i, L in enumerate(wl.ALEXNET_FC):
+        w = wl.gen_fc_weights(i, L)
+        x = wl.gen_fc_input(i, L, wl.FC_BATCH)
+        fc = skc.SparseLinear(w, wl.FC_BATCH)
+        skc.skc_plan_verify(fc.plan)
+        y = fc.forward(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        yo = y.cpu().numpy()
+        ref = w.astype(np.float64) @ x.astype(np.float64)
+        bound = np.abs(w).astype(np.float64) @ np.abs(x).astype(np.float64)
+        check(yo, ref, bound, f"fc {L.name}")
+
+
+def test_sparse_fc_small_vs_oracle():
+    """f2 on small ragged shapes through the C oracle (the FC is its 1x1 special case)."""
+    rng = np.random.default_rng(51)
+    for (M, K, B) in [(1, 1, 1), (7, 13, 5), (40, 33, 64), (65, 100, 31)]:
+        w = np.where(rng.random((M, K)) < 0.3, rng.standard_normal((M, K)), 0).astype(np.float32)
+        x = np.maximum(rng.standard_normal((K, B)), 0).astype(np.float32)
+        fc = skc.SparseLinear(w, B)
+        y = fc.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+        ref, bound = oracle.conv2d_fp64(x.reshape(1, K, 1, B), w.reshape(M, K, 1, 1))
+        check(y.reshape(1, M, 1, B), ref, bound, f"fc {M}x{K}x{B}")

@@ -99,6 +99,39 @@ CONFIGS = {
 }
 
 
+@dataclass(frozen=True)
+class FCLayer:
+    name: str
+    M: int          # outputs
+    K: int          # inputs
+    sparsity: float
+    sigma: float
+
+    @property
+    def density(self) -> float:
+        return 1.0 - self.sparsity
+
+
+# Row f2 (not a BASELINE config): AlexNet's fully connected layers fc6-fc8 at batch 256,
+# element-wise pruned to 90% (a round synthetic value; the paper gives no FC sparsities).
+ALEXNET_FC = (FCLayer("fc6", 4096, 9216, 0.90, 0.005), FCLayer("fc7", 4096, 4096, 0.90, 0.005),
+              FCLayer("fc8", 1000, 4096, 0.90, 0.01))
+FC_BATCH = 256
+FC_CFG_ID = 6
+
+
+def gen_fc_weights(layer_idx: int, L: FCLayer) -> np.ndarray:
+    w = _rng(FC_CFG_ID, layer_idx, 0).standard_normal((L.M, L.K), dtype=np.float32) * np.float32(L.sigma)
+    keep = _rng(FC_CFG_ID, layer_idx, 1).random((L.M, L.K), dtype=np.float64) < L.density
+    return np.where(keep, w, np.float32(0.0)).astype(np.float32)
+
+
+def gen_fc_input(layer_idx: int, L: FCLayer, batch: int) -> np.ndarray:
+    """X [K x B] (batch-minor), ReLU(N(0,1))."""
+    x = _rng(FC_CFG_ID, layer_idx, 2).standard_normal((L.K, batch), dtype=np.float32)
+    return np.maximum(x, np.float32(0.0))
+
+
 def _rng(cfg_id: int, layer: int, role: int, block: int = 0) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(
         np.random.SeedSequence([1608, 1409, int(cfg_id), int(layer), int(role), int(block)])))
