@@ -718,7 +718,10 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
     // nnz-sorted permutation: descending nnz, stable (ties by ascending k), per group
     p->perm.resize(size_t(K));
     std::iota(p->perm.begin(), p->perm.end(), 0);
-    for (int g = 0; g < groups; ++g) {
+    // SKC_NO_NNZ_SORT=1 keeps the natural channel order (load-balance experiments only;
+    // the default, and the checked contract, is the nnz-sorted order)
+    const char *nosort = std::getenv("SKC_NO_NNZ_SORT");
+    for (int g = 0; g < groups && !(nosort && nosort[0] == '1'); ++g) {
         auto b = p->perm.begin() + ptrdiff_t(g) * p->Kg;
         std::stable_sort(b, b + p->Kg, [p](int a, int c) {
             return p->rowptr[a + 1] - p->rowptr[a] > p->rowptr[c + 1] - p->rowptr[c];

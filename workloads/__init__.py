@@ -146,6 +146,19 @@ def gen_weights(cfg_id: int, layer_idx: int, L: Layer) -> np.ndarray:
     return np.where(keep, w, np.float32(0.0)).astype(np.float32)
 
 
+def gen_weights_skewed(cfg_id: int, layer_idx: int, L: Layer, spread: float = 1.0) -> np.ndarray:
+    """Row f4 stress input: like gen_weights, but each output channel k keeps its weights with
+    its own probability x_k = density * LogNormal(0, spread) / mean (clipped to [0, 1]), so
+    per-channel nnz is heavily skewed at the same average density."""
+    shape = (L.K, L.C // L.groups, L.R, L.S)
+    w = (_rng(cfg_id, layer_idx, 0).standard_normal(shape, dtype=np.float32)
+         * np.float32(L.sigma))
+    z = _rng(cfg_id, layer_idx, 3).lognormal(0.0, spread, L.K)
+    xk = np.clip(L.density * z / z.mean(), 0.0, 1.0)
+    keep = _rng(cfg_id, layer_idx, 1).random(shape, dtype=np.float64) < xk[:, None, None, None]
+    return np.where(keep, w, np.float32(0.0)).astype(np.float32)
+
+
 def gen_input(cfg_id: int, layer_idx: int, L: Layer, n0: int, n1: int) -> np.ndarray:
     """Images [n0, n1) of the layer's input, float32 NCHW, ReLU(N(0,1))."""
     n0, n1 = int(n0), int(n1)
