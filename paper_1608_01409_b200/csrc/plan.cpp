@@ -243,7 +243,10 @@ skc_status build_direct_image(skc_plan *p) {
                 std::vector<std::vector<std::pair<uint32_t, uint32_t>>>(
                     static_cast<size_t>(g.nchunks)));
             for (int j = 0; j < nslot; ++j) {
-                const int lc = cb * nslot + j;  // channel position inside the group (perm)
+                // slot j = m*NW + w is computed by warp w; sorted channels are dealt to the
+                // warps in snake order (m odd reverses w) so per-warp nnz sums balance
+                const int m = j / p->NW, wi = j % p->NW;
+                const int lc = cb * nslot + m * p->NW + ((m & 1) ? p->NW - 1 - wi : wi);
                 if (lc >= p->Kg) continue;
                 const int k = p->perm[size_t(gi) * p->Kg + lc];
                 chan[size_t(gb) * nslot + j] = k;
