@@ -184,13 +184,13 @@ skc_status configure_direct(skc_plan *p) {
                 for (int b = 0; b < nb; ++b)
                     T = std::max(T, band_slots(NI, IS, std::min(BH, Ho - b * BH), Wo, p->Wp,
                                                p->stride, nullptr));
-                if (T > 32) continue;
+                if (T > 16) continue;
                 // per nonzero and image: T loads + 1 broadcast per band (wavefront-cycles)
                 double cost = double(nb) * (T + 1) / NI + 1e-3 * NI + 1e-4 * nb;
                 if (!bulk_legal(p, NI, BH, BHin, nb, whole, CB, chan_stride, IS)) {
                     // cp.async fallback: ~8 cycles per 32 staged words, repeated by every
                     // channel block; expressed per nonzero of the layer
-                    const int M = T <= 8 ? 4 : (T <= 24 ? 2 : 1);
+                    const int M = T <= 8 ? 4 : 2;
                     const double blocks = std::ceil(double(p->Kg) / (kDirectNW * M)) * p->groups;
                     const double words = double(nb) * BHin * p->Wp * p->C * blocks;
                     cost += words / 32.0 * 8.0 / std::max<double>(1.0, double(p->colidx.size()));
@@ -211,7 +211,7 @@ skc_status configure_direct(skc_plan *p) {
                                  g.img_stride);
     g.bulk = bulk ? 1 : 0;
     p->NW = kDirectNW;
-    p->M = p->T <= 8 ? 4 : (p->T <= 24 ? 2 : 1);
+    p->M = p->T <= 8 ? 4 : (p->T <= 16 ? 2 : 1);
     // tuning overrides (benchmarks): SKC_DIRECT_NW (compute warps, 1..16), SKC_DIRECT_M
     if (const char *e = std::getenv("SKC_DIRECT_NW")) p->NW = std::max(1, std::min(16, std::atoi(e)));
     if (const char *e = std::getenv("SKC_DIRECT_M")) p->M = std::max(1, std::min(4, std::atoi(e)));

@@ -219,11 +219,7 @@ cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
     X(4, 2) X(4, 4) X(5, 1) X(5, 2) X(5, 4) X(6, 1) X(6, 2) X(6, 4) X(7, 1) X(7, 2) \
     X(7, 4) X(8, 1) X(8, 2) X(8, 4) X(9, 1) X(9, 2) X(9, 4) X(10, 1) X(10, 2) X(10, 4) \
     X(11, 1) X(11, 2) X(11, 4) X(12, 1) X(12, 2) X(12, 4) X(13, 1) X(13, 2) X(13, 4) \
-    X(14, 1) X(14, 2) X(14, 4) X(15, 1) X(15, 2) X(15, 4) X(16, 1) X(16, 2) X(16, 4) \
-    X(17, 1) X(17, 2) X(18, 1) X(18, 2) X(19, 1) X(19, 2) X(20, 1) X(20, 2) X(21, 1) \
-    X(21, 2) X(22, 1) X(22, 2) X(23, 1) X(23, 2) X(24, 1) X(24, 2) X(25, 1) X(25, 2) \
-    X(26, 1) X(26, 2) X(27, 1) X(27, 2) X(28, 1) X(28, 2) X(29, 1) X(29, 2) X(30, 1) \
-    X(30, 2) X(31, 1) X(31, 2) X(32, 1) X(32, 2)
+    X(14, 1) X(14, 2) X(14, 4) X(15, 1) X(15, 2) X(15, 4) X(16, 1) X(16, 2) X(16, 4)
 
 }  // namespace
 
