@@ -412,7 +412,9 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
     const double density = double(p->colidx.size()) / (double(p->K) * p->Cg * p->R * p->S);
     const double chan_bytes = double(c.NI) * double(plane) * 4.0 +
                               8.0 * (sh.nwmax * (sh.M * sh.R * sh.S * density + 1.0));
-    int CB = int(std::max(1.0, double(kRtStageTarget) / chan_bytes));
+    double stage_target = double(kRtStageTarget);
+    if (const char *e = std::getenv("SKC_RT_STAGE_KB")) stage_target = std::atof(e) * 1024.0;
+    int CB = int(std::max(1.0, stage_target / chan_bytes));
     CB = std::min(CB, p->Cg);
     while (CB > 1 && (int64_t(CB) * plane) % 4) --CB;
     if ((int64_t(CB) * plane) % 4) {
