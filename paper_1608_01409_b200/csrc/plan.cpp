@@ -406,13 +406,33 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
     const int total = c.NI * tiles;
     c.NG = (total + 31) / 32;
     if (c.NG > sh.nwmax) return false;
-    // channels per stage: input slab of NI images + the op stream of up to 12 tasks of M
-    // channels (8 B per nonzero), aiming at kRtStageTarget bytes; CB*plane must keep image
-    // slots 16-byte aligned
+    // tasks per CTA: keep the most warps resident per SM, fill the last block, and prefer
+    // more tasks per CTA (each CTA re-reads its images' slabs: fewer blocks, less traffic)
+    const int tasks = (p->Kg + sh.M - 1) / sh.M;
+    double best = -1;
+    const char *nt_env = std::getenv("SKC_RT_NT");
+    const int nt_force = nt_env ? std::atoi(nt_env) : 0;
+    for (int NT = std::min(sh.nwmax / c.NG, tasks); NT >= 1; --NT) {
+        if (nt_force > 0 && NT != std::min(nt_force, std::min(sh.nwmax / c.NG, tasks))) continue;
+        const int nb = (tasks + NT - 1) / NT;
+        const int warps = c.NG * NT;
+        const int by_regs = 65536 / (warps * 32 * rt_regs(sh));
+        if (by_regs < 1) continue;
+        const int resident = std::min(64, warps * std::min(by_regs, 3));
+        const double fill = double(tasks) / double(nb * NT);
+        const double score = fill * double(resident) * (1.0 + 0.05 * NT);
+        if (score > best) { best = score; c.NT = NT; c.nblocks = nb; c.ctas_per_sm = by_regs; }
+    }
+    if (!c.NT) return false;
+    // channels per stage: input slab of NI images + the op stream of the NT tasks (8 B per
+    // nonzero).  Stages as large as the shared-memory budget of the ctas_per_sm CTAs that
+    // the register cap allows (fewer chunk hand-offs; measured +4..13%), capped at 48 KB;
+    // CB*plane must keep image slots 16-byte aligned
     const double density = double(p->colidx.size()) / (double(p->K) * p->Cg * p->R * p->S);
     const double chan_bytes = double(c.NI) * double(plane) * 4.0 +
-                              8.0 * (sh.nwmax * (sh.M * sh.R * sh.S * density + 1.0));
-    double stage_target = double(kRtStageTarget);
+                              8.0 * (c.NT * (sh.M * sh.R * sh.S * density + 1.0));
+    const double budget = (227.0 * 1024) / std::max(1, std::min(c.ctas_per_sm, 3)) - 2048.0;
+    double stage_target = std::min(48.0 * 1024, budget / kRtStages);
     if (const char *e = std::getenv("SKC_RT_STAGE_KB")) stage_target = std::atof(e) * 1024.0;
     int CB = int(std::max(1.0, stage_target / chan_bytes));
     CB = std::min(CB, p->Cg);
@@ -480,24 +500,6 @@ bool regtile_candidate(const skc_plan *p, const RegtileShape &sh, RtCandidate &c
         if (wf < best_wf) { best_wf = wf; c.img_stride = IS; c.lanemap = lm; }
     }
     c.wf = best_wf;
-    // tasks per CTA: keep the most warps resident per SM, fill the last block, and prefer
-    // more tasks per CTA (each CTA re-reads its images' slabs: fewer blocks, less traffic)
-    const int tasks = (p->Kg + sh.M - 1) / sh.M;
-    double best = -1;
-    const char *nt_env = std::getenv("SKC_RT_NT");
-    const int nt_force = nt_env ? std::atoi(nt_env) : 0;
-    for (int NT = std::min(sh.nwmax / c.NG, tasks); NT >= 1; --NT) {
-        if (nt_force > 0 && NT != std::min(nt_force, std::min(sh.nwmax / c.NG, tasks))) continue;
-        const int nb = (tasks + NT - 1) / NT;
-        const int warps = c.NG * NT;
-        const int by_regs = 65536 / (warps * 32 * rt_regs(sh));
-        if (by_regs < 1) continue;
-        const int resident = std::min(64, warps * std::min(by_regs, 3));
-        const double fill = double(tasks) / double(nb * NT);
-        const double score = fill * double(resident) * (1.0 + 0.05 * NT);
-        if (score > best) { best = score; c.NT = NT; c.nblocks = nb; c.ctas_per_sm = by_regs; }
-    }
-    if (!c.NT) return false;
     // Cost model, SM-cycles per image summed over SMs (fitted to B200 measurements, see
     // DESIGN.md "Kernel selection"): every dispatched op costs a(occ) -- the brx.idx dispatch
     // is latency-bound, so its cost falls with the warps resident per SM -- and every HDR
