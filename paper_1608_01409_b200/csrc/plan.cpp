@@ -213,7 +213,7 @@ skc_status configure_direct(skc_plan *p) {
     p->NW = kDirectNW;
     p->M = p->T <= 8 ? 4 : (p->T <= 16 ? 2 : 1);
     // tuning overrides (benchmarks): SKC_DIRECT_NW (compute warps, 1..16), SKC_DIRECT_M
-    if (const char *e = std::getenv("SKC_DIRECT_NW")) p->NW = std::max(1, std::min(8, std::atoi(e)));
+    if (const char *e = std::getenv("SKC_DIRECT_NW")) p->NW = std::max(1, std::min(16, std::atoi(e)));
     if (const char *e = std::getenv("SKC_DIRECT_M")) p->M = std::max(1, std::min(4, std::atoi(e)));
     while (p->M > 1 && p->NW * p->M > p->Kg * 2) p->M /= 2;
     if (!direct_supported(p->T, p->M))
@@ -312,12 +312,7 @@ skc_status build_direct_image(skc_plan *p) {
     const int slab = g.NI * g.img_stride;
     g.stage_floats = slab + 2 * stream_cap + 32;  // +32: empty slots read off + lane
     const size_t stage_bytes = size_t(g.stage_floats) * 4;
-    // shared memory per CTA: 3 CTAs/SM when the tile's register cap allows it (see
-    // direct_min_blocks in sconv_direct.cu), else 2; SKC_DIRECT_SMEM_KB overrides
-    size_t budget = (p->T * (p->M + 2) <= 48) ? (72u << 10) : kSmemBudget;
-    if (budget / stage_bytes < 3) budget = kSmemBudget;  // keep >= 3 stages of overlap
-    if (const char *e = std::getenv("SKC_DIRECT_SMEM_KB")) budget = size_t(std::atoi(e)) << 10;
-    g.NS = int(std::min<size_t>(4, std::max<size_t>(1, budget / stage_bytes)));
+    g.NS = int(std::min<size_t>(4, std::max<size_t>(1, kSmemBudget / stage_bytes)));
     g.NS = std::min(g.NS, std::max(1, g.nchunks));
     if (size_t(g.NS) * stage_bytes + 2 * kMaxStages * 8 > (227u << 10))
         return fail(SKC_ERR_UNSUPPORTED, "direct stage of %zu B does not fit", stage_bytes);

@@ -87,13 +87,8 @@ __device__ __forceinline__ void produce(const DirectParams &p, float *dst, uint6
     }
 }
 
-// Register cap: small tiles (T*(M+2) <= 48 live values) fit three 288-thread CTAs per SM
-// (<= 75 registers), larger ones two.
 template <int T, int M>
-constexpr int direct_min_blocks() { return T * (M + 2) <= 48 ? 3 : 1; }
-
-template <int T, int M>
-__global__ void __launch_bounds__(288, direct_min_blocks<T, M>()) sconv_direct_kernel(const DirectParams p) {
+__global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams p) {
     extern __shared__ __align__(128) float smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + size_t(p.NS) * p.stage_floats);
     uint64_t *empty = full + kMaxStages;
@@ -214,7 +209,7 @@ cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
     }
     const int64_t grid =
         int64_t((p.N + p.NI - 1) / p.NI) * p.nbands * p.groups * p.cblocks;
-    if (grid > 0x7fffffff || p.NW < 1 || p.NW > 8) return cudaErrorInvalidConfiguration;
+    if (grid > 0x7fffffff || p.NW < 1 || p.NW > 16) return cudaErrorInvalidConfiguration;
     fn<<<unsigned(grid), (p.NW + 1) * 32, smem, st>>>(p);
     return cudaGetLastError();
 }
