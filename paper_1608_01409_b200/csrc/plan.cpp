@@ -165,8 +165,11 @@ skc_status configure_direct(skc_plan *p) {
         return fail(SKC_ERR_UNSUPPORTED, "output %dx%d too large for the direct kernel", Ho, Wo);
     const int64_t plane = int64_t(p->Hp) * p->Wp;
     double best_cost = 1e300;
+    const char *nb_env = std::getenv("SKC_DIRECT_BANDS");
+    const int nb_force = nb_env ? std::atoi(nb_env) : 0;
     for (int NI = 1; NI <= p->max_ni; NI *= 2) {
         for (int nb = 1; nb <= Ho; ++nb) {
+            if (nb_force > 0 && nb != std::min(nb_force, Ho)) continue;
             const int BH = (Ho + nb - 1) / nb;
             if ((Ho + BH - 1) / BH != nb) continue;  // same BH as a smaller nb
             const int BHin = std::min((BH - 1) * p->stride + p->R, p->Hp);
@@ -800,8 +803,13 @@ skc_status skc_pack_fc(const float *w, int M, int K, int B, int kernel, skc_plan
     // Y[M x B] = W[M x K] X[K x B] is the 1x1 convolution of one "image" with K channels of
     // 1 x B pixels: PAPER.md:318-329 (sparse FC layers as SpMDM)
     if (B < 1) return fail(SKC_ERR_GEOMETRY, "batch B = %d < 1", B);
-    // one "image" per call: never stage more than one image per CTA
-    return pack_common(w, M, K, 1, 1, 1, B, 1, 0, 1, kernel, 1, out);
+    // one "image" per call: never stage more than one image per CTA.  The batch axis may be
+    // folded into rows (B = rows x B/rows, same memory layout) so the direct kernel can split
+    // it into bands -- more CTAs for a single image (SKC_FC_ROWS, tuning)
+    int rows = 1;
+    if (const char *e = std::getenv("SKC_FC_ROWS")) rows = std::max(1, std::atoi(e));
+    if (B % rows) rows = 1;
+    return pack_common(w, M, K, 1, 1, rows, B / rows, 1, 0, 1, kernel, 1, out);
 }
 
 skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
