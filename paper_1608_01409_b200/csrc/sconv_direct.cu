@@ -25,6 +25,8 @@
 //     layer's zero-padded layout.
 // Accumulation order per output element: CSR order (c ascending, then r, s) -> bitwise
 // deterministic results.
+#include <atomic>
+
 #include "ptx.cuh"
 #include "skc_internal.h"
 
@@ -199,13 +201,17 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
 
 template <int T, int M>
 cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
-    static bool attr_set = false;
+    // the opt-in shared-memory limit is a per-device function attribute: set it once per
+    // device this process launches on
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     auto fn = sconv_direct_kernel<T, M>;
-    if (!attr_set) {
+    if (!(attr_set.load(std::memory_order_acquire) >> dev & 1u)) {
         cudaError_t e =
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel);
     }
     const int64_t grid =
         int64_t((p.N + p.NI - 1) / p.NI) * p.nbands * p.groups * p.cblocks;

@@ -20,6 +20,8 @@
 // images by TMA bulk copies, together with the op-stream segment of the chunk, into a ring
 // of NS stages.  There is no producer warp: the last warp to release a stage (an atomic
 // counter) refills it with chunk i+NS.
+#include <atomic>
+
 #include "ptx.cuh"
 #include "skc_internal.h"
 #include "regtile_gen.inc"
@@ -147,13 +149,17 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
 
 template <int R, int S, int TY, int TX, int M, int NWMAX, int MINB>
 cudaError_t launch_shape(const RegtileParams &p, size_t smem, cudaStream_t st) {
-    static bool attr_set = false;
+    // the opt-in shared-memory limit is a per-device function attribute: set it once per
+    // device this process launches on
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     auto fn = sconv_regtile_kernel<R, S, TY, TX, M, NWMAX, MINB>;
-    if (!attr_set) {
+    if (!(attr_set.load(std::memory_order_acquire) >> dev & 1u)) {
         cudaError_t e =
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel);
     }
     const int64_t grid = int64_t((p.N + p.NI - 1) / p.NI) * p.groups * p.nblocks;
     if (grid > 0x7fffffff || p.NG * p.NT > NWMAX) return cudaErrorInvalidConfiguration;
