@@ -399,3 +399,26 @@ def test_sparse_fc_small_vs_oracle():
         y = fc.forward(torch.from_numpy(x).cuda()).cpu().numpy()
         ref, bound = oracle.conv2d_fp64(x.reshape(1, K, 1, B), w.reshape(M, K, 1, 1))
         check(y.reshape(1, M, 1, B), ref, bound, f"fc {M}x{K}x{B}")
+
+
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_batch_split_invariance(kernel):
+    """a batch-sharded multi-GPU run must be bitwise identical to the
+    1-GPU run.  CTAs stage NI images together, so this holds iff each image's result does
+    not depend on which images share its CTA: run the full batch, then shards of it at odd
+    offsets (as dist.shard_range produces), and compare bit for bit."""
+    from paper_1608_01409_b200 import dist as skd
+    for li in range(4):
+        L = wl.CONFIGS[2].layers[li]
+        w = wl.gen_weights(2, li, L)
+        n = 37
+        x = wl.gen_input(2, li, L, 0, n)
+        full, conv = run_gpu(w, x, L, kernel)
+        for world in (2, 3, 8):
+            parts = []
+            for r in range(world):
+                lo, hi = skd.shard_range(n, world, r)
+                xs = torch.from_numpy(x[lo:hi]).cuda()
+                parts.append(conv.forward(xs).cpu().numpy())
+            np.testing.assert_array_equal(np.concatenate(parts).view(np.uint32),
+                                          full.view(np.uint32))
