@@ -60,7 +60,10 @@ typedef struct skc_plan skc_plan; /* opaque */
 typedef enum {
     SKC_KERNEL_AUTO = 0,
     SKC_KERNEL_DIRECT = 1,   /* Fig. 2 statement per lane: one shared-memory read per MAC */
-    SKC_KERNEL_REGTILE = 2   /* register-tiled input window, per-nonzero dispatch        */
+    SKC_KERNEL_REGTILE = 2,  /* register-tiled input window, per-nonzero dispatch        */
+    SKC_KERNEL_JIT = 3       /* "compiled weights": the CSR walk emitted as straight-line
+                                sm_100a code (immediate weights, register windows, packed
+                                FFMA2), compiled at plan time, see skc_plan_compile      */
 } skc_kernel;
 
 typedef struct {
@@ -76,6 +79,13 @@ typedef struct {
     int lane_mapping;              /* direct kernel: images sharing residue-bucketed slots */
     int tile_h, tile_w;            /* regtile kernel: register tile per lane (0: direct)  */
     int images_per_cta;            /* images staged together in one CTA                   */
+    /* JIT kernel (kernel == SKC_KERNEL_JIT; zero otherwise) */
+    int jit_blocks;                /* channel blocks = separately compiled code modules   */
+    int jit_compiled;              /* 1 once skc_plan_compile / upload compiled the code  */
+    int jit_cache_hit;             /* 1 if the linked code came from the on-disk cache    */
+    double jit_compile_s;          /* wall seconds of generate + compile + link           */
+    size_t code_bytes;             /* linked device code (cubin) bytes                    */
+    double model_instr_per_image;  /* modelled warp-instructions per image (JIT config)   */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).
@@ -171,6 +181,15 @@ skc_status skc_forward_host(const skc_plan *plan, const float *h_in, float *h_ou
 /* Layout function f(c,y,x) of the padded input: test hook.
  * Returns -1 when (c,y,x) is outside [0,C) x [0,Hp) x [0,Wp). */
 int64_t skc_layout_offset(const skc_plan *plan, int c, int y, int x);
+
+/* JIT kernel only: generate, compile (PTX compiler library, one module per channel block,
+ * in parallel host threads) and link (nvJitLink) the plan's code now, on the host -- no GPU
+ * is needed.  Otherwise this happens in skc_plan_upload.  The linked cubin is cached on disk
+ * under $SKC_JIT_CACHE (default $HOME/.cache/skc_jit), keyed by a hash of the generated
+ * code; SKC_JIT_NOCACHE=1 disables the cache.  No-op for other kernels.
+ * Errors: SKC_ERR_ARG (NULL), SKC_ERR_UNSUPPORTED (compile or link failed; message in
+ * skc_last_error). */
+skc_status skc_plan_compile(skc_plan *plan);
 
 /* Static self-check of a plan (host only, no GPU): every kernel-private index the kernels
  * will dereference -- shared-memory windows and pixel slots against the stage and allocation

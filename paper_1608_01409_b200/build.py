@@ -19,7 +19,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include"),
           "-I", CSRC]
-SOURCES = ["plan.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu"]
+SOURCES = ["plan.cpp", "jit.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu"]
+# the JIT kernel compiles and links its generated code in-process (no ptxas on PATH needed)
+CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+JIT_LIBS = [os.path.join(CUDA_LIB, "libnvJitLink_static.a"),
+            os.path.join(CUDA_LIB, "libnvptxcompiler_static.a"), "-lpthread", "-ldl", "-lrt"]
 HEADERS = ["skc_internal.h", "ptx.cuh", "regtile_gen.inc"]
 
 
@@ -53,7 +57,7 @@ def build(force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
     if force or _newer(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + JIT_LIBS
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -1,0 +1,1209 @@
+// jit.cpp -- rows a3..a6, "compiled weights" variant of direct sparse convolution.
+//
+// Same computation as Fig. 2:  out[k][y][x] += w * in[f(c,r,s) + f(0,y,x)]
+// for every nonzero w = W(k,c,r,s), accumulated in CSR order.  The sparse matrix is known
+// before the layer runs ("pre-computed"), so instead of walking a (w, off)
+// stream at run time, the plan emits the walk itself as straight-line sm_100a code:
+//
+//   for each input channel c (ascending; staged CB at a time in shared memory by TMA):
+//       load the lane's input-window positions that the block's nonzeros at c touch:
+//           ld.shared [lane base + f(c, y, x)]        -- f folded into an immediate
+//       for each nonzero (m, r, s, w) of the block's M output channels at c, in CSR order:
+//           acc[m][ty][tx] += w * win[ty + r][tx + s]  -- FFMA2 (fma.rn.f32x2) with w as an
+//                                                         immediate, two pixels per instruction
+//
+// Each lane owns a TY x TX output tile (register blocking of the y, x loops,
+// PAPER.md:309-310) for M output channels; pixels tx and tx + PX share one packed FFMA2, so
+// the window is held as register pairs (win[u], win[u + PX]) and every (r, s) shift of the
+// tile is an aligned pair.  There is no per-nonzero dispatch, no weight or offset load and
+// no address arithmetic in the inner code: the instruction stream is FFMA2 + window loads.
+// Straight-line code does not fit the instruction cache, so B200 runs it at the
+// instruction-fetch rate; the design therefore minimises instructions per MAC: packed pairs
+// (64 MACs per warp instruction), needed-only window loads, volatile (CSE-free) pair loads
+// so no register moves are needed to build pairs.
+//
+// Code layout: one PTX module per channel block (a .func holding the block's whole walk and
+// its epilogue), compiled in parallel with the PTX compiler library and linked by nvJitLink
+// with an entry module (stage setup, lane tables, dispatch on the CTA's block).  Loaded with
+// cudaLibraryLoadData at the first launch, launched with cudaLaunchKernel.
+#include "skc.h"
+#include "skc_internal.h"
+
+#include <nvJitLink.h>
+#include <nvPTXCompiler.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <sys/stat.h>
+#include <thread>
+#include <unistd.h>
+#include <vector>
+
+namespace skc {
+
+namespace {
+
+constexpr int kMaxSmem = 227 * 1024;
+constexpr int kStageTarget = 72 * 1024;
+// cost model (clk per image): unique-code fetch ~0.12 instr/clk/SM, shared by the CTA's warps;
+// issue ~2.5 warp-instr/clk/SM (fitted to the B200 sweeps in profiles/r01_jit_*.jsonl)
+constexpr double kFetchInv = 1.0 / 0.12;
+constexpr double kIssue = 2.5;
+constexpr int kJitVersion = 5;  // bump when the generated code changes (cache key)
+
+// Fast appender for the (large) generated PTX.
+struct Out {
+    std::string s;
+    void operator()(const char *fmt, ...) __attribute__((format(printf, 2, 3))) {
+        char buf[320];
+        va_list ap;
+        va_start(ap, fmt);
+        const int n = vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        s.append(buf, size_t(std::max(0, std::min<int>(n, int(sizeof buf) - 1))));
+        s.push_back('\n');
+    }
+};
+
+uint32_t fbits(float v) {
+    uint32_t u;
+    std::memcpy(&u, &v, 4);
+    return u;
+}
+
+uint64_t fnv1a(const void *data, size_t n, uint64_t h = 1469598103934665603ull) {
+    const uint8_t *p = static_cast<const uint8_t *>(data);
+    for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return h;
+}
+
+// One nonzero of a block at one input channel: output-channel slot m, tap (r, s), weight.
+struct JNz {
+    int m, r, s;
+    float w;
+};
+
+}  // namespace
+
+struct JitPlan {
+    JitInput in{};
+    // configuration
+    int TY = 0, TX = 0, PX = 0;  // lane tile; pixel pairs (tx, tx + PX) for tx < PX
+    int M = 0, NW = 0, NI = 0, CB = 0, NS = 0, nchunks = 0;
+    int tiles_y = 0, tiles_x = 0;
+    int plane = 0, img_stride = 0, stage_bytes = 0;
+    int off_bar = 0, off_cnt = 0, off_info = 0;
+    size_t smem = 0;
+    int maxreg = 255;          // register cap of the block functions (NW warps per SM)
+    int nbg = 0, nblocks = 0;  // blocks per group, total blocks
+    double cost = 0;           // modelled warp-instructions per image
+    int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
+    std::vector<int32_t> chan; // [nblocks][M] original output channel or -1
+    std::vector<uint32_t> lanemap;  // [NW*32][4]: lane smem byte base, pos, store mask, 0
+    // compiled code
+    std::vector<char> cubin;
+    uint64_t key = 0;
+    bool compiled = false;
+    double compile_s = 0;
+    int cache_hit = 0;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    std::atomic<uint64_t> attr_set{0};
+    std::mutex mu;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// nonzeros per block and channel
+// ---------------------------------------------------------------------------------------
+
+// Block q of group g: sorted channels perm[g*Kg + q*M ...] (nnz-descending, PAPER.md:313-314
+// load balance via the plan's permutation).
+void block_channels(const JitInput &in, int M, int g, int q, std::vector<int> &ks) {
+    ks.clear();
+    for (int m = 0; m < M; ++m) {
+        const int idx = q * M + m;
+        if (idx < in.Kg) ks.push_back(in.perm[size_t(g) * in.Kg + size_t(idx)]);
+    }
+}
+
+// A block's nonzeros per local input channel, in CSR order per output channel.
+void block_nz(const JitInput &in, const std::vector<int> &ks,
+              std::vector<std::vector<JNz>> &per_c) {
+    per_c.assign(size_t(in.Cg), {});
+    const int64_t plane = int64_t(in.Hp) * in.Wp;
+    for (size_t m = 0; m < ks.size(); ++m) {
+        const int k = ks[m];
+        const int64_t gbase = int64_t(k / in.Kg) * in.Cg * plane;
+        for (int32_t j = in.rowptr[k]; j < in.rowptr[k + 1]; ++j) {
+            const int64_t off = in.colidx[j] - gbase;
+            const int cl = int(off / plane);
+            const int rem = int(off % plane);
+            per_c[size_t(cl)].push_back(JNz{int(m), rem / in.Wp, rem % in.Wp, in.values[j]});
+        }
+    }
+}
+
+// Window positions (wy * WCw + wx, relative to the lane's tile origin) a channel's
+// nonzeros touch: `pairs` are loaded as (win[u], win[u + PX*st]) register pairs, `scalars`
+// (the odd column of an odd-width tile) only where no pair half already holds them.
+struct Need {
+    std::vector<int> pairs, scalars;
+    std::vector<uint32_t> stamp_p, stamp_s;
+    uint32_t gen = 0;
+    void reset(size_t n) {
+        if (stamp_p.size() < n) {
+            stamp_p.assign(n, 0);
+            stamp_s.assign(n, 0);
+            gen = 0;
+        }
+        ++gen;
+        pairs.clear();
+        scalars.clear();
+    }
+};
+
+void window_need(const std::vector<JNz> &nz, int TY, int TX, int PX, int st, int WRw, int WCw,
+                 Need &nd) {
+    nd.reset(size_t(WRw) * WCw);
+    for (const JNz &z : nz)
+        for (int ty = 0; ty < TY; ++ty) {
+            const int row = (ty * st + z.r) * WCw;
+            for (int q = 0; q < PX; ++q) {
+                const int u = row + q * st + z.s;
+                if (nd.stamp_p[size_t(u)] != nd.gen) {
+                    nd.stamp_p[size_t(u)] = nd.gen;
+                    nd.pairs.push_back(u);
+                }
+            }
+            for (int tx = 2 * PX; tx < TX; ++tx) {
+                const int v = row + tx * st + z.s;
+                if (nd.stamp_s[size_t(v)] != nd.gen) {
+                    nd.stamp_s[size_t(v)] = nd.gen;
+                    nd.scalars.push_back(v);
+                }
+            }
+        }
+    std::sort(nd.pairs.begin(), nd.pairs.end());
+    std::sort(nd.scalars.begin(), nd.scalars.end());
+    // scalars already held as the low or high half of a loaded pair need no load
+    std::vector<int> keep;
+    for (int v : nd.scalars) {
+        const bool lo = nd.stamp_p[size_t(v)] == nd.gen;
+        const bool hi = (v % WCw) >= PX * st && nd.stamp_p[size_t(v - PX * st)] == nd.gen;
+        if (!lo && !hi) keep.push_back(v);
+    }
+    nd.scalars.swap(keep);
+}
+
+int window_regs(int TY, int TX, int PX, int R, int S, int st) {
+    const int rows = (TY - 1) * st + R;
+    if (PX == 0) return rows * ((TX - 1) * st + S);
+    const int npc = (PX - 1) * st + S;
+    return rows * (2 * npc + (TX > 2 * PX ? st + 1 : 0));
+}
+
+// Register cap per thread for NW warps on one SM: warps are spread over the 4 SM
+// sub-partitions, each with a 16K-register file, so ceil(NW/4) * regs * 32 <= 16384.
+int reg_cap(int NW) {
+    const int per = 16384 / (32 * ((NW + 3) / 4));
+    return per >= 256 ? 255 : (per & ~7);
+}
+
+// Modelled warp-instructions of one block's code (per CTA pass).
+double block_instr(const JitInput &in, const std::vector<std::vector<JNz>> &per_c, int TY,
+                   int TX, int PX, int CB, int Mb, Need &nd) {
+    const int st = in.stride, WRw = (TY - 1) * st + in.R, WCw = (TX - 1) * st + in.S;
+    double n = 0;
+    for (int c = 0; c < in.Cg; ++c) {
+        const auto &nz = per_c[size_t(c)];
+        if (nz.empty()) continue;
+        window_need(nz, TY, TX, PX, st, WRw, WCw, nd);
+        n += double(nz.size()) * TY * (PX + (TX - 2 * PX));
+        n += 2.0 * double(nd.pairs.size()) + double(nd.scalars.size());
+    }
+    n += ((in.Cg + CB - 1) / CB) * 14.0;
+    n += Mb * (TY * TX * 4.0 + TY * 3.0);
+    return n;
+}
+
+// ---------------------------------------------------------------------------------------
+// lane assignment: the tiles of the NI image slots onto NW warps x 32 lanes, first fit by
+// shared-memory bank residue of the lane base, so that a warp's window load (one
+// immediate offset for all lanes) touches 32 distinct banks
+// ---------------------------------------------------------------------------------------
+struct Tile {
+    int img, y0, x0, ry0, rx0;  // origin (shifted back inside the image), nominal origin
+};
+
+int assign_lanes(const JitPlan &jp, int IS, std::vector<uint32_t> *lanemap) {
+    const JitInput &in = jp.in;
+    const int st = in.stride;
+    std::vector<Tile> tiles;
+    for (int j = 0; j < jp.NI; ++j)
+        for (int iy = 0; iy < jp.tiles_y; ++iy)
+            for (int ix = 0; ix < jp.tiles_x; ++ix) {
+                const int ry = iy * jp.TY, rx = ix * jp.TX;
+                tiles.push_back(
+                    Tile{j, std::min(ry, in.Ho - jp.TY), std::min(rx, in.Wo - jp.TX), ry, rx});
+            }
+    std::vector<int> base(tiles.size());
+    for (size_t i = 0; i < tiles.size(); ++i)
+        base[i] = tiles[i].img * IS + tiles[i].y0 * st * in.Wp + tiles[i].x0 * st;
+    std::vector<char> used(tiles.size(), 0);
+    std::vector<int> lane_tile(size_t(jp.NW) * 32, -1);
+    size_t left = tiles.size();
+    int extra = 0;
+    for (int w = 0; w < jp.NW && left; ++w) {
+        int cnt[32] = {0};
+        int filled = 0;
+        // pass 0: distinct residues only; pass 1: any tile, when the remaining warps could
+        // not take the rest conflict-free anyway
+        for (int pass = 0; pass < 2 && filled < 32 && left; ++pass) {
+            if (pass == 1 && int(left) <= (jp.NW - w - 1) * 32) break;
+            for (size_t i = 0; i < tiles.size() && filled < 32; ++i) {
+                if (used[i]) continue;
+                const int res = base[i] & 31;
+                if (pass == 0 && cnt[res]) continue;
+                used[i] = 1;
+                --left;
+                ++cnt[res];
+                lane_tile[size_t(w) * 32 + size_t(filled++)] = int(i);
+                if (pass == 1 && int(left) <= (jp.NW - w - 1) * 32) break;
+            }
+        }
+        int mx = 0;
+        for (int r = 0; r < 32; ++r) mx = std::max(mx, cnt[r]);
+        extra += std::max(0, mx - 1);
+    }
+    if (left) return -1;  // does not fit
+    if (lanemap) {
+        lanemap->assign(size_t(jp.NW) * 32 * 4, 0);
+        for (int w = 0; w < jp.NW; ++w)
+            for (int l = 0; l < 32; ++l) {
+                int ti = lane_tile[size_t(w) * 32 + size_t(l)];
+                const bool idle = ti < 0;
+                if (idle) ti = lane_tile[size_t(w) * 32];  // mirror lane 0 (broadcast loads)
+                if (ti < 0) ti = 0;                        // whole warp idle
+                const Tile &t = tiles[size_t(ti)];
+                uint32_t mask = 0;
+                if (!idle)
+                    for (int ty = 0; ty < jp.TY; ++ty)
+                        for (int tx = 0; tx < jp.TX; ++tx) {
+                            const int y = t.y0 + ty, x = t.x0 + tx;
+                            // pixels of a shifted-back tile that an earlier tile owns are
+                            // computed twice but stored once
+                            if (y >= t.ry0 && x >= t.rx0 && y < in.Ho && x < in.Wo)
+                                mask |= 1u << (ty * jp.TX + tx);
+                        }
+                uint32_t *e = lanemap->data() + (size_t(w) * 32 + size_t(l)) * 4;
+                e[0] = uint32_t(base[size_t(ti)]) * 4u;
+                e[1] = (uint32_t(t.img) << 24) | (uint32_t(t.y0) << 12) | uint32_t(t.x0);
+                e[2] = mask;
+                e[3] = idle ? 1u : 0u;
+            }
+    }
+    return extra;
+}
+
+// ---------------------------------------------------------------------------------------
+// PTX emission
+// ---------------------------------------------------------------------------------------
+const char *kHdr = ".version 8.8\n.target sm_100a\n.address_size 64\n";
+const char *kBlkParams =
+    "(.param .b32 q_lb, .param .b32 q_sm, .param .b64 q_out, .param .b32 q_mask, "
+    ".param .b32 q_nimg, .param .b64 q_bias, .param .b32 q_relu, .param .b32 q_rs, "
+    ".param .b64 q_cs)";
+
+int chunk_channels(const JitPlan &jp, int i) { return std::min(jp.CB, jp.in.Cg - i * jp.CB); }
+
+std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
+                       const std::vector<std::vector<JNz>> &per_c) {
+    const JitInput &in = jp.in;
+    const int st = in.stride, TY = jp.TY, TX = jp.TX, PX = jp.PX;
+    const int WRw = (TY - 1) * st + in.R, WCw = (TX - 1) * st + in.S;
+    const int NWIN = WRw * WCw;
+    const int Mb = int(ks.size());
+    const int NPT = TY * PX, NST = TY * (TX - 2 * PX);
+    Out o;
+    o.s.reserve(1 << 20);
+    o("%s", kHdr);
+    o(".visible .func skc_b%d%s", b, kBlkParams);
+    o("{");
+    o(".reg .pred %%p<8>;");
+    o(".reg .b32 %%r<24>;");
+    o(".reg .b64 %%rd<12>;");
+    o(".reg .b32 %%rb<%d>;", jp.NS);
+    o(".reg .b64 %%a<%d>;", std::max(1, Mb * NPT));
+    o(".reg .f32 %%f<%d>;", std::max(1, Mb * NST));
+    o(".reg .f32 %%wl<%d>;", NWIN);
+    o(".reg .f32 %%wh<%d>;", NWIN);
+    o(".reg .f32 %%ws<%d>;", NWIN);
+    o(".reg .b64 %%wp<%d>;", NWIN);
+    o(".reg .b64 %%wt;");
+    o(".reg .f32 %%e<4>;");
+    o("ld.param.b32 %%r0, [q_lb];");
+    o("ld.param.b32 %%r1, [q_sm];");
+    o("ld.param.b64 %%rd0, [q_out];");
+    o("ld.param.b32 %%r2, [q_mask];");
+    o("ld.param.b32 %%r3, [q_nimg];");
+    o("ld.param.b64 %%rd1, [q_bias];");
+    o("ld.param.b32 %%r4, [q_relu];");
+    o("ld.param.b32 %%r5, [q_rs];");
+    o("ld.param.b64 %%rd2, [q_cs];");
+    o("mov.u32 %%r6, %%laneid;");
+    o("setp.eq.u32 %%p0, %%r6, 0;");
+    o("mov.u32 %%r7, 0;");
+    o("mov.u32 %%r8, 1;");
+    o("add.u32 %%rb0, %%r1, %%r0;");
+    for (int s = 1; s < jp.NS; ++s) o("add.u32 %%rb%d, %%rb0, %d;", s, s * jp.stage_bytes);
+    for (int i = 0; i < Mb * NPT; ++i) o("mov.b64 %%a%d, 0;", i);
+    for (int i = 0; i < Mb * NST; ++i) o("mov.f32 %%f%d, 0f00000000;", i);
+
+    Need nd;
+    for (int i = 0; i < jp.nchunks; ++i) {
+        const int s = i % jp.NS;
+        const int par = (i / jp.NS) & 1;
+        o("$W%d:", i);
+        o("mbarrier.try_wait.parity.shared::cta.b64 %%p4, [%%r1+%d], %%r%d;", jp.off_bar + 8 * s,
+          par ? 8 : 7);
+        o("@!%%p4 bra $W%d;", i);
+        const int cn = chunk_channels(jp, i);
+        for (int cl = 0; cl < cn; ++cl) {
+            const int c = i * jp.CB + cl;
+            const auto &nz = per_c[size_t(c)];
+            if (nz.empty()) continue;
+            window_need(nz, TY, TX, PX, st, WRw, WCw, nd);
+            const int cbase = cl * jp.plane;
+            auto off = [&](int u) { return (cbase + (u / WCw) * in.Wp + (u % WCw)) * 4; };
+            for (int u : nd.pairs) {
+                o("ld.volatile.shared.f32 %%wl%d, [%%rb%d+%d];", u, s, off(u));
+                o("ld.volatile.shared.f32 %%wh%d, [%%rb%d+%d];", u, s, off(u + PX * st));
+                o("mov.b64 %%wp%d, {%%wl%d, %%wh%d};", u, u, u);
+            }
+            for (int v : nd.scalars) o("ld.volatile.shared.f32 %%ws%d, [%%rb%d+%d];", v, s, off(v));
+            // which register holds scalar position v
+            auto sreg = [&](int v, char *buf) {
+                if (nd.stamp_p[size_t(v)] == nd.gen)
+                    std::snprintf(buf, 32, "%%wl%d", v);
+                else if ((v % WCw) >= PX * st && nd.stamp_p[size_t(v - PX * st)] == nd.gen)
+                    std::snprintf(buf, 32, "%%wh%d", v - PX * st);
+                else
+                    std::snprintf(buf, 32, "%%ws%d", v);
+            };
+            char src[32];
+            for (const JNz &z : nz) {
+                const uint32_t wb = fbits(z.w);
+                if (NPT) o("mov.b64 %%wt, 0x%08X%08X;", wb, wb);
+                for (int ty = 0; ty < TY; ++ty) {
+                    const int row = (ty * st + z.r) * WCw;
+                    for (int q = 0; q < PX; ++q) {
+                        const int a = z.m * NPT + ty * PX + q;
+                        o("fma.rn.f32x2 %%a%d, %%wt, %%wp%d, %%a%d;", a, row + q * st + z.s, a);
+                    }
+                    for (int tx = 2 * PX; tx < TX; ++tx) {
+                        const int f = z.m * NST + ty * (TX - 2 * PX) + (tx - 2 * PX);
+                        sreg(row + tx * st + z.s, src);
+                        o("fma.rn.f32 %%f%d, %s, 0f%08X, %%f%d;", f, src, wb, f);
+                    }
+                }
+            }
+        }
+        // release the stage; the last warp out refills it with chunk i + NS
+        if (i + jp.NS < jp.nchunks) {
+            const int nxt = i + jp.NS;
+            const int bytes = chunk_channels(jp, nxt) * jp.plane * 4;
+            o("bar.warp.sync -1;");
+            o("@!%%p0 bra $R%d;", i);
+            o("fence.acq_rel.cta;");
+            o("atom.shared.add.u32 %%r10, [%%r1+%d], 1;", jp.off_cnt + 4 * s);
+            o("setp.ne.u32 %%p5, %%r10, %d;", jp.NW * (i / jp.NS + 1) - 1);
+            o("@%%p5 bra $R%d;", i);
+            o("fence.proxy.async.shared::cta;");
+            o("add.u32 %%r15, %%r1, %d;", jp.off_bar + 8 * s);
+            o("mul.lo.u32 %%r11, %%r3, %d;", bytes);
+            o("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%%r15], %%r11;");
+            o("mov.u32 %%r12, 0;");
+            o("$L%d:", i);
+            o("shl.b32 %%r13, %%r12, 3;");
+            o("add.u32 %%r13, %%r13, %%r1;");
+            o("ld.shared.u64 %%rd6, [%%r13+%d];", jp.off_info);
+            o("add.u64 %%rd6, %%rd6, %lld;", (long long)nxt * jp.CB * jp.plane * 4);
+            o("mad.lo.u32 %%r14, %%r12, %d, %%r1;", jp.img_stride * 4);
+            o("add.u32 %%r14, %%r14, %d;", s * jp.stage_bytes);
+            o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r14], [%%rd6], "
+              "%d, [%%r15];", bytes);
+            o("add.u32 %%r12, %%r12, 1;");
+            o("setp.lt.u32 %%p6, %%r12, %%r3;");
+            o("@%%p6 bra $L%d;", i);
+            o("$R%d:", i);
+        }
+    }
+
+    // a6: epilogue -- out = act(acc + bias[k]) at the original channel index; stores only
+    // the pixels this lane owns (mask)
+    o("setp.ne.u64 %%p1, %%rd1, 0;");
+    o("setp.ne.u32 %%p2, %%r4, 0;");
+    for (int m = 0; m < Mb; ++m) {
+        const int k = ks[size_t(m)];
+        o("mov.f32 %%e2, 0f00000000;");
+        o("@%%p1 ld.global.nc.f32 %%e2, [%%rd1+%d];", 4 * k);
+        o("mul.lo.u64 %%rd3, %%rd2, %d;", k);
+        o("add.u64 %%rd3, %%rd0, %%rd3;");
+        for (int ty = 0; ty < TY; ++ty) {
+            if (ty == 0) {
+                o("mov.b64 %%rd4, %%rd3;");
+            } else {
+                o("mul.wide.u32 %%rd5, %%r5, %d;", ty);
+                o("add.u64 %%rd4, %%rd3, %%rd5;");
+            }
+            for (int tx = 0; tx < TX; ++tx) {
+                const char *val;
+                if (tx < 2 * PX) {
+                    if (tx < PX) o("mov.b64 {%%e0, %%e1}, %%a%d;", m * NPT + ty * PX + tx);
+                    else o("mov.b64 {%%e0, %%e1}, %%a%d;", m * NPT + ty * PX + tx - PX);
+                    val = tx < PX ? "%e0" : "%e1";
+                    o("add.f32 %%e3, %s, %%e2;", val);
+                } else {
+                    o("add.f32 %%e3, %%f%d, %%e2;", m * NST + ty * (TX - 2 * PX) + tx - 2 * PX);
+                }
+                o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
+                o("and.b32 %%r9, %%r2, %u;", 1u << (ty * TX + tx));
+                o("setp.ne.u32 %%p3, %%r9, 0;");
+                o("@%%p3 st.global.f32 [%%rd4+%d], %%e3;", 4 * tx);
+            }
+        }
+    }
+    o("ret;");
+    o("}");
+    return std::move(o.s);
+}
+
+// Entry: a persistent loop over work items t = b * NIG + ig (block-major: channel block b,
+// image group ig), CTA j taking items j, j + G, j + 2G, ...  At any moment the CTAs of the
+// grid therefore run the SAME block's code, started together, so the straight-line code is
+// fetched once for many SMs (instruction fetch is the limit of this kernel).
+std::string emit_entry(const JitPlan &jp) {
+    const JitInput &in = jp.in;
+    Out o;
+    o("%s", kHdr);
+    for (int b = 0; b < jp.nblocks; ++b) o(".extern .func skc_b%d%s;", b, kBlkParams);
+    o(".extern .shared .align 128 .b8 skc_smem[];");
+    o(".visible .entry skc_jit_kernel(.param .u64 p_in, .param .u64 p_out, .param .u64 p_lm, "
+      ".param .u64 p_bias, .param .u32 p_N, .param .u32 p_relu, .param .u32 p_opad)");
+    o("{");
+    o(".reg .pred %%p<8>;");
+    o(".reg .b32 %%r<48>;");
+    o(".reg .b64 %%rd<24>;");
+    o("ld.param.u64 %%rd0, [p_in];");
+    o("cvta.to.global.u64 %%rd0, %%rd0;");
+    o("ld.param.u64 %%rd1, [p_out];");
+    o("cvta.to.global.u64 %%rd1, %%rd1;");
+    o("ld.param.u64 %%rd2, [p_lm];");
+    o("cvta.to.global.u64 %%rd2, %%rd2;");
+    o("ld.param.u64 %%rd3, [p_bias];");
+    o("setp.eq.u64 %%p7, %%rd3, 0;");
+    o("@!%%p7 cvta.to.global.u64 %%rd3, %%rd3;");
+    o("ld.param.u32 %%r0, [p_N];");
+    o("ld.param.u32 %%r1, [p_relu];");
+    o("ld.param.u32 %%r2, [p_opad];");
+    o("mov.u32 %%r3, %%tid.x;");
+    // item t = u * CS + rank for cluster-level items u = clusterid, clusterid + nclusters, ...
+    // (CS = cluster size, 1 without clusters): the CTAs of a cluster -- co-scheduled on one
+    // GPC, which shares one L1.5 instruction cache -- run the same block's code together
+    o("mov.u32 %%r35, %%cluster_ctarank;");
+    o("mov.u32 %%r36, %%cluster_nctarank;");
+    o("mov.u32 %%r37, %%clusterid.x;");
+    o("mov.u32 %%r38, %%nclusterid.x;");
+    o("mad.lo.u32 %%r4, %%r37, %%r36, %%r35;");   // item t
+    o("mul.lo.u32 %%r31, %%r38, %%r36;");         // stride G
+    o("add.u32 %%r5, %%r0, %d;", jp.NI - 1);
+    o("div.u32 %%r5, %%r5, %d;", jp.NI);   // image groups NIG
+    o("mul.lo.u32 %%r32, %%r5, %d;", jp.nblocks);  // items
+    o("mov.u32 %%r11, skc_smem;");
+    o("mov.u32 %%r34, 1;");                 // first item: barriers not yet initialised
+    // lane table (item independent): {smem byte base, (img<<24)|(y0<<12)|x0, store mask, idle}
+    o("mul.wide.u32 %%rd7, %%r3, 16;");
+    o("add.u64 %%rd7, %%rd2, %%rd7;");
+    o("ld.global.nc.v4.u32 {%%r17, %%r18, %%r33, %%r20}, [%%rd7];");
+    o("shr.u32 %%r21, %%r18, 24;");          // img
+    o("shr.u32 %%r22, %%r18, 12;");
+    o("and.b32 %%r22, %%r22, 4095;");        // y0
+    o("and.b32 %%r23, %%r18, 4095;");        // x0
+    o("add.u32 %%r24, %%r2, %%r2;");
+    o("add.u32 %%r25, %%r24, %d;", in.Ho);   // Hop
+    o("add.u32 %%r26, %%r24, %d;", in.Wo);   // Wop
+    o("mul.lo.u32 %%r27, %%r25, %%r26;");    // Hop*Wop
+    o("add.u32 %%r29, %%r22, %%r2;");
+    o("mad.lo.u32 %%r29, %%r29, %%r26, %%r23;");
+    o("add.u32 %%r29, %%r29, %%r2;");        // (y0+opad)*Wop + x0+opad
+    o("shl.b32 %%r30, %%r26, 2;");           // row stride bytes
+    o("mul.wide.u32 %%rd10, %%r27, 4;");     // channel stride bytes
+    o("$ITEM:");
+    o("setp.ge.u32 %%p0, %%r4, %%r32;");
+    o("@%%p0 bra $EXIT;");
+    o("rem.u32 %%r6, %%r4, %%r5;");          // image group
+    o("div.u32 %%r7, %%r4, %%r5;");          // block
+    o("mul.lo.u32 %%r8, %%r6, %d;", jp.NI);  // n0
+    o("sub.u32 %%r9, %%r0, %%r8;");
+    o("min.u32 %%r9, %%r9, %d;", jp.NI);    // images in this item
+    o("div.u32 %%r10, %%r7, %d;", jp.nbg);  // conv group
+    o("bar.sync 0;");                        // every warp is done with the previous item
+    o("setp.ne.u32 %%p0, %%r3, 0;");
+    o("@%%p0 bra $INIT_DONE;");
+    // barriers of the previous item have completed every phase and have no pending
+    // transfers: invalidate and re-initialise them (phase parity restarts at 0)
+    o("setp.eq.u32 %%p4, %%r34, 0;");
+    for (int s = 0; s < jp.NS; ++s) {
+        o("@%%p4 mbarrier.inval.shared::cta.b64 [%%r11+%d];", jp.off_bar + 8 * s);
+        o("mbarrier.init.shared::cta.b64 [%%r11+%d], 1;", jp.off_bar + 8 * s);
+        o("st.shared.u32 [%%r11+%d], 0;", jp.off_cnt + 4 * s);
+    }
+    o("mov.u32 %%r34, 0;");
+    // per-image source base: in + ((n0 + j) * C + g * Cg) * plane * 4
+    const long long img_bytes = (long long)in.C * jp.plane * 4;
+    o("cvt.u64.u32 %%rd4, %%r8;");
+    o("mul.lo.u64 %%rd4, %%rd4, %lld;", img_bytes);
+    o("cvt.u64.u32 %%rd5, %%r10;");
+    o("mul.lo.u64 %%rd5, %%rd5, %lld;", (long long)in.Cg * jp.plane * 4);
+    o("add.u64 %%rd4, %%rd4, %%rd5;");
+    o("add.u64 %%rd4, %%rd0, %%rd4;");
+    o("mov.u32 %%r12, 0;");
+    o("add.u32 %%r13, %%r11, %d;", jp.off_info);
+    o("$INFO:");
+    o("st.shared.u64 [%%r13], %%rd4;");
+    o("add.u64 %%rd4, %%rd4, %lld;", img_bytes);
+    o("add.u32 %%r13, %%r13, 8;");
+    o("add.u32 %%r12, %%r12, 1;");
+    o("setp.lt.u32 %%p1, %%r12, %%r9;");
+    o("@%%p1 bra $INFO;");
+    o("fence.mbarrier_init.release.cluster;");
+    o("fence.proxy.async.shared::cta;");
+    for (int i = 0; i < std::min(jp.NS, jp.nchunks); ++i) {
+        const int bytes = chunk_channels(jp, i) * jp.plane * 4;
+        o("add.u32 %%r15, %%r11, %d;", jp.off_bar + 8 * i);
+        o("mul.lo.u32 %%r14, %%r9, %d;", bytes);
+        o("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%%r15], %%r14;");
+        o("mov.u32 %%r12, 0;");
+        o("$F%d:", i);
+        o("shl.b32 %%r13, %%r12, 3;");
+        o("add.u32 %%r13, %%r13, %%r11;");
+        o("ld.shared.u64 %%rd6, [%%r13+%d];", jp.off_info);
+        o("add.u64 %%rd6, %%rd6, %lld;", (long long)i * jp.CB * jp.plane * 4);
+        o("mad.lo.u32 %%r16, %%r12, %d, %%r11;", jp.img_stride * 4);
+        o("add.u32 %%r16, %%r16, %d;", i * jp.stage_bytes);
+        o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r16], [%%rd6], "
+          "%d, [%%r15];", bytes);
+        o("add.u32 %%r12, %%r12, 1;");
+        o("setp.lt.u32 %%p1, %%r12, %%r9;");
+        o("@%%p1 bra $F%d;", i);
+    }
+    o("$INIT_DONE:");
+    o("bar.sync 0;");
+    o("mov.u32 %%r19, %%r33;");
+    o("setp.ge.u32 %%p2, %%r21, %%r9;");
+    o("@%%p2 mov.u32 %%r19, 0;");            // image past N: no stores
+    // output lane pointer: out + ((n0+img)*K*Hop*Wop + (y0+opad)*Wop + x0+opad)*4
+    o("add.u32 %%r28, %%r8, %%r21;");
+    o("cvt.u64.u32 %%rd8, %%r28;");
+    o("mul.lo.u64 %%rd8, %%rd8, %d;", in.K);
+    o("cvt.u64.u32 %%rd9, %%r27;");
+    o("mul.lo.u64 %%rd8, %%rd8, %%rd9;");
+    o("cvt.u64.u32 %%rd9, %%r29;");
+    o("add.u64 %%rd8, %%rd8, %%rd9;");
+    o("shl.b64 %%rd8, %%rd8, 2;");
+    o("add.u64 %%rd8, %%rd1, %%rd8;");
+    for (int b = 0; b < jp.nblocks; ++b) {
+        o("setp.eq.u32 %%p3, %%r7, %d;", b);
+        o("@%%p3 bra $C%d;", b);
+    }
+    o("bra.uni $NEXT;");
+    for (int b = 0; b < jp.nblocks; ++b) {
+        o("$C%d:", b);
+        o("{");
+        o(".param .b32 t0;\n.param .b32 t1;\n.param .b64 t2;\n.param .b32 t3;\n.param .b32 t4;");
+        o(".param .b64 t5;\n.param .b32 t6;\n.param .b32 t7;\n.param .b64 t8;");
+        o("st.param.b32 [t0], %%r17;\nst.param.b32 [t1], %%r11;\nst.param.b64 [t2], %%rd8;");
+        o("st.param.b32 [t3], %%r19;\nst.param.b32 [t4], %%r9;\nst.param.b64 [t5], %%rd3;");
+        o("st.param.b32 [t6], %%r1;\nst.param.b32 [t7], %%r30;\nst.param.b64 [t8], %%rd10;");
+        o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8);", b);
+        o("}");
+        o("bra.uni $NEXT;");
+    }
+    o("$NEXT:");
+    o("add.u32 %%r4, %%r4, %%r31;");
+    o("bra.uni $ITEM;");
+    o("$EXIT:");
+    o("ret;");
+    o("}");
+    return std::move(o.s);
+}
+
+// ---------------------------------------------------------------------------------------
+// compile + link (PTX compiler library in a thread pool, nvJitLink), with an on-disk cache
+// ---------------------------------------------------------------------------------------
+bool compile_ptx(const std::string &ptx, const char *opt, int maxreg, std::vector<char> &obj,
+                 std::string *msg) {
+    nvPTXCompilerHandle h = nullptr;
+    if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
+        *msg = "nvPTXCompilerCreate failed";
+        return false;
+    }
+    const std::string mr = "--maxrregcount=" + std::to_string(maxreg);
+    const char *opts[] = {"--gpu-name=sm_100a", "--compile-only", opt, mr.c_str()};
+    const nvPTXCompileResult r = nvPTXCompilerCompile(h, 4, opts);
+    bool okr = r == NVPTXCOMPILE_SUCCESS;
+    if (!okr) {
+        size_t n = 0;
+        nvPTXCompilerGetErrorLogSize(h, &n);
+        std::string log(n, '\0');
+        if (n) nvPTXCompilerGetErrorLog(h, &log[0]);
+        *msg = "PTX compile failed (" + std::to_string(int(r)) + "): " + log.substr(0, 800);
+    } else {
+        size_t n = 0;
+        nvPTXCompilerGetCompiledProgramSize(h, &n);
+        obj.resize(n);
+        nvPTXCompilerGetCompiledProgram(h, obj.data());
+    }
+    nvPTXCompilerDestroy(&h);
+    return okr;
+}
+
+std::string cache_dir() {
+    if (const char *d = std::getenv("SKC_JIT_CACHE")) return d;
+    const char *home = std::getenv("HOME");
+    return std::string(home ? home : "/tmp") + "/.cache/skc_jit";
+}
+
+bool cache_read(uint64_t key, std::vector<char> &out) {
+    if (std::getenv("SKC_JIT_NOCACHE")) return false;
+    char name[64];
+    std::snprintf(name, sizeof name, "/%016llx.cubin", (unsigned long long)key);
+    FILE *f = std::fopen((cache_dir() + name).c_str(), "rb");
+    if (!f) return false;
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    out.resize(size_t(std::max(0L, n)));
+    const bool okr = n > 0 && std::fread(out.data(), 1, out.size(), f) == out.size();
+    std::fclose(f);
+    return okr;
+}
+
+void cache_write(uint64_t key, const std::vector<char> &data) {
+    if (std::getenv("SKC_JIT_NOCACHE")) return;
+    const std::string dir = cache_dir();
+    // mkdir -p (two levels is enough for $HOME/.cache/skc_jit)
+    std::string acc;
+    for (size_t i = 0; i <= dir.size(); ++i)
+        if (i == dir.size() || (dir[i] == '/' && i > 0)) {
+            acc = dir.substr(0, i);
+            mkdir(acc.c_str(), 0755);
+        }
+    char name[96];
+    std::snprintf(name, sizeof name, "/%016llx.cubin", (unsigned long long)key);
+    const std::string tmp = dir + name + ".tmp" + std::to_string(getpid());
+    FILE *f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const bool okw = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+    std::fclose(f);
+    if (okw) std::rename(tmp.c_str(), (dir + name).c_str());
+    else std::remove(tmp.c_str());
+}
+
+
+// ---------------------------------------------------------------------------------------
+// static verification: tables + the emitted code decoded back to the CSR
+// ---------------------------------------------------------------------------------------
+int jit_verify(const JitPlan *jp, std::string *msg) {
+    const JitInput &in = jp->in;
+    const int st = in.stride, TY = jp->TY, TX = jp->TX, PX = jp->PX;
+    auto bad = [&](const std::string &m) {
+        *msg = "verify (jit): " + m;
+        return int(SKC_ERR_STATE);
+    };
+    // channel table: every output channel exactly once, in its own group's blocks
+    std::vector<int> seen(size_t(in.K), 0);
+    for (int b = 0; b < jp->nblocks; ++b)
+        for (int m = 0; m < jp->M; ++m) {
+            const int k = jp->chan[size_t(b) * jp->M + m];
+            if (k < 0) continue;
+            if (k >= in.K || k / in.Kg != b / jp->nbg) return bad("channel in the wrong block");
+            ++seen[size_t(k)];
+        }
+    for (int k = 0; k < in.K; ++k)
+        if (seen[size_t(k)] != 1) return bad("output channel not covered exactly once");
+    // lane table: tiles inside the output (so every window read stays inside its channel
+    // plane of its image slot), lane base consistent, every output pixel of every image slot
+    // stored by exactly one (lane, pixel)
+    std::vector<int> cover(size_t(jp->NI) * in.Ho * in.Wo, 0);
+    for (int l = 0; l < jp->NW * 32; ++l) {
+        const uint32_t *e = jp->lanemap.data() + size_t(l) * 4;
+        const int img = int(e[1] >> 24), y0 = int((e[1] >> 12) & 4095), x0 = int(e[1] & 4095);
+        if (img >= jp->NI || y0 + TY > in.Ho || x0 + TX > in.Wo) return bad("lane tile out of range");
+        if (e[0] != uint32_t(img * jp->img_stride + y0 * st * in.Wp + x0 * st) * 4u)
+            return bad("lane base inconsistent with its tile");
+        if (jp->img_stride < jp->CB * jp->plane) return bad("image slots overlap");
+        for (int b = 0; b < TY * TX; ++b)
+            if (e[2] >> b & 1u) ++cover[(size_t(img) * in.Ho + y0 + b / TX) * in.Wo + x0 + b % TX];
+    }
+    for (int v : cover)
+        if (v != 1) return bad("output pixel stored " + std::to_string(v) + " times");
+    if (size_t(jp->off_info) + size_t(jp->NI) * 8 > jp->smem ||
+        size_t(jp->NS) * jp->stage_bytes > size_t(jp->off_bar) || jp->smem > size_t(kMaxSmem))
+        return bad("shared-memory layout");
+    // code: decode every window load and FMA of every block back to (k, c, r, s, w) per pixel
+    const int NPT = TY * PX, NST = TY * (TX - 2 * PX);
+    std::vector<int> ks;
+    std::vector<std::vector<JNz>> per_c;
+    for (int b = 0; b < jp->nblocks; ++b) {
+        block_channels(in, jp->M, b / jp->nbg, b % jp->nbg, ks);
+        block_nz(in, ks, per_c);
+        const std::string code = emit_block(*jp, b, ks, per_c);
+        const int Mb = int(ks.size());
+        const size_t NWIN = size_t((TY - 1) * st + in.R) * size_t((TX - 1) * st + in.S);
+        std::vector<int> lo_off(NWIN, -1), hi_off(NWIN, -1), sc_off(NWIN, -1);
+        std::vector<int> wp_lo(NWIN, -1), wp_hi(NWIN, -1);
+        uint64_t wt = 0;
+        bool wt_ok = false;
+        int chunk = -1;
+        // per (m, pixel): decoded sequence of (c, r, s, bits)
+        struct Op { int c, r, s; uint32_t w; };
+        std::vector<std::vector<Op>> seq(size_t(Mb) * TY * TX);
+        auto decode = [&](int off, int ty, int tx, Op &op) -> bool {
+            if (off < 0 || off % 4) return false;
+            const int wv = off / 4;
+            const int cl = wv / jp->plane, rem = wv % jp->plane;
+            const int wy = rem / in.Wp, wx = rem % in.Wp;
+            op.c = chunk * jp->CB + cl;
+            op.r = wy - ty * st;
+            op.s = wx - tx * st;
+            return cl < chunk_channels(*jp, chunk) && op.r >= 0 && op.r < in.R && op.s >= 0 &&
+                   op.s < in.S;
+        };
+        size_t pos = 0;
+        while (pos < code.size()) {
+            size_t eol = code.find('\n', pos);
+            if (eol == std::string::npos) eol = code.size();
+            const std::string ln = code.substr(pos, eol - pos);
+            pos = eol + 1;
+            int a0, a1, a2, a3;
+            unsigned u0, u1;
+            char rn[4];
+            if (std::sscanf(ln.c_str(), "$W%d:", &a0) == 1) {
+                if (a0 != chunk + 1) return bad("chunks out of order");
+                chunk = a0;
+                continue;
+            }
+            if (std::sscanf(ln.c_str(), "ld.volatile.shared.f32 %%w%1[lhs]%d, [%%rb%d+%d];", rn, &a0,
+                            &a1, &a2) == 4) {
+                if (a1 != chunk % jp->NS || a0 < 0 || size_t(a0) >= NWIN) return bad("load stage");
+                (rn[0] == 'l' ? lo_off : rn[0] == 'h' ? hi_off : sc_off)[size_t(a0)] = a2;
+                continue;
+            }
+            if (std::sscanf(ln.c_str(), "mov.b64 %%wp%d, {%%wl%d, %%wh%d};", &a0, &a1, &a2) == 3) {
+                if (a0 != a1 || a0 != a2 || size_t(a0) >= NWIN) return bad("pair build");
+                wp_lo[size_t(a0)] = lo_off[size_t(a0)];
+                wp_hi[size_t(a0)] = hi_off[size_t(a0)];
+                continue;
+            }
+            if (std::sscanf(ln.c_str(), "mov.b64 %%wt, 0x%08X%08X;", &u0, &u1) == 2) {
+                if (u0 != u1) return bad("weight pair halves differ");
+                wt = u0;
+                wt_ok = true;
+                continue;
+            }
+            if (std::sscanf(ln.c_str(), "fma.rn.f32x2 %%a%d, %%wt, %%wp%d, %%a%d;", &a0, &a1, &a2) == 3) {
+                if (a0 != a2 || !wt_ok || size_t(a1) >= NWIN || a0 >= Mb * NPT) return bad("pair fma");
+                const int m = a0 / NPT, ty = (a0 % NPT) / PX, q = (a0 % NPT) % PX;
+                Op lo{}, hi{};
+                if (!decode(wp_lo[size_t(a1)], ty, q, lo) || !decode(wp_hi[size_t(a1)], ty, q + PX, hi))
+                    return bad("pair operand does not decode to a tap");
+                lo.w = hi.w = uint32_t(wt);
+                seq[(size_t(m) * TY + ty) * TX + q].push_back(lo);
+                seq[(size_t(m) * TY + ty) * TX + q + PX].push_back(hi);
+                continue;
+            }
+            if (std::sscanf(ln.c_str(), "fma.rn.f32 %%f%d, %%w%1[lhs]%d, 0f%08X, %%f%d;", &a0, rn, &a1,
+                            &u0, &a3) == 5) {
+                if (a0 != a3 || size_t(a1) >= NWIN || a0 >= Mb * NST) return bad("scalar fma");
+                const int m = a0 / NST, rest = a0 % NST, w1 = TX - 2 * PX;
+                const int ty = rest / w1, tx = 2 * PX + rest % w1;
+                const int off = (rn[0] == 'l' ? wp_lo : rn[0] == 'h' ? wp_hi : sc_off)[size_t(a1)];
+                Op op{};
+                if (!decode(rn[0] == 's' ? off : off, ty, tx, op))
+                    return bad("scalar operand does not decode to a tap");
+                op.w = u0;
+                seq[(size_t(m) * TY + ty) * TX + tx].push_back(op);
+                continue;
+            }
+        }
+        if (chunk != jp->nchunks - 1) return bad("missing chunks");
+        // compare with the canonical CSR rows, in order, for every pixel of the tile
+        const int64_t plane = int64_t(in.Hp) * in.Wp;
+        for (int m = 0; m < Mb; ++m) {
+            const int k = ks[size_t(m)];
+            const int64_t gbase = int64_t(k / in.Kg) * in.Cg * plane;
+            for (int px = 0; px < TY * TX; ++px) {
+                const auto &sq = seq[size_t(m) * TY * TX + size_t(px)];
+                if (int64_t(sq.size()) != in.rowptr[k + 1] - in.rowptr[k])
+                    return bad("channel " + std::to_string(k) + ": nonzero count differs");
+                for (size_t t = 0; t < sq.size(); ++t) {
+                    const int32_t j = in.rowptr[k] + int32_t(t);
+                    const int64_t off = in.colidx[j] - gbase;
+                    const int cl = int(off / plane), rem = int(off % plane);
+                    if (sq[t].c != cl || sq[t].r != rem / in.Wp || sq[t].s != rem % in.Wp ||
+                        sq[t].w != fbits(in.values[j]))
+                        return bad("channel " + std::to_string(k) + ": code differs from the CSR");
+                }
+            }
+        }
+    }
+    return SKC_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// public (library-internal) interface
+// ---------------------------------------------------------------------------------------
+int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *msg) {
+    *out = nullptr;
+    const int plane = in.Hp * in.Wp;
+    // TMA bulk copies of whole channel runs need 16-byte aligned sources and sizes
+    const bool plane4 = plane % 4 == 0;
+    if (!plane4 && (in.C % 4 || in.Cg % 4)) {
+        *msg = "JIT kernel: plane not a multiple of 4 floats and C % 4 != 0 (TMA alignment)";
+        return SKC_ERR_UNSUPPORTED;
+    }
+    const int cb_unit = plane4 ? 1 : 4;
+    std::unique_ptr<JitPlan> best;
+    std::vector<int> ks;
+    std::vector<std::vector<JNz>> per_c;
+    Need nd;
+    const char *force = std::getenv("SKC_JIT_TILE");  // "TY,TX[,M]" (tuning)
+    int fty = 0, ftx = 0, fm = 0;
+    if (force) std::sscanf(force, "%d,%d,%d", &fty, &ftx, &fm);
+    // warps per CTA (1 CTA per SM): more warps share each fetched instruction of the
+    // straight-line code, fewer registers each (SKC_JIT_NW, tuning)
+    int nw_force = 0;
+    if (const char *e = std::getenv("SKC_JIT_NW")) nw_force = std::max(1, std::min(32, std::atoi(e)));
+    std::vector<int> nw_opts = {8, 12, 16, 20, 24};
+    if (nw_force) nw_opts = {nw_force};
+    for (int nw_max : nw_opts) {
+    const int regs = reg_cap(nw_max);
+    const int reg_budget = regs - 17;
+    const int lanes_max = nw_max * 32;
+    for (int TY = 1; TY <= 6; ++TY)
+        for (int TX = 1; TX <= 16; ++TX) {
+            if (force && (TY != fty || TX != ftx)) continue;
+            const int T = TY * TX;
+            if (TY > in.Ho || TX > in.Wo || T > 32 || T < 2) continue;
+            const int PX = TX / 2;
+            const int wr = window_regs(TY, TX, PX, in.R, in.S, in.stride);
+            int M = (reg_budget - wr - 12) / T;
+            if (fm > 0) M = fm;
+            M = std::min(M, in.Kg);
+            if (M < 1) continue;
+            const int ty_n = (in.Ho + TY - 1) / TY, tx_n = (in.Wo + TX - 1) / TX;
+            const int tpi = ty_n * tx_n;
+            int NI = std::min(max_ni, lanes_max / tpi);
+            if (NI < 1) continue;
+            int CB = 0, NS = 0, IS = 0, stage = 0;
+            size_t smem = 0;
+            for (; NI >= 1; --NI) {
+                CB = kStageTarget / (NI * plane * 4);
+                CB = std::min(in.Cg, CB / cb_unit * cb_unit);
+                if (CB < cb_unit) CB = cb_unit;
+                CB = std::min(CB, in.Cg);
+                const int nch = (in.Cg + CB - 1) / CB;
+                NS = std::min(3, nch);
+                IS = (CB * plane + 3) / 4 * 4;
+                stage = NI * IS * 4;
+                smem = size_t(NS) * stage + 256 + size_t(NI) * 8;
+                if (smem <= size_t(kMaxSmem)) break;
+            }
+            if (NI < 1) continue;
+            const int NW = (NI * tpi + 31) / 32;
+            if (NW > nw_max) continue;
+            const int nbg = (in.Kg + M - 1) / M;
+            double instr = 0;
+            for (int g = 0; g < in.groups; ++g)
+                for (int q = 0; q < nbg; ++q) {
+                    block_channels(in, M, g, q, ks);
+                    block_nz(in, ks, per_c);
+                    instr += block_instr(in, per_c, TY, TX, PX, CB, int(ks.size()), nd);
+                }
+            // time per image (model): the straight-line code is fetched once per CTA item and
+            // shared by its NW warps; fetch-bound below ~20 warps, issue-bound above
+            const double cost = instr / NI * std::max(kFetchInv, NW / kIssue);
+            if (best && cost >= best->cost) continue;
+            std::unique_ptr<JitPlan> jp(new JitPlan());
+            jp->in = in;
+            jp->TY = TY; jp->TX = TX; jp->PX = PX; jp->M = M;
+            jp->NW = NW; jp->NI = NI; jp->CB = CB; jp->NS = NS;
+            jp->nchunks = (in.Cg + CB - 1) / CB;
+            jp->tiles_y = ty_n; jp->tiles_x = tx_n;
+            jp->plane = plane; jp->img_stride = IS; jp->stage_bytes = stage;
+            jp->nbg = nbg; jp->nblocks = nbg * in.groups;
+            jp->cost = cost;
+            best = std::move(jp);
+        }
+    }
+    if (!best) {
+        *msg = "JIT kernel: no tile configuration fits this geometry";
+        return SKC_ERR_UNSUPPORTED;
+    }
+    JitPlan &jp = *best;
+    // image-slot stride: a multiple of 4 floats (TMA), chosen for the fewest bank conflicts
+    const int IS0 = jp.img_stride;
+    int best_extra = -1, best_is = IS0;
+    for (int t = 0; t < 8; ++t) {
+        const int IS = IS0 + 4 * t;
+        const size_t smem = size_t(jp.NS) * jp.NI * IS * 4 + 256 + size_t(jp.NI) * 8;
+        if (smem > size_t(kMaxSmem)) break;
+        const int e = assign_lanes(jp, IS, nullptr);
+        if (e >= 0 && (best_extra < 0 || e < best_extra)) {
+            best_extra = e;
+            best_is = IS;
+        }
+        if (jp.NI == 1 || best_extra == 0) break;
+    }
+    if (best_extra < 0) {
+        *msg = "JIT kernel: lane assignment failed";
+        return SKC_ERR_UNSUPPORTED;
+    }
+    jp.img_stride = best_is;
+    jp.conflict = best_extra;
+    jp.stage_bytes = jp.NI * best_is * 4;
+    assign_lanes(jp, best_is, &jp.lanemap);
+    jp.off_bar = jp.NS * jp.stage_bytes;           // 128-byte aligned: stages are 16 B multiples
+    jp.off_bar = (jp.off_bar + 15) / 16 * 16;
+    jp.off_cnt = jp.off_bar + 8 * kMaxStages;
+    jp.off_info = jp.off_cnt + 4 * kMaxStages;
+    jp.off_info = (jp.off_info + 7) / 8 * 8;
+    jp.smem = size_t(jp.off_info) + size_t(jp.NI) * 8;
+    jp.maxreg = reg_cap(jp.NW);
+    jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
+    for (int g = 0; g < in.groups; ++g)
+        for (int q = 0; q < jp.nbg; ++q) {
+            block_channels(in, jp.M, g, q, ks);
+            for (size_t m = 0; m < ks.size(); ++m)
+                jp.chan[size_t(g * jp.nbg + q) * jp.M + m] = ks[m];
+        }
+    *out = best.release();
+    return SKC_OK;
+}
+
+int jit_compile(JitPlan *jp, std::string *msg) {
+    std::lock_guard<std::mutex> lk(jp->mu);
+    if (jp->compiled) return SKC_OK;
+    const JitInput &in = jp->in;
+    const auto t0 = std::chrono::steady_clock::now();
+    // generate every module (cheap next to compiling), then hash them for the cache key
+    std::vector<std::string> mods(size_t(jp->nblocks) + 1);
+    {
+        std::vector<int> ks;
+        std::vector<std::vector<JNz>> per_c;
+        for (int b = 0; b < jp->nblocks; ++b) {
+            const int g = b / jp->nbg, q = b % jp->nbg;
+            block_channels(in, jp->M, g, q, ks);
+            block_nz(in, ks, per_c);
+            mods[size_t(b)] = emit_block(*jp, b, ks, per_c);
+        }
+        mods.back() = emit_entry(*jp);
+    }
+    const char *opt = std::getenv("SKC_JIT_OPT") ? std::getenv("SKC_JIT_OPT") : "-O1";
+    uint64_t key = fnv1a(&kJitVersion, sizeof kJitVersion);
+    key = fnv1a(opt, std::strlen(opt), key);
+    key = fnv1a(&jp->maxreg, sizeof jp->maxreg, key);
+    for (const auto &m : mods) key = fnv1a(m.data(), m.size(), key);
+    jp->key = key;
+    if (cache_read(key, jp->cubin)) {
+        jp->cache_hit = 1;
+        jp->compiled = true;
+        return SKC_OK;
+    }
+    // compile modules in parallel
+    std::vector<std::vector<char>> objs(mods.size());
+    std::vector<std::string> errs(mods.size());
+    std::atomic<size_t> next{0};
+    std::atomic<bool> bad{false};
+    unsigned nth = std::max(1u, std::thread::hardware_concurrency());
+    if (const char *e = std::getenv("SKC_JIT_THREADS")) nth = unsigned(std::max(1, std::atoi(e)));
+    nth = std::min<unsigned>(nth, unsigned(mods.size()));
+    // biggest modules first
+    std::vector<size_t> order(mods.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(),
+              [&](size_t a, size_t b) { return mods[a].size() > mods[b].size(); });
+    auto work = [&]() {
+        for (;;) {
+            const size_t i = next.fetch_add(1);
+            if (i >= order.size() || bad.load()) return;
+            const size_t m = order[i];
+            if (!compile_ptx(mods[m], opt, jp->maxreg, objs[m], &errs[m])) bad.store(true);
+            std::string().swap(mods[m]);  // free the text early
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work);
+    work();
+    for (auto &t : pool) t.join();
+    for (const auto &e : errs)
+        if (!e.empty()) {
+            *msg = e;
+            return SKC_ERR_UNSUPPORTED;
+        }
+    // link
+    nvJitLinkHandle lh = nullptr;
+    const char *lopts[] = {"-arch=sm_100a"};
+    if (nvJitLinkCreate(&lh, 1, lopts) != NVJITLINK_SUCCESS) {
+        *msg = "nvJitLinkCreate failed";
+        return SKC_ERR_UNSUPPORTED;
+    }
+    nvJitLinkResult lr = NVJITLINK_SUCCESS;
+    for (size_t i = 0; i < objs.size() && lr == NVJITLINK_SUCCESS; ++i) {
+        const std::string name = "m" + std::to_string(i);
+        lr = nvJitLinkAddData(lh, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(),
+                              name.c_str());
+    }
+    if (lr == NVJITLINK_SUCCESS) lr = nvJitLinkComplete(lh);
+    if (lr != NVJITLINK_SUCCESS) {
+        size_t n = 0;
+        nvJitLinkGetErrorLogSize(lh, &n);
+        std::string log(n, '\0');
+        if (n) nvJitLinkGetErrorLog(lh, &log[0]);
+        nvJitLinkDestroy(&lh);
+        *msg = "nvJitLink failed (" + std::to_string(int(lr)) + "): " + log.substr(0, 800);
+        return SKC_ERR_UNSUPPORTED;
+    }
+    size_t n = 0;
+    nvJitLinkGetLinkedCubinSize(lh, &n);
+    jp->cubin.resize(n);
+    nvJitLinkGetLinkedCubin(lh, jp->cubin.data());
+    nvJitLinkDestroy(&lh);
+    cache_write(key, jp->cubin);
+    jp->compiled = true;
+    jp->compile_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return SKC_OK;
+}
+
+size_t jit_lanemap_bytes(const JitPlan *jp) { return jp->lanemap.size() * 4; }
+const void *jit_lanemap(const JitPlan *jp) { return jp->lanemap.data(); }
+
+void jit_info(const JitPlan *jp, JitInfo *o) {
+    o->TY = jp->TY; o->TX = jp->TX; o->PX = jp->PX; o->M = jp->M; o->NW = jp->NW;
+    o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks;
+    o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
+    o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
+    o->compiled = jp->compiled ? 1 : 0;
+}
+
+const std::vector<int32_t> &jit_chan(const JitPlan *jp) { return jp->chan; }
+const std::vector<uint32_t> &jit_lanes(const JitPlan *jp) { return jp->lanemap; }
+
+cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_lanemap, int N,
+                       const Epilogue &epi, cudaStream_t st, std::string *msg) {
+    if (!jp->compiled) {
+        const int r = jit_compile(jp, msg);
+        if (r != SKC_OK) return cudaErrorInvalidPtx;
+    }
+    {
+        std::lock_guard<std::mutex> lk(jp->mu);
+        if (!jp->lib) {
+            cudaError_t e = cudaLibraryLoadData(&jp->lib, jp->cubin.data(), nullptr, nullptr, 0,
+                                                nullptr, nullptr, 0);
+            if (e != cudaSuccess) {
+                *msg = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+                return e;
+            }
+            e = cudaLibraryGetKernel(&jp->kern, jp->lib, "skc_jit_kernel");
+            if (e != cudaSuccess) {
+                *msg = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+                return e;
+            }
+        }
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!(jp->attr_set.load(std::memory_order_acquire) >> dev & 1u)) {
+        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(jp->kern),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(jp->smem));
+        if (e != cudaSuccess) {
+            *msg = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+            return e;
+        }
+        jp->attr_set.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel);
+    }
+    // persistent grid: one CTA per SM slot (the kernel loops over its work items)
+    const int64_t nig = (int64_t(N) + jp->NI - 1) / jp->NI;
+    const int64_t items = nig * jp->nblocks;
+    if (items > 0x7fffffff) return cudaErrorInvalidConfiguration;
+    int nsm = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, reinterpret_cast<const void *>(jp->kern), jp->NW * 32, jp->smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    int cs = 1;
+    if (const char *e = std::getenv("SKC_JIT_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(e)));
+    int64_t grid = std::min<int64_t>(items, int64_t(nsm) * per_sm);
+    if (const char *e = std::getenv("SKC_JIT_GRID")) grid = std::min<int64_t>(items, std::max(1, std::atoi(e)));
+    if (std::getenv("SKC_JIT_DEBUG")) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, reinterpret_cast<const void *>(jp->kern));
+        std::fprintf(stderr, "skc jit: regs %d maxThreads %d local %zu shared %zu NW %d smem %zu per_sm %d\n",
+                     fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes, jp->NW,
+                     jp->smem, per_sm);
+    }
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute at[1];
+    lc.blockDim = dim3(unsigned(jp->NW * 32));
+    lc.dynamicSmemBytes = jp->smem;
+    lc.stream = st;
+    if (cs > 1) {
+        if (cs > 8)
+            cudaFuncSetAttribute(reinterpret_cast<const void *>(jp->kern),
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = unsigned(cs);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        lc.gridDim = dim3(1);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void *>(jp->kern), &lc) != cudaSuccess || ncl < 1)
+            ncl = int(nsm / cs);
+        grid = std::min<int64_t>((items + cs - 1) / cs, ncl) * cs;
+    }
+    lc.gridDim = dim3(unsigned(grid));
+    const float *bias = epi.bias;
+    unsigned un = unsigned(N), relu = unsigned(epi.relu), opad = unsigned(epi.opad);
+    void *args[] = {(void *)&in, (void *)&out, (void *)&d_lanemap, (void *)&bias,
+                    (void *)&un, (void *)&relu, (void *)&opad};
+    return cudaLaunchKernelExC(&lc, reinterpret_cast<const void *>(jp->kern), args);
+}
+
+int jit_verify_code(const JitPlan *jp, std::string *msg) { return jit_verify(jp, msg); }
+
+void jit_destroy(JitPlan *jp) {
+    if (!jp) return;
+    if (jp->lib) cudaLibraryUnload(jp->lib);
+    delete jp;
+}
+
+}  // namespace skc

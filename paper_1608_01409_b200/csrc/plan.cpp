@@ -83,7 +83,15 @@ struct skc_plan {
     size_t off_nz = 0, off_chunkptr = 0, off_perm = 0;
     size_t off_stream = 0, off_segoff = 0, off_chan = 0, off_lanemap = 0;
 
+    // "compiled weights" kernel (kernel == SKC_KERNEL_JIT, jit.cpp)
+    JitPlan *jit = nullptr;
+
     void *d_ws = nullptr;  // set by skc_plan_upload
+
+    skc_plan() = default;
+    skc_plan(const skc_plan &) = delete;
+    skc_plan &operator=(const skc_plan &) = delete;
+    ~skc_plan() { jit_destroy(jit); }
 };
 
 namespace {
@@ -676,7 +684,7 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
                        int pad, int groups, int kernel, int max_ni, skc_plan **out) {
     if (!w || !out) return fail(SKC_ERR_ARG, "NULL weights or output pointer");
     *out = nullptr;
-    if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_REGTILE)
+    if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_JIT)
         return fail(SKC_ERR_ARG, "unknown kernel variant %d", kernel);
     skc_status st = check_geometry(K, C, R, S, H, W, stride, pad, groups);
     if (st != SKC_OK) return st;
@@ -738,8 +746,31 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
         });
     }
 
-    // kernel choice: the register-tiled kernel when an instantiated tile shape fits and the
-    // cost model prefers it; the direct kernel otherwise (any stride, any R x S)
+    // kernel choice: the compiled-weights kernel when a configuration fits (AUTO; disabled
+    // with SKC_NO_JIT=1); else the register-tiled kernel when an instantiated tile shape fits
+    // and the cost model prefers it; the direct kernel otherwise (any stride, any R x S)
+    const char *nojit = std::getenv("SKC_NO_JIT");
+    if (kernel == SKC_KERNEL_JIT || (kernel == SKC_KERNEL_AUTO && !(nojit && nojit[0] == '1'))) {
+        const JitInput ji{K, C, R, S, p->Hp, p->Wp, p->Ho, p->Wo, stride, groups, p->Kg, p->Cg,
+                          p->rowptr.data(), p->colidx.data(), p->perm.data(), p->values.data()};
+        std::string msg;
+        const int r = jit_configure(ji, max_ni == 1 ? 1 : 64, &p->jit, &msg);
+        if (r == SKC_OK) {
+            p->kernel = SKC_KERNEL_JIT;
+            p->image.resize(jit_lanemap_bytes(p->jit));
+            std::memcpy(p->image.data(), jit_lanemap(p->jit), p->image.size());
+            p->off_lanemap = 0;
+            JitInfo ji2{};
+            jit_info(p->jit, &ji2);
+            p->smem = ji2.smem;
+            *out = p;
+            return ok();
+        }
+        if (kernel == SKC_KERNEL_JIT) {
+            delete p;
+            return fail(skc_status(r), "%s", msg.c_str());
+        }
+    }
     RtCandidate best_rt;
     if (kernel != SKC_KERNEL_DIRECT) {
         RegtileShape shapes[32];
@@ -830,6 +861,18 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.tile_h = p->kernel == SKC_KERNEL_REGTILE ? p->rsh.TY : 0;
     i.tile_w = p->kernel == SKC_KERNEL_REGTILE ? p->rsh.TX : 0;
     i.images_per_cta = p->kernel == SKC_KERNEL_REGTILE ? p->rp.NI : p->sg.NI;
+    i.jit_blocks = 0; i.jit_compiled = 0; i.jit_cache_hit = 0; i.jit_compile_s = 0;
+    i.code_bytes = 0; i.model_instr_per_image = 0;
+    if (p->kernel == SKC_KERNEL_JIT) {
+        JitInfo j{};
+        jit_info(p->jit, &j);
+        i.band_rows = 0; i.chunk_channels = j.CB; i.stages = j.NS; i.warps = j.NW;
+        i.channels_per_warp = j.M; i.pixels_per_lane = j.TY * j.TX; i.smem_bytes = j.smem;
+        i.lane_mapping = 0; i.tile_h = j.TY; i.tile_w = j.TX; i.images_per_cta = j.NI;
+        i.jit_blocks = j.nblocks; i.jit_compiled = j.compiled; i.jit_cache_hit = j.cache_hit;
+        i.jit_compile_s = j.compile_s; i.code_bytes = j.cubin_bytes;
+        i.model_instr_per_image = j.cost;
+    }
     return ok();
 }
 
@@ -969,6 +1012,13 @@ skc_status verify_direct(const skc_plan *p) {
     return SKC_OK;
 }
 
+skc_status verify_jit(const skc_plan *p) {
+    std::string msg;
+    const int r = jit_verify_code(p->jit, &msg);
+    if (r != SKC_OK) return fail(skc_status(r), "%s", msg.c_str());
+    return SKC_OK;
+}
+
 skc_status verify_regtile(const skc_plan *p) {
     const RegtileParams &r = p->rp;
     const RegtileShape &sh = p->rsh;
@@ -1062,9 +1112,20 @@ skc_status verify_regtile(const skc_plan *p) {
 
 extern "C" {
 
+skc_status skc_plan_compile(skc_plan *p) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (p->kernel != SKC_KERNEL_JIT) return ok();
+    std::string msg;
+    const int r = jit_compile(p->jit, &msg);
+    if (r != SKC_OK) return fail(skc_status(r), "JIT compile: %s", msg.c_str());
+    return ok();
+}
+
 skc_status skc_plan_verify(const skc_plan *p) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
-    const skc_status st = p->kernel == SKC_KERNEL_REGTILE ? verify_regtile(p) : verify_direct(p);
+    const skc_status st = p->kernel == SKC_KERNEL_JIT       ? verify_jit(p)
+                          : p->kernel == SKC_KERNEL_REGTILE ? verify_regtile(p)
+                                                            : verify_direct(p);
     return st == SKC_OK ? ok() : st;
 }
 
@@ -1074,6 +1135,11 @@ skc_status skc_plan_upload(skc_plan *p, void *d_ws, size_t bytes, void *stream) 
     if (bytes < p->image.size())
         return fail(SKC_ERR_ARG, "workspace has %zu bytes, plan needs %zu", bytes,
                     p->image.size());
+    if (p->kernel == SKC_KERNEL_JIT) {
+        std::string msg;
+        const int r = jit_compile(p->jit, &msg);
+        if (r != SKC_OK) return fail(skc_status(r), "JIT compile: %s", msg.c_str());
+    }
     cudaError_t e = cudaMemcpyAsync(d_ws, p->image.data(), p->image.size(),
                                     cudaMemcpyHostToDevice, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
@@ -1122,6 +1188,14 @@ skc_status skc_sparse_conv_forward_ex(const skc_plan *p, const float *d_in, floa
     if (!aligned16(d_in) || !aligned16(d_out))
         return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
     const uint8_t *ws = static_cast<const uint8_t *>(p->d_ws);
+    if (p->kernel == SKC_KERNEL_JIT) {
+        std::string msg;
+        cudaError_t e = jit_launch(p->jit, d_in, d_out, ws + p->off_lanemap, N, epi,
+                                   (cudaStream_t)stream, &msg);
+        if (e != cudaSuccess)
+            return fail(SKC_ERR_CUDA, "JIT conv launch: %s %s", cudaGetErrorString(e), msg.c_str());
+        return ok();
+    }
     if (p->kernel == SKC_KERNEL_REGTILE) {
         RegtileParams rp = p->rp;
         rp.N = N;

@@ -5,6 +5,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <string>
+#include <vector>
+
 namespace skc {
 
 constexpr int kMaxStages = 8;
@@ -94,6 +97,35 @@ cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_
                            cudaStream_t st);
 // Instantiated register-tile shapes (count returned, shapes written to out[0..max)).
 int regtile_shapes(RegtileShape *out, int max);
+// "Compiled weights" kernel (jit.cpp).  JitInput points into the plan's canonical CSR.
+struct JitInput {
+    int K, C, R, S, Hp, Wp, Ho, Wo, stride, groups, Kg, Cg;
+    const int32_t *rowptr, *colidx, *perm;
+    const float *values;
+};
+struct JitInfo {
+    int TY, TX, PX, M, NW, NI, CB, NS, nblocks;
+    size_t smem, cubin_bytes;
+    double cost;
+    int conflict;
+    double compile_s;
+    int cache_hit, compiled;
+};
+struct JitPlan;
+// Pick the tile / channel-block / staging configuration (host, cheap; no code generated).
+int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *msg);
+// Generate + compile + link the code (host; thread pool; on-disk cache).
+int jit_compile(JitPlan *jp, std::string *msg);
+size_t jit_lanemap_bytes(const JitPlan *jp);
+const void *jit_lanemap(const JitPlan *jp);
+void jit_info(const JitPlan *jp, JitInfo *o);
+const std::vector<int32_t> &jit_chan(const JitPlan *jp);
+cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_lanemap, int N,
+                       const Epilogue &epi, cudaStream_t st, std::string *msg);
+// Static check: tables + the emitted code decoded back to the canonical CSR (host).
+int jit_verify_code(const JitPlan *jp, std::string *msg);
+void jit_destroy(JitPlan *jp);
+
 cudaError_t bench_ffma(void *scratch, int blocks, int iters, float *ms, double *flops);
 cudaError_t bench_lds(void *scratch, int blocks, int iters, float *ms, double *bytes);
 

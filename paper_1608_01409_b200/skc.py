@@ -17,7 +17,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libskc.so")
 
-SKC_KERNEL_AUTO, SKC_KERNEL_DIRECT, SKC_KERNEL_REGTILE = 0, 1, 2
+SKC_KERNEL_AUTO, SKC_KERNEL_DIRECT, SKC_KERNEL_REGTILE, SKC_KERNEL_JIT = 0, 1, 2, 3
 STATUS = {0: "SKC_OK", -1: "SKC_ERR_ARG", -2: "SKC_ERR_GEOMETRY", -3: "SKC_ERR_NONFINITE",
           -4: "SKC_ERR_OVERFLOW", -5: "SKC_ERR_UNSUPPORTED", -6: "SKC_ERR_ALIGN",
           -7: "SKC_ERR_STATE", -8: "SKC_ERR_CUDA"}
@@ -27,7 +27,8 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
-           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc")
+           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc",
+           "skc_plan_compile")
 
 
 class SkcError(RuntimeError):
@@ -45,7 +46,10 @@ class skc_info(ctypes.Structure):
         ("stages", ctypes.c_int), ("warps", ctypes.c_int), ("channels_per_warp", ctypes.c_int),
         ("pixels_per_lane", ctypes.c_int), ("smem_bytes", ctypes.c_size_t),
         ("lane_mapping", ctypes.c_int), ("tile_h", ctypes.c_int), ("tile_w", ctypes.c_int),
-        ("images_per_cta", ctypes.c_int)]
+        ("images_per_cta", ctypes.c_int), ("jit_blocks", ctypes.c_int),
+        ("jit_compiled", ctypes.c_int), ("jit_cache_hit", ctypes.c_int),
+        ("jit_compile_s", ctypes.c_double), ("code_bytes", ctypes.c_size_t),
+        ("model_instr_per_image", ctypes.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -89,6 +93,7 @@ def lib():
             "skc_pack_csr_ex": [_P] + [_I] * 10 + [ctypes.POINTER(_P)],
             "skc_plan_info": [_P, ctypes.POINTER(skc_info)],
             "skc_plan_verify": [_P],
+            "skc_plan_compile": [_P],
             "skc_plan_csr": [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
             "skc_plan_perm": [_P, ctypes.POINTER(_P)],
             "skc_plan_upload": [_P, _P, ctypes.c_size_t, _P],
@@ -212,6 +217,11 @@ def skc_pack_csr(w: np.ndarray, H: int, W: int, stride: int = 1, pad: int = 0, g
 def skc_plan_verify(plan: Plan):
     """Static self-check of the plan's kernel-private data (raises SkcError on a violation)."""
     _check(lib().skc_plan_verify(plan.handle))
+
+
+def skc_plan_compile(plan: Plan):
+    """JIT kernel: generate + compile + link the plan's code now (host only, no GPU)."""
+    _check(lib().skc_plan_compile(plan.handle))
 
 
 def skc_plan_upload(plan: Plan, workspace, stream=None):
