@@ -898,13 +898,16 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     // straight-line code, fewer registers each (SKC_JIT_NW, tuning)
     int nw_force = 0;
     if (const char *e = std::getenv("SKC_JIT_NW")) nw_force = std::max(1, std::min(32, std::atoi(e)));
-    std::vector<int> nw_opts = {8, 12, 16, 20, 24};
+    double code_cap = 3.0e6;  // warp-instructions of all blocks' code (SKC_JIT_MAX_CODE)
+    if (const char *e = std::getenv("SKC_JIT_MAX_CODE")) code_cap = std::atof(e);
+    std::vector<int> nw_opts = {20, 12, 16, 24, 8};  // likely winners first (pruning)
+    const int64_t nnz_total = in.rowptr[in.K];
     if (nw_force) nw_opts = {nw_force};
     for (int nw_max : nw_opts) {
     const int regs = reg_cap(nw_max);
     const int reg_budget = regs - 17;
     const int lanes_max = nw_max * 32;
-    for (int TY = 1; TY <= 6; ++TY)
+    for (int TY = 1; TY <= 4; ++TY)
         for (int TX = 1; TX <= 16; ++TX) {
             if (force && (TY != fty || TX != ftx)) continue;
             const int T = TY * TX;
@@ -937,6 +940,10 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
             const int NW = (NI * tpi + 31) / 32;
             if (NW > nw_max) continue;
             const int nbg = (in.Kg + M - 1) / M;
+            const double share = std::max(kFetchInv, NW / kIssue) / NI;
+            // lower bound (FMA instructions only; independent of the blocking) prunes most
+            // candidates before the exact count
+            if (best && double(nnz_total) * TY * (PX + (TX - 2 * PX)) * share >= best->cost) continue;
             double instr = 0;
             for (int g = 0; g < in.groups; ++g)
                 for (int q = 0; q < nbg; ++q) {
@@ -946,7 +953,8 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                 }
             // time per image (model): the straight-line code is fetched once per CTA item and
             // shared by its NW warps; fetch-bound below ~20 warps, issue-bound above
-            const double cost = instr / NI * std::max(kFetchInv, NW / kIssue);
+            if (instr > code_cap) continue;  // code size: compile time and I-fetch footprint
+            const double cost = instr * share;
             if (best && cost >= best->cost) continue;
             std::unique_ptr<JitPlan> jp(new JitPlan());
             jp->in = in;

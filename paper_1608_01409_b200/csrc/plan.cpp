@@ -750,7 +750,10 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
     // with SKC_NO_JIT=1); else the register-tiled kernel when an instantiated tile shape fits
     // and the cost model prefers it; the direct kernel otherwise (any stride, any R x S)
     const char *nojit = std::getenv("SKC_NO_JIT");
-    if (kernel == SKC_KERNEL_JIT || (kernel == SKC_KERNEL_AUTO && !(nojit && nojit[0] == '1'))) {
+    // (AUTO keeps single-image FC plans -- max_ni == 1 -- on the data-driven kernels: their
+    // code would be millions of instructions for ~one CTA item per block)
+    if (kernel == SKC_KERNEL_JIT ||
+        (kernel == SKC_KERNEL_AUTO && max_ni > 1 && !(nojit && nojit[0] == '1'))) {
         const JitInput ji{K, C, R, S, p->Hp, p->Wp, p->Ho, p->Wo, stride, groups, p->Kg, p->Cg,
                           p->rowptr.data(), p->colidx.data(), p->perm.data(), p->values.data()};
         std::string msg;

@@ -119,13 +119,22 @@ def test_errors(L):
 
 
 def test_plan_info_configuration(L):
-    """The direct kernel's tiling for the AlexNet layers: full-image slabs staged with TMA."""
+    """Kernel configurations for the AlexNet layers: the direct kernel's tiling covers every
+    output pixel with full-image slabs; AUTO picks the compiled-weights (JIT) kernel, whose
+    lanes x images cover the CTA's images and whose staging fits shared memory."""
     for li, layer in enumerate(wl.ALEXNET):
         w = wl.gen_weights(2, li, layer)
-        info = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups).info()
-        assert info["kernel"] in (skc.SKC_KERNEL_DIRECT, skc.SKC_KERNEL_REGTILE)
+        info = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                skc.SKC_KERNEL_DIRECT).info()
+        assert info["kernel"] == skc.SKC_KERNEL_DIRECT
         assert info["smem_bytes"] <= 227 * 1024
         assert info["pixels_per_lane"] * 32 * -(-layer.Ho // info["band_rows"]) >= layer.Ho * layer.Wo
+        info = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups).info()
+        assert info["kernel"] == skc.SKC_KERNEL_JIT
+        assert info["smem_bytes"] <= 227 * 1024
+        tiles = -(-layer.Ho // info["tile_h"]) * -(-layer.Wo // info["tile_w"])
+        assert tiles * info["images_per_cta"] <= info["warps"] * 32
+        assert info["jit_blocks"] * info["channels_per_warp"] >= layer.K
 
 
 @pytest.mark.parametrize("li", range(4))

@@ -272,7 +272,8 @@ def check_epi(out, ref, bound, bias, relu, what=""):
     assert worst <= TOL, f"{what}: max err/scale {worst:.3e}"
 
 
-@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_DIRECT, skc.SKC_KERNEL_REGTILE])
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_DIRECT, skc.SKC_KERNEL_REGTILE,
+                                    skc.SKC_KERNEL_JIT])
 def test_fused_epilogue(kernel):
     """f1: conv + bias + ReLU written into the interior of an out_pad-wide halo; the halo is
     never touched (pre-filled sentinel survives)."""
@@ -422,3 +423,68 @@ def test_batch_split_invariance(kernel):
                 parts.append(conv.forward(xs).cpu().numpy())
             np.testing.assert_array_equal(np.concatenate(parts).view(np.uint32),
                                           full.view(np.uint32))
+
+
+def run_jit_and_direct(w, x, layer):
+    """Both kernels on the same padded input; returns (jit_out, direct_out, jit_conv)."""
+    jit = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                      skc.SKC_KERNEL_JIT)
+    skc.skc_plan_verify(jit.plan)
+    direct = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                         layer.groups, skc.SKC_KERNEL_DIRECT)
+    N = x.shape[0]
+    xp = torch.empty(jit.padded_shape(N), device="cuda")
+    skc.skc_pad_input(jit.plan, torch.from_numpy(x).cuda(), xp, N)
+    yj = torch.full(jit.out_shape(N), float("nan"), device="cuda")
+    jit.forward_padded(xp, yj)
+    yd = direct.forward_padded(xp)
+    torch.cuda.synchronize()
+    return yj.cpu().numpy(), yd.cpu().numpy(), jit
+
+
+def test_jit_random_geometries():
+    """The compiled-weights kernel forced on random layers (1x1..5x5, stride 1/2, groups,
+    ragged K and C/g, batches not a multiple of the images per CTA, empty channels, tiles
+    overhanging the output): within tolerance of the fp64 oracle and BITWISE equal to the
+    direct kernel (same fp32 FMA sequence per output element, CSR order)."""
+    rng = np.random.default_rng(21)
+    n_jit = 0
+    for it in range(150):
+        if it % 2:
+            layer = wl.random_layer(rng, max_c=32, max_hw=20, rs=(1, 2, 3, 5), groups=(1, 2, 4))
+        else:
+            R = int(rng.choice([1, 3, 5]))
+            g = int(rng.choice([1, 2]))
+            C = g * 4 * int(rng.integers(1, 9))
+            K = g * int(rng.integers(1, 48))
+            H, W = int(rng.integers(R, 32)), int(rng.integers(R, 32))
+            layer = wl.Layer("j", K, C, H, W, R, R, int(rng.choice([1, 2])), (R - 1) // 2, g,
+                             float(rng.choice([0.0, 0.5, 0.9, 0.98])), 1.0)
+        N = int(rng.integers(1, 24))
+        w, x = wl.random_tensors(rng, layer, N)
+        if it % 5 == 0:
+            w[rng.integers(0, layer.K)] = 0.0
+        try:
+            yj, yd, conv = run_jit_and_direct(w, x, layer)
+        except skc.SkcError as e:
+            assert e.status == -5, e  # unsupported staging alignment only
+            continue
+        n_jit += 1
+        np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32),
+                                      err_msg=f"it{it} {layer} {conv.geom}")
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        check(yj, ref, bound, f"jit it{it} {layer}")
+    assert n_jit >= 100, n_jit
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_jit_bitwise_equals_direct_full_batch(cfg_id):
+    """Full batch (256) of every config-2 / config-4 layer: JIT output == direct output bit
+    for bit (the direct kernel is checked against the oracle in test_config_parity)."""
+    cfg = wl.CONFIGS[cfg_id]
+    for li, L in enumerate(cfg.layers):
+        w = wl.gen_weights(cfg_id, li, L)
+        x = wl.gen_input(cfg_id, li, L, 0, cfg.batch)
+        yj, yd, conv = run_jit_and_direct(w, x, L)
+        assert conv.geom["kernel"] == skc.SKC_KERNEL_JIT
+        np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32), err_msg=L.name)
