@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "regtile"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "regtile", "jit"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -232,12 +232,14 @@ def run_ours(args, cfg, rank, world, local_rank):
     per_gpu = args.batch or cfg.batch
     n0, n1 = skd.shard_range(per_gpu * world, world, rank)  # weak scaling: per_gpu images each
     kernel = {"auto": skc.SKC_KERNEL_AUTO, "direct": skc.SKC_KERNEL_DIRECT,
-              "regtile": skc.SKC_KERNEL_REGTILE}[args.kernel]
+              "regtile": skc.SKC_KERNEL_REGTILE, "jit": skc.SKC_KERNEL_JIT}[args.kernel]
     stream = torch.cuda.current_stream(dev)
 
     layers = []
+    t_build = time.time()
     for li, L in enumerate(cfg.layers):
         w = wl.gen_weights(cfg.cfg_id, li, L)
+        # plan build (pack + JIT compile + upload): one-off, untimed
         conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kernel, dev)
         x_host = torch.from_numpy(wl.gen_input(cfg.cfg_id, li, L, n0, n1))
         x = x_host.to(dev)
@@ -248,6 +250,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         if world > 1 and not skd.check_same_plan(conv.plan, dev):
             raise SystemExit(f"bench.py: rank {rank} packed a different plan for {L.name}")
 
+    t_build = time.time() - t_build
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step(evs=None):
@@ -388,9 +391,10 @@ def run_ours(args, cfg, rank, world, local_rank):
             "conv_ms": float(cm), "pad_ms": float(pm),
             "conv_nnz_tflops": nnz_flops(L, d["nnz"], per_gpu) / (cm * 1e-3) / 1e12,
             "pad_gbs": per_gpu * 4 * (L.C * L.H * L.W + L.C * (L.H + 2 * L.pad) * (L.W + 2 * L.pad)) / (pm * 1e-3) / 1e9,
-            "kernel_cfg": {k: d["conv"].geom[k] for k in ("kernel", "band_rows", "chunk_channels",
-                                                            "stages", "warps", "channels_per_warp",
-                                                            "pixels_per_lane", "smem_bytes")},
+            "kernel_cfg": {k: d["conv"].plan.info()[k] for k in (
+                "kernel", "band_rows", "chunk_channels", "stages", "warps", "channels_per_warp",
+                "pixels_per_lane", "smem_bytes", "tile_h", "tile_w", "images_per_cta",
+                "jit_blocks", "code_bytes", "jit_compile_s", "jit_cache_hit")},
         })
     cpu = None
     if not args.no_cpu and world >= 1:
@@ -423,6 +427,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": e2e,
         "clocks": clocks,
         "gpu_launches": 2 * len(layers) * args.steps,
+        "plan_build_s": t_build,
     }
     print(json.dumps(line), flush=True)
 
