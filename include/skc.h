@@ -66,6 +66,15 @@ typedef enum {
                                 FFMA2), compiled at plan time, see skc_plan_compile      */
 } skc_kernel;
 
+/* Padded-input layouts (the method only needs a layout function f with
+ * f(c, y+r, x+s) = f(c, y, x) + f(0, r, s); the CSR colidx always encodes the canonical f).
+ *   SKC_LAYOUT_NCHW   [N][C][Hp][Wp]                          (direct / regtile kernels)
+ *   SKC_LAYOUT_PAIRS  [ceil(N/2)][C][Hp][Wp][2]: images 2p and 2p+1 interleaved element by
+ *                     element, so one aligned 8-byte load feeds a packed FFMA2 over both
+ *                     images (JIT kernel); an odd batch's last pair has a zero second image.
+ * skc_info.layout says which one a plan reads; skc_pad_input writes it. */
+typedef enum { SKC_LAYOUT_NCHW = 0, SKC_LAYOUT_PAIRS = 1 } skc_layout;
+
 typedef struct {
     int K, C, R, S, H, W, stride, pad, groups;
     int Ho, Wo, Hp, Wp;
@@ -86,6 +95,7 @@ typedef struct {
     double jit_compile_s;          /* wall seconds of generate + compile + link           */
     size_t code_bytes;             /* linked device code (cubin) bytes                    */
     double model_instr_per_image;  /* modelled warp-instructions per image (JIT config)   */
+    int layout;                    /* skc_layout of the padded input this plan reads      */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).
@@ -130,14 +140,15 @@ skc_status skc_plan_perm(const skc_plan *plan, const int32_t **perm);
 skc_status skc_plan_upload(skc_plan *plan, void *d_workspace, size_t bytes, void *stream);
 
 /* a2 -- padded-input layout (R1): d_in [N][C][H][W] ->
- * d_in_padded [N][C][Hp][Wp], zeros in the pad-wide border, interior copied bit-exactly.
- * Both device pointers, caller-owned, must not overlap.  N = 0 is a no-op; N < 0 is
- * SKC_ERR_ARG. */
+ * d_in_padded in the plan's layout (skc_info.layout): [N][C][Hp][Wp], or for
+ * SKC_LAYOUT_PAIRS [ceil(N/2)][C][Hp][Wp][2]; zeros in the pad-wide border, interior copied
+ * bit-exactly.  Both device pointers, caller-owned, must not overlap.  N = 0 is a no-op;
+ * N < 0 is SKC_ERR_ARG. */
 skc_status skc_pad_input(const skc_plan *plan, const float *d_in_nchw, float *d_in_padded,
                          int N, void *stream);
 
 /* a3..a6 -- the sparse conv (PAPER.md:198-208 Fig. 2; :303-316).  d_in_padded as written by
- * skc_pad_input (or any buffer in that layout, zero border required), d_out [N][K][Ho][Wo]
+ * skc_pad_input (or any buffer in the plan's layout, zero border required), d_out [N][K][Ho][Wo]
  * (fully overwritten, no accumulation into it).  Requires skc_plan_upload first
  * (else SKC_ERR_STATE).  Deterministic: each output element is accumulated by one thread in
  * a fixed order, so repeated calls are bitwise identical. */
@@ -167,12 +178,24 @@ skc_status skc_sparse_conv_forward_ex(const skc_plan *plan, const float *d_in_pa
                                       float *d_out, int N, const float *d_bias, int relu,
                                       int out_pad, void *stream);
 
+/* Row f1 for chains: the same fused epilogue, written straight into the padded input buffer
+ * of the NEXT layer's plan `next` (its pad and its layout, skc_info.layout), so the next
+ * layer needs no skc_pad_input pass:
+ *     d_next_in[n][k][y + pad'][x + pad'] (in next's layout) = act(conv(n, k, y, x) + bias[k])
+ * Requires next's C == this K, next's H x W == this Ho x Wo (else SKC_ERR_GEOMETRY).  Only the
+ * interior is written; the caller zero-fills the halo once.  Otherwise as
+ * skc_sparse_conv_forward_ex. */
+skc_status skc_sparse_conv_forward_into(const skc_plan *plan, const float *d_in_padded,
+                                        const skc_plan *next, float *d_next_in, int N,
+                                        const float *d_bias, int relu, void *stream);
+
 /* End-to-end entry with HOST buffers (the host-buffer measurement): h_in [N][C][H][W] ->
  * h_out [N][K][Ho][Wo] (host memory; pinned for asynchronous overlap).  The batch is cut
  * into image chunks; the H2D copy of a chunk, pad + conv of the previous one (on `stream`)
  * and the D2H copy of the one before run concurrently on two internal copy streams.  The
  * call returns after enqueueing; `stream` completes after the last D2H copy.  Caller-owned
- * device scratch for the whole batch: d_in [N][C][H][W], d_in_padded, d_out.  Requires
+ * device scratch for the whole batch: d_in [N][C][H][W], d_in_padded (in the plan's layout),
+ * d_out.  Requires
  * skc_plan_upload.  Errors: as skc_pad_input / skc_sparse_conv_forward, SKC_ERR_CUDA for
  * stream/copy failures. */
 skc_status skc_forward_host(const skc_plan *plan, const float *h_in, float *h_out, int N,

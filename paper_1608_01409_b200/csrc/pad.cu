@@ -85,6 +85,61 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ i
     }
 }
 
+// Image-pair interleaved variant (the padded layout of JIT plans; a layout function in the
+// sense of PAPER.md:289-292 -- f(n, c, y, x) = (((n/2)*C + c)*Hp + y)*Wp + x)*2 + n%2 keeps
+// f(c, y+r, x+s) = f(c, y, x) + f(0, r, s) per image): out[p][c][y][x][j] = in[2p+j][c][y-pad]
+// [x-pad], zero in the halo and for a missing second image.  grid.y = pair; each thread
+// writes two consecutive (A, B) elements as one float4.
+__global__ void __launch_bounds__(256) pad_pairs_kernel(const float *__restrict__ in,
+                                                        float *__restrict__ out, int C, int H,
+                                                        int W, int pad, int Wp, uint32_t per_img,
+                                                        FastDiv div_plane, FastDiv div_wp,
+                                                        int has_b) {
+    const int64_t p = blockIdx.y;
+    const int64_t img = int64_t(C) * H * W;
+    const float *srcA = in + 2 * p * img;
+    const float *srcB = srcA + img;
+    const bool hb = has_b || p + 1 < gridDim.y;
+    float *dst = out + p * int64_t(per_img) * 2;
+    const uint32_t span = blockDim.x * 2;
+    const uint32_t stride = gridDim.x * span * kPadUnroll;
+    for (uint32_t base = blockIdx.x * span * kPadUnroll + threadIdx.x * 2; base < per_img;
+         base += stride) {
+        float v[kPadUnroll][4];
+#pragma unroll
+        for (int u = 0; u < kPadUnroll; ++u) {
+            const uint32_t i0 = base + u * span;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t i = i0 + k;
+                v[u][2 * k] = v[u][2 * k + 1] = 0.0f;
+                if (i < per_img) {
+                    const uint32_t plane = fdiv(i, div_plane);
+                    const uint32_t rem = i - plane * div_plane.d;
+                    const uint32_t yy = fdiv(rem, div_wp);
+                    const int y = int(yy) - pad;
+                    const int x = int(rem - yy * uint32_t(Wp)) - pad;
+                    if (y >= 0 && y < H && x >= 0 && x < W) {
+                        const int64_t o = (int64_t(plane) * H + y) * W + x;
+                        v[u][2 * k] = __ldg(srcA + o);
+                        if (hb) v[u][2 * k + 1] = __ldg(srcB + o);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPadUnroll; ++u) {
+            const uint32_t i0 = base + u * span;
+            if (i0 + 1 < per_img) {
+                *reinterpret_cast<float4 *>(dst + 2 * size_t(i0)) =
+                    make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+            } else if (i0 < per_img) {
+                *reinterpret_cast<float2 *>(dst + 2 * size_t(i0)) = make_float2(v[u][0], v[u][1]);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
@@ -119,6 +174,28 @@ cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int
                                              out + n0 * int64_t(per_img), C, H, W, pad, Wp,
                                              per_img, make_fastdiv(uint32_t(Hp * Wp)),
                                              make_fastdiv(uint32_t(Wp)), per_img % 4 == 0);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int H, int W,
+                             int pad, cudaStream_t st) {
+    const int Hp = H + 2 * pad, Wp = W + 2 * pad;
+    const uint32_t per_img = uint32_t(int64_t(C) * Hp * Wp);
+    const int threads = 256;
+    int64_t bx = (int64_t(per_img) + threads * 8 - 1) / (threads * 8);
+    bx = bx > 4096 ? 4096 : bx;
+    const int64_t P = (N + 1) / 2;
+    for (int64_t p0 = 0; p0 < P; p0 += 65535) {
+        const int64_t np = (P - p0) < 65535 ? (P - p0) : 65535;
+        // the last pair of an odd batch has no second image (has_b = 0 for that launch's
+        // last pair: the kernel checks p + 1 < gridDim.y)
+        const int has_b = (p0 + np < P) || (N % 2 == 0);
+        const dim3 grid{static_cast<unsigned>(bx), static_cast<unsigned>(np), 1u};
+        pad_pairs_kernel<<<grid, threads, 0, st>>>(in + 2 * p0 * int64_t(C) * H * W,
+                                                   out + 2 * p0 * int64_t(per_img), C, H, W, pad,
+                                                   Wp, per_img, make_fastdiv(uint32_t(Hp * Wp)),
+                                                   make_fastdiv(uint32_t(Wp)), has_b);
     }
     return cudaGetLastError();
 }

@@ -85,6 +85,9 @@ struct skc_plan {
 
     // "compiled weights" kernel (kernel == SKC_KERNEL_JIT, jit.cpp)
     JitPlan *jit = nullptr;
+    // padded-input layout the plan's kernel reads (skc_pad_input writes it):
+    // SKC_LAYOUT_NCHW [N][C][Hp][Wp] or SKC_LAYOUT_PAIRS [ceil(N/2)][C][Hp][Wp][2]
+    int layout = SKC_LAYOUT_NCHW;
 
     void *d_ws = nullptr;  // set by skc_plan_upload
 
@@ -766,6 +769,7 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
             JitInfo ji2{};
             jit_info(p->jit, &ji2);
             p->smem = ji2.smem;
+            p->layout = ji2.pair ? SKC_LAYOUT_PAIRS : SKC_LAYOUT_NCHW;
             *out = p;
             return ok();
         }
@@ -866,6 +870,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.images_per_cta = p->kernel == SKC_KERNEL_REGTILE ? p->rp.NI : p->sg.NI;
     i.jit_blocks = 0; i.jit_compiled = 0; i.jit_cache_hit = 0; i.jit_compile_s = 0;
     i.code_bytes = 0; i.model_instr_per_image = 0;
+    i.layout = p->layout;
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -1158,7 +1163,9 @@ skc_status skc_pad_input(const skc_plan *p, const float *d_in, float *d_pad, int
     if (!d_in || !d_pad) return fail(SKC_ERR_ARG, "NULL device pointer");
     if (!aligned16(d_in) || !aligned16(d_pad))
         return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
-    cudaError_t e = launch_pad(d_in, d_pad, N, p->C, p->H, p->W, p->pad, (cudaStream_t)stream);
+    cudaError_t e = p->layout == SKC_LAYOUT_PAIRS
+                        ? launch_pad_pairs(d_in, d_pad, N, p->C, p->H, p->W, p->pad, (cudaStream_t)stream)
+                        : launch_pad(d_in, d_pad, N, p->C, p->H, p->W, p->pad, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "pad launch: %s", cudaGetErrorString(e));
     return ok();
 }
@@ -1177,13 +1184,31 @@ skc_status skc_im2col(const skc_plan *p, const float *d_in, float *d_lowered, in
     return ok();
 }
 
+static skc_status forward_epi(const skc_plan *p, const float *d_in, float *d_out, int N,
+                              const float *d_bias, int relu, int out_pad, int olay, void *stream);
+
 skc_status skc_sparse_conv_forward_ex(const skc_plan *p, const float *d_in, float *d_out,
                                       int N, const float *d_bias, int relu, int out_pad,
                                       void *stream) {
+    return forward_epi(p, d_in, d_out, N, d_bias, relu, out_pad, SKC_LAYOUT_NCHW, stream);
+}
+
+skc_status skc_sparse_conv_forward_into(const skc_plan *p, const float *d_in,
+                                        const skc_plan *next, float *d_next_in, int N,
+                                        const float *d_bias, int relu, void *stream) {
+    if (!p || !next) return fail(SKC_ERR_ARG, "NULL plan");
+    if (next->C != p->K || next->H != p->Ho || next->W != p->Wo)
+        return fail(SKC_ERR_GEOMETRY, "next plan expects C=%d H=%d W=%d, this layer gives %d x %d x %d",
+                    next->C, next->H, next->W, p->K, p->Ho, p->Wo);
+    return forward_epi(p, d_in, d_next_in, N, d_bias, relu, next->pad, next->layout, stream);
+}
+
+static skc_status forward_epi(const skc_plan *p, const float *d_in, float *d_out, int N,
+                              const float *d_bias, int relu, int out_pad, int olay, void *stream) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
     if (out_pad < 0 || out_pad > 64) return fail(SKC_ERR_ARG, "out_pad = %d outside [0, 64]", out_pad);
     if (relu != 0 && relu != 1) return fail(SKC_ERR_ARG, "relu must be 0 or 1");
-    const Epilogue epi{d_bias, relu, out_pad};
+    const Epilogue epi{d_bias, relu, out_pad, olay};
     if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
     if (!p->d_ws) return fail(SKC_ERR_STATE, "plan not uploaded (call skc_plan_upload)");
     if (N == 0) return ok();
@@ -1250,7 +1275,8 @@ skc_status skc_forward_host(const skc_plan *p, const float *h_in, float *h_out, 
     const size_t out_img = size_t(p->K) * p->Ho * p->Wo;
     // chunks: a few per call, whole images, >= 8 images each
     int nchunk = std::max(1, std::min(8, N / 8));
-    const int per = (N + nchunk - 1) / nchunk;
+    int per = (N + nchunk - 1) / nchunk;
+    if (p->layout == SKC_LAYOUT_PAIRS) per += per & 1;  // chunks start on an image pair
     nchunk = (N + per - 1) / per;
     cudaStream_t s_in = nullptr, s_out = nullptr;
     std::vector<cudaEvent_t> ev(size_t(2 * nchunk + 2), nullptr);

@@ -80,4 +80,13 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
     return (__umulhi(n, f.m) + n) >> f.s;
 }
 
+// Output element index of (image n, channel k, padded row yy, padded column xx) in the
+// epilogue's output layout: olay 0 = [N][K][Hop][Wop]; olay 1 = image-pair interleaved
+// [ceil(N/2)][K][Hop][Wop][2] (the padded input layout of a JIT plan, for chaining).
+__device__ __forceinline__ int64_t out_index(int64_t n, int k, int yy, int xx, int K, int Hop,
+                                             int Wop, int olay) {
+    if (!olay) return ((n * K + k) * Hop + yy) * int64_t(Wop) + xx;
+    return ((((n >> 1) * K + k) * Hop + yy) * int64_t(Wop) + xx) * 2 + (n & 1);
+}
+
 }  // namespace skc

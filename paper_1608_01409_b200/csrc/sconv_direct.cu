@@ -184,8 +184,7 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
         const int k = __ldg(p.chan + int64_t(gb) * nslot + m * NW + warp);
         if (k < 0) continue;
         const float bias = p.epi.bias ? __ldg(p.epi.bias + k) : 0.0f;
-        float *o = p.out + (int64_t(n0) * p.K + k) * Hop * Wop +
-                   int64_t(band * p.BH + opad) * Wop + opad;
+        const int yb = band * p.BH + opad;
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             const int code = __ldg(so + t * 32);
@@ -194,7 +193,8 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
             if (p.epi.relu) v = fmaxf(v, 0.0f);
             const int img = code >> 24;
             if (code >= 0 && img < nimg)
-                o[int64_t(img) * p.K * Hop * Wop + ((code >> 12) & 0xfff) * Wop + (code & 0xfff)] = v;
+                p.out[out_index(n0 + img, k, yb + ((code >> 12) & 0xfff), opad + (code & 0xfff),
+                                p.K, Hop, Wop, p.epi.olay)] = v;
         }
     }
 }

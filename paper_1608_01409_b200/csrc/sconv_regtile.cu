@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
         const int k = __ldg(ch + m);
         if (k < 0) continue;
         const float bias = p.epi.bias ? __ldg(p.epi.bias + k) : 0.0f;
-        float *o = p.out + (int64_t(n0 + img) * p.K + k) * Hop * Wop + int64_t(opad) * Wop + opad;
 #pragma unroll
         for (int ty = 0; ty < TY; ++ty)
 #pragma unroll
@@ -142,7 +141,8 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
                 const int y = y0 + ty, x = x0 + tx;
                 float v = acc[m][ty][tx] + bias;
                 if (p.epi.relu) v = fmaxf(v, 0.0f);
-                if (y < p.Ho && x < p.Wo) o[y * Wop + x] = v;
+                if (y < p.Ho && x < p.Wo)
+                    p.out[out_index(n0 + img, k, y + opad, x + opad, p.K, Hop, Wop, p.epi.olay)] = v;
             }
     }
 }

@@ -27,6 +27,8 @@ struct Epilogue {
     const float *bias;  // [K] or nullptr
     int relu;           // 1: max(., 0)
     int opad;           // output halo width (0: plain NCHW output)
+    int olay;           // output layout: 0 [N][K][..][..]; 1 image-pair interleaved
+                        // [ceil(N/2)][K][..][..][2] (the padded layout of JIT plans)
 };
 
 // Direct kernel (sconv_direct.cu).  CTA = (group of NI images, output-row band, block of
@@ -89,6 +91,10 @@ struct RegtileShape {
 // Launchers (defined in the .cu files).  Return cudaError_t of the launch.
 cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int W, int pad,
                        cudaStream_t st);
+// NCHW -> image-pair interleaved padded layout [ceil(N/2)][C][Hp][Wp][2] (zero halo; the
+// second image of an odd batch's last pair is zero).
+cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int H, int W,
+                             int pad, cudaStream_t st);
 cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
                           int S, int stride, int pad, int Ho, int Wo, cudaStream_t st);
 cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st);
@@ -110,6 +116,7 @@ struct JitInfo {
     int conflict;
     double compile_s;
     int cache_hit, compiled;
+    int pair;  // 1: the plan reads the image-pair interleaved padded layout
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).

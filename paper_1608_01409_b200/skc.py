@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libskc.so")
 
 SKC_KERNEL_AUTO, SKC_KERNEL_DIRECT, SKC_KERNEL_REGTILE, SKC_KERNEL_JIT = 0, 1, 2, 3
+SKC_LAYOUT_NCHW, SKC_LAYOUT_PAIRS = 0, 1
 STATUS = {0: "SKC_OK", -1: "SKC_ERR_ARG", -2: "SKC_ERR_GEOMETRY", -3: "SKC_ERR_NONFINITE",
           -4: "SKC_ERR_OVERFLOW", -5: "SKC_ERR_UNSUPPORTED", -6: "SKC_ERR_ALIGN",
           -7: "SKC_ERR_STATE", -8: "SKC_ERR_CUDA"}
@@ -28,7 +29,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
            "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc",
-           "skc_plan_compile")
+           "skc_plan_compile", "skc_sparse_conv_forward_into")
 
 
 class SkcError(RuntimeError):
@@ -49,7 +50,7 @@ class skc_info(ctypes.Structure):
         ("images_per_cta", ctypes.c_int), ("jit_blocks", ctypes.c_int),
         ("jit_compiled", ctypes.c_int), ("jit_cache_hit", ctypes.c_int),
         ("jit_compile_s", ctypes.c_double), ("code_bytes", ctypes.c_size_t),
-        ("model_instr_per_image", ctypes.c_double)]
+        ("model_instr_per_image", ctypes.c_double), ("layout", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -100,6 +101,7 @@ def lib():
             "skc_pad_input": [_P, _P, _P, _I, _P],
             "skc_sparse_conv_forward": [_P, _P, _P, _I, _P],
             "skc_sparse_conv_forward_ex": [_P, _P, _P, _I, _P, _I, _I, _P],
+            "skc_sparse_conv_forward_into": [_P, _P, _P, _P, _I, _P, _I, _P],
             "skc_im2col": [_P, _P, _P, _I, _P],
             "skc_pack_fc": [_P, _I, _I, _I, _I, ctypes.POINTER(_P)],
             "skc_forward_host": [_P, _P, _P, _I, _P, _P, _P, _P],
@@ -247,6 +249,29 @@ def skc_sparse_conv_forward_ex(plan: Plan, d_in_padded, d_out, N: int, d_bias=No
                                             int(bool(relu)), int(out_pad), _stream(stream)))
 
 
+def skc_sparse_conv_forward_into(plan: Plan, d_in_padded, next_plan: Plan, d_next_in, N: int,
+                                 d_bias=None, relu: bool = False, stream=None):
+    """f1 chain: conv + bias + ReLU written into the next plan's padded input (its layout)."""
+    _check(lib().skc_sparse_conv_forward_into(plan.handle, _dptr(d_in_padded), next_plan.handle,
+                                              _dptr(d_next_in), int(N),
+                                              _dptr(d_bias) if d_bias is not None else None,
+                                              int(bool(relu)), _stream(stream)))
+
+
+def padded_shape(info: dict, N: int) -> tuple:
+    """Shape of the padded-input buffer of N images in the plan's layout (skc_info.layout)."""
+    if info["layout"] == SKC_LAYOUT_PAIRS:
+        return ((N + 1) // 2, info["C"], info["Hp"], info["Wp"], 2)
+    return (N, info["C"], info["Hp"], info["Wp"])
+
+
+def unpad_view(info: dict, xp, N: int):
+    """NCHW-padded view [N][C][Hp][Wp] (a copy for the pair layout) of a padded buffer."""
+    if info["layout"] == SKC_LAYOUT_PAIRS:
+        return xp.movedim(-1, 1).reshape(-1, *xp.shape[1:4])[:N]
+    return xp
+
+
 def skc_im2col(plan: Plan, d_in, d_lowered, N: int, stream=None):
     """f3: lowered (im2col) tensor [N][C*R*S][Ho][Wo] of an NCHW input (CUDA kernel)."""
     _check(lib().skc_im2col(plan.handle, _dptr(d_in), _dptr(d_lowered), int(N), _stream(stream)))
@@ -370,12 +395,18 @@ class SparseConv2d:
         return (N, g["K"], g["Ho"], g["Wo"])
 
     def padded_shape(self, N):
-        g = self.geom
-        return (N, g["C"], g["Hp"], g["Wp"])
+        """Padded-input buffer shape in the plan's layout (NCHW, or image pairs)."""
+        return padded_shape(self.geom, N)
 
-    def forward_padded(self, xp, out=None, stream=None):
+    def forward_padded(self, xp, out=None, stream=None, N=None):
+        """Conv of a padded input in the plan's layout.  N defaults to out's batch, else to
+        the padded buffer's images (2 per leading index in the image-pair layout)."""
         import torch
-        N = xp.shape[0]
+        if N is None:
+            if out is not None:
+                N = out.shape[0]
+            else:
+                N = xp.shape[0] * (2 if self.geom["layout"] == SKC_LAYOUT_PAIRS else 1)
         if out is None:
             out = torch.empty(self.out_shape(N), dtype=torch.float32, device=xp.device)
         skc_sparse_conv_forward(self.plan, xp, out, N, stream)
@@ -387,4 +418,4 @@ class SparseConv2d:
         if xp is None:
             xp = torch.empty(self.padded_shape(N), dtype=torch.float32, device=x.device)
         skc_pad_input(self.plan, x, xp, N, stream)
-        return self.forward_padded(xp, out, stream)
+        return self.forward_padded(xp, out, stream, N)

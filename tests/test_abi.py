@@ -133,7 +133,8 @@ def test_plan_info_configuration(L):
         assert info["kernel"] == skc.SKC_KERNEL_JIT
         assert info["smem_bytes"] <= 227 * 1024
         tiles = -(-layer.Ho // info["tile_h"]) * -(-layer.Wo // info["tile_w"])
-        assert tiles * info["images_per_cta"] <= info["warps"] * 32
+        per_lane = 2 if info["layout"] == skc.SKC_LAYOUT_PAIRS else 1  # images per lane tile
+        assert tiles * info["images_per_cta"] <= info["warps"] * 32 * per_lane
         assert info["jit_blocks"] * info["channels_per_warp"] >= layer.K
 
 

@@ -50,22 +50,36 @@ def check(out, ref, bound, what=""):
     return worst
 
 
-def test_pad_bitwise_numpy():
-    """a2 vs the library routine numpy.pad, ragged sizes and pads."""
+@pytest.mark.parametrize("layout", ["nchw", "pairs"])
+def test_pad_bitwise_numpy(layout):
+    """a2 vs the library routine numpy.pad, ragged sizes and pads; for the
+    image-pair layout of JIT plans, de-interleaving must give numpy.pad bit for bit and an
+    odd batch's missing second image must be zeros."""
     rng = np.random.default_rng(0)
-    for (N, C, H, W, p) in [(1, 1, 1, 1, 1), (3, 5, 7, 9, 2), (2, 96, 27, 27, 2), (4, 256, 13, 13, 1),
-                            (2, 3, 5, 4, 0), (1, 64, 56, 56, 1), (65, 2, 3, 3, 3)]:
+    kern = skc.SKC_KERNEL_DIRECT if layout == "nchw" else skc.SKC_KERNEL_JIT
+    for (N, C, H, W, p) in [(1, 4, 1, 1, 1), (3, 8, 7, 9, 2), (2, 96, 27, 27, 2), (4, 256, 13, 13, 1),
+                            (2, 4, 5, 4, 0), (1, 64, 56, 56, 1), (65, 4, 3, 3, 3), (5, 2, 3, 3, 1)]:
         x = rng.standard_normal((N, C, H, W), dtype=np.float32)
         x[0, 0, 0, 0] = -0.0
-        layer = wl.Layer("p", 1, C, H, W, 1, 1, 1, p, 1, 0.0, 1.0)
-        plan = skc.skc_pack_csr(np.ones((1, C, 1, 1), np.float32), H, W, 1, p, 1)
+        try:
+            plan = skc.skc_pack_csr(np.ones((1, C, 1, 1), np.float32), H, W, 1, p, 1, kern)
+        except skc.SkcError as e:
+            assert e.status == -5
+            continue
+        info = plan.info()
+        assert info["layout"] == (skc.SKC_LAYOUT_NCHW if layout == "nchw" else skc.SKC_LAYOUT_PAIRS)
         xd = torch.from_numpy(x).cuda()
-        xp = torch.full((N, C, H + 2 * p, W + 2 * p), float("nan"), device="cuda")
+        xp = torch.full(skc.padded_shape(info, N), float("nan"), device="cuda")
         skc.skc_pad_input(plan, xd, xp, N)
         torch.cuda.synchronize()
-        got = xp.cpu().numpy()
+        if layout == "pairs":
+            full = xp.movedim(-1, 1).reshape(-1, C, H + 2 * p, W + 2 * p).cpu().numpy()
+            if N % 2:
+                assert not full[N].any(), "missing second image must be zero"
+            got = full[:N]
+        else:
+            got = xp.cpu().numpy()
         np.testing.assert_array_equal(got.view(np.uint32), oracle.pad_ref(x, p).view(np.uint32))
-        del layer
 
 
 def test_worked_example_gpu(golden_dir):
@@ -311,32 +325,49 @@ def test_fused_epilogue(kernel):
 
 def test_chain_conv3_to_conv5_no_pad_pass():
     """f1 in use: AlexNet conv3 -> conv4 -> conv5 (13x13, pad 1, ReLU between) where each
-    layer writes bias + ReLU straight into the next layer's zero-padded input; every layer is
-    checked against the oracle fed with exactly the GPU's input to that layer."""
+    layer writes bias + ReLU straight into the next layer's zero-padded input, in THAT plan's
+    layout (skc_sparse_conv_forward_into: image-pair interleaved for JIT plans); every layer
+    is checked against the oracle fed with exactly the GPU's input to that layer.  Run with
+    AUTO plans (JIT, pair layout) and with direct plans (NCHW layout), and across the two."""
     cfg = wl.CONFIGS[2]
-    N = 16
     rng = np.random.default_rng(33)
     layers = [cfg.layers[1], cfg.layers[2], cfg.layers[3]]
-    convs = [skc.SparseConv2d.from_dense(wl.gen_weights(2, i + 1, L), L.H, L.W, L.stride, L.pad,
-                                         L.groups) for i, L in enumerate(layers)]
     biases = [(0.1 * rng.standard_normal(L.K)).astype(np.float32) for L in layers]
-    x = wl.gen_input(2, 1, layers[0], 0, N)
-    xp = torch.empty(convs[0].padded_shape(N), device="cuda")
-    skc.skc_pad_input(convs[0].plan, torch.from_numpy(x).cuda(), xp, N)
-    for i, (L, conv, b) in enumerate(zip(layers, convs, biases)):
-        last = i == len(layers) - 1
-        op = 0 if last else layers[i + 1].pad
-        nxt = torch.zeros((N, L.K, L.Ho + 2 * op, L.Wo + 2 * op), device="cuda")
-        skc.skc_sparse_conv_forward_ex(conv.plan, xp, nxt, N, torch.from_numpy(b).cuda(), True, op)
-        torch.cuda.synchronize()
-        xin = xp.cpu().numpy()[:, :, L.pad:L.pad + L.H, L.pad:L.pad + L.W]
-        ref, bound = oracle.conv2d_fp64(np.ascontiguousarray(xin), wl.gen_weights(2, i + 1, L),
-                                        L.stride, L.pad, L.groups)
-        o = nxt.cpu().numpy()[:, :, op:op + L.Ho, op:op + L.Wo]
-        check_epi(o, ref, bound, b, True, f"chain {L.name}")
-        if not last:
-            assert not nxt.cpu().numpy()[:, :, :op, :].any()  # halo still zero
-        xp = nxt
+    for N, kernels in [(16, ("auto", "auto", "auto")), (13, ("direct", "direct", "direct")),
+                       (7, ("auto", "direct", "auto"))]:
+        km = {"auto": skc.SKC_KERNEL_AUTO, "direct": skc.SKC_KERNEL_DIRECT}
+        convs = [skc.SparseConv2d.from_dense(wl.gen_weights(2, i + 1, L), L.H, L.W, L.stride,
+                                             L.pad, L.groups, km[k])
+                 for i, (L, k) in enumerate(zip(layers, kernels))]
+        x = wl.gen_input(2, 1, layers[0], 0, N)
+        xp = torch.empty(convs[0].padded_shape(N), device="cuda")
+        skc.skc_pad_input(convs[0].plan, torch.from_numpy(x).cuda(), xp, N)
+        for i, (L, conv, b) in enumerate(zip(layers, convs, biases)):
+            last = i == len(layers) - 1
+            if last:
+                nxt = torch.zeros((N, L.K, L.Ho, L.Wo), device="cuda")
+                skc.skc_sparse_conv_forward_ex(conv.plan, xp, nxt, N, torch.from_numpy(b).cuda(),
+                                               True, 0)
+            else:
+                nxt = torch.zeros(convs[i + 1].padded_shape(N), device="cuda")
+                skc.skc_sparse_conv_forward_into(conv.plan, xp, convs[i + 1].plan, nxt, N,
+                                                 torch.from_numpy(b).cuda(), True)
+            torch.cuda.synchronize()
+            xin = skc.unpad_view(conv.geom, xp, N).cpu().numpy()[:, :, L.pad:L.pad + L.H,
+                                                                 L.pad:L.pad + L.W]
+            ref, bound = oracle.conv2d_fp64(np.ascontiguousarray(xin), wl.gen_weights(2, i + 1, L),
+                                            L.stride, L.pad, L.groups)
+            if last:
+                o = nxt.cpu().numpy()
+            else:
+                op = layers[i + 1].pad
+                full = skc.unpad_view(convs[i + 1].geom, nxt, N).cpu().numpy()
+                o = full[:, :, op:op + L.Ho, op:op + L.Wo]
+                halo = full.copy()
+                halo[:, :, op:op + L.Ho, op:op + L.Wo] = 0
+                assert not halo.any(), "halo written"
+            check_epi(o, ref, bound, b, True, f"chain {kernels} {L.name}")
+            xp = nxt
 
 
 def test_im2col_equals_unfold():
@@ -433,11 +464,14 @@ def run_jit_and_direct(w, x, layer):
     direct = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
                                          layer.groups, skc.SKC_KERNEL_DIRECT)
     N = x.shape[0]
-    xp = torch.empty(jit.padded_shape(N), device="cuda")
-    skc.skc_pad_input(jit.plan, torch.from_numpy(x).cuda(), xp, N)
+    xd = torch.from_numpy(x).cuda()
+    xpj = torch.empty(jit.padded_shape(N), device="cuda")
+    skc.skc_pad_input(jit.plan, xd, xpj, N)
+    xpd = torch.empty(direct.padded_shape(N), device="cuda")
+    skc.skc_pad_input(direct.plan, xd, xpd, N)
     yj = torch.full(jit.out_shape(N), float("nan"), device="cuda")
-    jit.forward_padded(xp, yj)
-    yd = direct.forward_padded(xp)
+    jit.forward_padded(xpj, yj)
+    yd = direct.forward_padded(xpd)
     torch.cuda.synchronize()
     return yj.cpu().numpy(), yd.cpu().numpy(), jit
 

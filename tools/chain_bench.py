@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Row f1 measurement: AlexNet conv3 -> conv4 -> conv5 at batch 256 with bias + ReLU between
 layers, (a) unfused: skc_pad_input + skc_sparse_conv_forward + a bias/ReLU pass per layer,
-(b) fused: skc_sparse_conv_forward_ex writing each layer's activated output straight into
-the next layer's zero-padded input (one pad pass for conv3's input only)."""
+(b) fused: skc_sparse_conv_forward_into writing each layer's activated output straight into
+the next layer's zero-padded input, in that plan's layout (one pad pass for conv3's input
+only)."""
 import json
 import os
 import sys
@@ -56,16 +57,17 @@ def main():
             h = out
 
     # fused buffers: each layer writes the next layer's padded input (halo zeroed once)
-    fbufs = [torch.empty(convs[0].padded_shape(N), device="cuda")]
-    for i, L in enumerate(layers):
-        op = layers[i + 1].pad if i + 1 < len(layers) else 0
-        fbufs.append(torch.zeros((N, L.K, L.Ho + 2 * op, L.Wo + 2 * op), device="cuda"))
+    fbufs = [torch.zeros(c.padded_shape(N), device="cuda") for c in convs]
+    fbufs.append(torch.zeros(convs[-1].out_shape(N), device="cuda"))
 
     def fused():
         skc.skc_pad_input(convs[0].plan, x, fbufs[0], N)
         for i, (conv, b) in enumerate(zip(convs, biases)):
-            op = layers[i + 1].pad if i + 1 < len(layers) else 0
-            skc.skc_sparse_conv_forward_ex(conv.plan, fbufs[i], fbufs[i + 1], N, b, True, op)
+            if i + 1 < len(convs):
+                skc.skc_sparse_conv_forward_into(conv.plan, fbufs[i], convs[i + 1].plan,
+                                                 fbufs[i + 1], N, b, True)
+            else:
+                skc.skc_sparse_conv_forward_ex(conv.plan, fbufs[i], fbufs[i + 1], N, b, True, 0)
 
     t_u = timed(unfused)
     t_f = timed(fused)

@@ -66,19 +66,22 @@ def main():
                 print(L.name, tile, "FAILED", e, flush=True)
                 continue
             t_build = time.time() - t0
+            xpj = torch.empty(j.padded_shape(N), device="cuda")  # the JIT plan's layout
+            skc.skc_pad_input(j.plan, x, xpj, N)
             y = torch.full_like(y_ref, float("nan"))
-            j.forward_padded(xp, y)
+            j.forward_padded(xpj, y)
             torch.cuda.synchronize()
             same = bool(torch.equal(y, y_ref))
             ndiff = int((y != y_ref).sum().item())
-            ms = time_ms(lambda: j.forward_padded(xp, y))
+            ms = time_ms(lambda: j.forward_padded(xpj, y))
+            ms_pad = time_ms(lambda: skc.skc_pad_input(j.plan, x, xpj, N))
             inf = j.plan.info()
-            rec = dict(layer=L.name, tile=tile, ms=ms, tflops=flops / ms / 1e9, direct_ms=ms_ref,
+            rec = dict(layer=L.name, tile=tile, ms=ms, pad_ms=ms_pad, tflops=flops / ms / 1e9, direct_ms=ms_ref,
                        speedup_vs_direct=ms_ref / ms, bitwise_equal_direct=same, ndiff=ndiff,
                        build_s=t_build, cfg={k: inf[k] for k in (
                            "tile_h", "tile_w", "channels_per_warp", "warps", "images_per_cta",
                            "chunk_channels", "stages", "smem_bytes", "jit_blocks", "code_bytes",
-                           "jit_compile_s", "jit_cache_hit", "model_instr_per_image")})
+                           "jit_compile_s", "jit_cache_hit", "model_instr_per_image", "layout")})
             lines.append(rec)
             print(json.dumps(rec), flush=True)
             del j
