@@ -1327,8 +1327,13 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
             &per_sm, reinterpret_cast<const void *>(jp->kern), jp->NW * 32, jp->smem) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
-    int cs = 1;
+    // clusters of 2 CTAs: the pair is co-scheduled on one GPC and runs the same block's code
+    // on neighbouring image groups, so they share instruction-cache lines (B200 packs 148 SMs
+    // into 74 pairs exactly; +2-7% measured, profiles/r01_jit_cluster.txt).  SKC_JIT_CLUSTER
+    // overrides (1 = no clusters).
+    int cs = 2;
     if (const char *e = std::getenv("SKC_JIT_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(e)));
+    if (items < 2 * cs) cs = 1;
     int64_t grid = std::min<int64_t>(items, int64_t(nsm) * per_sm);
     if (const char *e = std::getenv("SKC_JIT_GRID")) grid = std::min<int64_t>(items, std::max(1, std::atoi(e)));
     if (std::getenv("SKC_JIT_DEBUG")) {
@@ -1353,10 +1358,12 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
         at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        lc.gridDim = dim3(1);
+        lc.gridDim = dim3(unsigned(cs));
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void *>(jp->kern), &lc) != cudaSuccess || ncl < 1)
+        if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void *>(jp->kern), &lc) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();  // the query's error must not leak into later launches
             ncl = int(nsm / cs);
+        }
         grid = std::min<int64_t>((items + cs - 1) / cs, ncl) * cs;
     }
     lc.gridDim = dim3(unsigned(grid));
