@@ -68,7 +68,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 7;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 9;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -116,6 +116,11 @@ struct JitPlan {
     size_t smem = 0;
     int maxreg = 255;          // register cap of the block functions (NW warps per SM)
     int sync_every = 0;        // FMA instructions between CTA barriers in the code (0: none)
+    int l2hint = 1;            // 1: evict-first TMA loads + streaming stores (code stays in L2)
+    // work-item order: 0 block-major, 1 spread (blocks interleaved), 2 first round spread then
+    // block-major.  2: every block's (cold, DRAM-resident) code is fetched in parallel by the
+    // first round, later rounds share one code stream chip-wide (profiles/r01_jit_order.txt)
+    int order = 2;
     int nbg = 0, nblocks = 0;  // blocks per group, total blocks
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
@@ -402,6 +407,8 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o("setp.eq.u32 %%p0, %%r6, 0;");
     o("mov.u32 %%r7, 0;");
     o("mov.u32 %%r8, 1;");
+    // activations stream through L2 (evict first) so the straight-line code stays resident
+    if (jp.l2hint) o("createpolicy.fractional.L2::evict_first.b64 %%rd10, 1.0;");
     o("add.u32 %%rb0, %%r1, %%r0;");
     for (int s = 1; s < jp.NS; ++s) o("add.u32 %%rb%d, %%rb0, %d;", s, s * jp.stage_bytes);
     for (int i = 0; i < Mb * NPT; ++i) o("mov.b64 %%a%d, 0;", i);
@@ -498,8 +505,12 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             o("add.u64 %%rd6, %%rd6, %lld;", (long long)nxt * jp.CB * jp.plane * 4 * sw);
             o("mad.lo.u32 %%r14, %%r12, %d, %%r1;", jp.img_stride * 4);
             o("add.u32 %%r14, %%r14, %d;", s * jp.stage_bytes);
-            o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r14], [%%rd6], "
-              "%d, [%%r15];", bytes);
+            if (jp.l2hint)
+                o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+                  "[%%r14], [%%rd6], %d, [%%r15], %%rd10;", bytes);
+            else
+                o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r14], [%%rd6], "
+                  "%d, [%%r15];", bytes);
             o("add.u32 %%r12, %%r12, 1;");
             o("setp.lt.u32 %%p6, %%r12, %%r3;");
             o("@%%p6 bra $L%d;", i);
@@ -544,12 +555,12 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
                     o("mov.b64 {%%e0, %%e1}, %%a%d;", m * NPT + ty * TX + tx);
                     o("add.f32 %%e3, %%e0, %%e2;");
                     o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
-                    o("@%%p3 st.global.f32 [%%rd5], %%e3;");
+                    o(jp.l2hint ? "@%%p3 st.global.cs.f32 [%%rd5], %%e3;" : "@%%p3 st.global.f32 [%%rd5], %%e3;");
                     o("add.f32 %%e3, %%e1, %%e2;");
                     o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
                     o("and.pred %%p3, %%p3, %%p7;");
                     o("add.u64 %%rd6, %%rd5, %%rd7;");
-                    o("@%%p3 st.global.f32 [%%rd6], %%e3;");
+                    o(jp.l2hint ? "@%%p3 st.global.cs.f32 [%%rd6], %%e3;" : "@%%p3 st.global.f32 [%%rd6], %%e3;");
                     continue;
                 }
                 if (tx < 2 * PX) {
@@ -559,7 +570,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
                     o("add.f32 %%e3, %%f%d, %%e2;", m * NST + ty * (TX - 2 * PX) + tx - 2 * PX);
                 }
                 o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
-                o("@%%p3 st.global.f32 [%%rd5], %%e3;");
+                o(jp.l2hint ? "@%%p3 st.global.cs.f32 [%%rd5], %%e3;" : "@%%p3 st.global.f32 [%%rd5], %%e3;");
             }
         }
     }
@@ -584,7 +595,7 @@ std::string emit_entry(const JitPlan &jp) {
       ".param .u32 p_olay)");
     o("{");
     o(".reg .pred %%p<8>;");
-    o(".reg .b32 %%r<48>;");
+    o(".reg .b32 %%r<56>;");
     o(".reg .b64 %%rd<24>;");
     o("ld.param.u64 %%rd0, [p_in];");
     o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -612,7 +623,8 @@ std::string emit_entry(const JitPlan &jp) {
     o("div.u32 %%r5, %%r5, %d;", jp.NI);        // image groups NIG
     o("mul.lo.u32 %%r32, %%r5, %d;", jp.nblocks);  // items
     o("mov.u32 %%r11, skc_smem;");
-    o("mov.u32 %%r34, 1;");                      // first item: barriers not yet initialised
+    o("mov.u32 %%r34, 1;");
+    if (jp.l2hint) o("createpolicy.fractional.L2::evict_first.b64 %%rd13, 1.0;");                      // first item: barriers not yet initialised
     // lane table (item independent): {smem byte base, (slot<<24)|(y0<<12)|x0, store mask, idle}
     o("mul.wide.u32 %%rd7, %%r3, 16;");
     o("add.u64 %%rd7, %%rd2, %%rd7;");
@@ -639,8 +651,33 @@ std::string emit_entry(const JitPlan &jp) {
     o("$ITEM:");
     o("setp.ge.u32 %%p0, %%r4, %%r32;");
     o("@%%p0 bra $EXIT;");
-    o("rem.u32 %%r6, %%r4, %%r5;");              // image group
-    o("div.u32 %%r7, %%r4, %%r5;");              // block
+    if (jp.order == 1) {
+        // spread: consecutive items are different blocks (every block's code is fetched
+        // in parallel from the first round on)
+        o("rem.u32 %%r7, %%r4, %d;", jp.nblocks);  // block
+        o("div.u32 %%r6, %%r4, %d;", jp.nblocks);  // image group
+    } else if (jp.order == 2) {
+        // first round spread (image groups 0..F-1 of every block, F = floor(G / nblocks):
+        // all blocks' code is pulled from DRAM in parallel), then block-major over the rest
+        o("div.u32 %%r46, %%r31, %d;", jp.nblocks);   // F
+        o("min.u32 %%r46, %%r46, %%r5;");
+        o("mul.lo.u32 %%r47, %%r46, %d;", jp.nblocks); // F * nblocks
+        o("setp.lt.u32 %%p3, %%r4, %%r47;");
+        o("@!%%p3 bra $ORD_REST;");
+        o("rem.u32 %%r7, %%r4, %d;", jp.nblocks);
+        o("div.u32 %%r6, %%r4, %d;", jp.nblocks);
+        o("bra.uni $ORD_DONE;");
+        o("$ORD_REST:");
+        o("sub.u32 %%r6, %%r4, %%r47;");               // t' = t - F*nb
+        o("sub.u32 %%r7, %%r5, %%r46;");               // NIG - F (> 0 here)
+        o("rem.u32 %%r14, %%r6, %%r7;");
+        o("div.u32 %%r7, %%r6, %%r7;");                // block
+        o("add.u32 %%r6, %%r14, %%r46;");              // image group
+        o("$ORD_DONE:");
+    } else {
+        o("rem.u32 %%r6, %%r4, %%r5;");              // image group
+        o("div.u32 %%r7, %%r4, %%r5;");              // block
+    }
     o("mul.lo.u32 %%r8, %%r6, %d;", jp.NI);      // n0
     o("sub.u32 %%r9, %%r0, %%r8;");
     o("min.u32 %%r9, %%r9, %d;", jp.NI);        // images in this item
@@ -692,8 +729,12 @@ std::string emit_entry(const JitPlan &jp) {
         o("add.u64 %%rd6, %%rd6, %lld;", (long long)i * jp.CB * jp.plane * 4 * sw);
         o("mad.lo.u32 %%r16, %%r12, %d, %%r11;", jp.img_stride * 4);
         o("add.u32 %%r16, %%r16, %d;", i * jp.stage_bytes);
-        o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r16], [%%rd6], "
-          "%d, [%%r15];", bytes);
+        if (jp.l2hint)
+            o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+              "[%%r16], [%%rd6], %d, [%%r15], %%rd13;", bytes);
+        else
+            o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r16], [%%rd6], "
+              "%d, [%%r15];", bytes);
         o("add.u32 %%r12, %%r12, 1;");
         o("setp.lt.u32 %%p1, %%r12, %%r41;");
         o("@%%p1 bra $F%d;", i);
@@ -1153,6 +1194,8 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.smem = size_t(jp.off_info) + size_t(NSL) * 8;
     jp.maxreg = reg_cap(jp.NW);
     if (const char *e = std::getenv("SKC_JIT_SYNC")) jp.sync_every = std::max(0, std::atoi(e));
+    if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
     for (int g = 0; g < in.groups; ++g)
         for (int q = 0; q < jp.nbg; ++q) {

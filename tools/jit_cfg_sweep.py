@@ -7,16 +7,18 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CASES = [
-    ("conv2", "0", "1,2", "12"), ("conv2", "1", "1,2", "12"), ("conv2", "1", "1,3", "16"),
-    ("conv2", "1", "2,2", "12"), ("conv2", "1", "1,4", "8"), ("conv2", "1", "1,2", "16"),
-    ("conv3", "1", "1,1", "24"), ("conv3", "1", "1,1", "16"), ("conv3", "1", "1,2", "12"),
-    ("conv3", "1", "1,1", "12"), ("conv3", "0", "1,2", "20"), ("conv3", "1", "1,2", "20"),
-    ("conv5", "1", "1,1", "24"), ("conv5", "1", "1,2", "12"), ("conv5", "1", "1,1", "16"),
+CASES = [  # (layer, pair layout, tile "TY,TX" or "auto", warps)
+    ("conv2", "0", "auto", "12"), ("conv2", "0", "auto", "8"), ("conv2", "0", "auto", "16"),
+    ("conv2", "1", "auto", "12"), ("conv2", "1", "auto", "8"), ("conv2", "1", "auto", "16"),
+    ("conv2", "0", "auto", "20"),
+    ("conv3", "1", "auto", "24"), ("conv3", "1", "auto", "16"), ("conv3", "1", "auto", "12"),
+    ("conv3", "1", "auto", "8"), ("conv3", "0", "auto", "12"), ("conv3", "0", "auto", "20"),
+    ("conv5", "1", "auto", "24"), ("conv5", "1", "auto", "12"), ("conv5", "1", "auto", "16"),
+    ("conv5", "1", "auto", "8"),
 ]
 for layer, pair, tile, nw in CASES:
-    env = dict(os.environ, SKC_JIT_PAIR=pair, SKC_JIT_TILE=tile, SKC_JIT_NW=nw)
-    r = subprocess.run([sys.executable, os.path.join(HERE, "jit_probe.py"), "--tiles", "auto",
+    env = dict(os.environ, SKC_JIT_PAIR=pair, SKC_JIT_NW=nw)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "jit_probe.py"), "--tiles", tile,
                         "--layers", layer], env=env, capture_output=True, text=True, timeout=600)
     for line in r.stdout.splitlines():
         if line.startswith("{"):

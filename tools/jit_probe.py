@@ -18,16 +18,32 @@ from paper_1608_01409_b200 import skc  # noqa: E402
 import workloads as wl  # noqa: E402
 
 
+FLUSH = None
+
+
 def time_ms(fn, reps=10):
+    """Mean device time; with --flush the L2 is flushed (256 MiB write) before every rep,
+    outside the events, as bench.py does (code and data start cold)."""
     fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    if FLUSH is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    tot = 0.0
     for _ in range(reps):
+        FLUSH.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    return tot / reps
 
 
 def main():
@@ -37,7 +53,11 @@ def main():
     ap.add_argument("--N", type=int, default=256)
     ap.add_argument("--cfg", type=int, default=2)
     ap.add_argument("--out", default="")
+    ap.add_argument("--warm", action="store_true", help="no L2 flush between reps")
     a = ap.parse_args()
+    global FLUSH
+    if not a.warm:
+        FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     cfg = wl.CONFIGS[a.cfg]
     N = a.N
     lines = []
