@@ -96,6 +96,7 @@ typedef struct {
     size_t code_bytes;             /* linked device code (cubin) bytes                    */
     double model_instr_per_image;  /* modelled warp-instructions per image (JIT config)   */
     int layout;                    /* skc_layout of the padded input this plan reads      */
+    int bands;                     /* JIT: row bands per image (pair), one CTA item each  */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).

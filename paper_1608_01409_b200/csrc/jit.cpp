@@ -55,9 +55,9 @@ namespace {
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageTarget = 72 * 1024;
 // cost model (clk per image): unique-code fetch ~0.12 instr/clk/SM, shared by the CTA's warps;
-// issue ~2.5 warp-instr/clk/SM (fitted to the B200 sweeps in profiles/r01_jit_*.jsonl)
+// issue ~1.6 warp-instr/clk/SM (fitted to the B200 sweeps in profiles/r01_jit_*.jsonl)
 constexpr double kFetchInv = 1.0 / 0.12;
-constexpr double kIssue = 2.5;
+constexpr double kIssue = 1.6;
 // ... times a penalty for the number of distinct block codes the 148 SMs run at once (the
 // L1.5 instruction cache is per GPC; microbenchmarks: 1 code 33 TF, 2-4 codes 22-24 TF), plus
 // a fixed cost per CTA work item (stage set-up, first TMA round trip, epilogue); fitted to
@@ -68,7 +68,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 9;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 10;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -111,6 +111,8 @@ struct JitPlan {
     int pair = 0;                // 1: image-pair interleaved input layout, FFMA2 over 2 images
     int M = 0, NW = 0, NI = 0, CB = 0, NS = 0, nchunks = 0;
     int tiles_y = 0, tiles_x = 0;
+    int NB = 1;                  // row bands: a work item covers tile rows of one band
+                                 // (lane table per band) -- pair mode on large images
     int plane = 0, img_stride = 0, stage_bytes = 0;
     int off_bar = 0, off_cnt = 0, off_info = 0;
     size_t smem = 0;
@@ -125,7 +127,7 @@ struct JitPlan {
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
     std::vector<int32_t> chan; // [nblocks][M] original output channel or -1
-    std::vector<uint32_t> lanemap;  // [NW*32][4]: lane smem byte base, pos, store mask, 0
+    std::vector<uint32_t> lanemap;  // [NB][NW*32][4]: lane smem byte base, pos, store mask, idle
     // compiled code
     std::vector<char> cubin;
     uint64_t key = 0;
@@ -274,13 +276,17 @@ struct Tile {
     int slot, y0, x0, ry0, rx0;  // origin (shifted back inside the image), nominal origin
 };
 
-int assign_lanes(const JitPlan &jp, int IS, std::vector<uint32_t> *lanemap) {
+// Tile rows of band b of NB: [b*tiles_y/NB, (b+1)*tiles_y/NB).
+int band_lo(int tiles_y, int NB, int b) { return int((int64_t(b) * tiles_y) / NB); }
+
+int assign_lanes(const JitPlan &jp, int IS, int band, uint32_t *lanemap) {
     const JitInput &in = jp.in;
     const int st = in.stride, sw = jp.pair ? 2 : 1;
     const int nslot = jp.NI / sw;
     std::vector<Tile> tiles;
+    const int iy0 = band_lo(jp.tiles_y, jp.NB, band), iy1 = band_lo(jp.tiles_y, jp.NB, band + 1);
     for (int j = 0; j < nslot; ++j)
-        for (int iy = 0; iy < jp.tiles_y; ++iy)
+        for (int iy = iy0; iy < iy1; ++iy)
             for (int ix = 0; ix < jp.tiles_x; ++ix) {
                 const int ry = iy * jp.TY, rx = ix * jp.TX;
                 tiles.push_back(
@@ -321,7 +327,7 @@ int assign_lanes(const JitPlan &jp, int IS, std::vector<uint32_t> *lanemap) {
     }
     if (left) return -1;  // does not fit
     if (lanemap) {
-        lanemap->assign(size_t(jp.NW) * 32 * 4, 0);
+        std::fill(lanemap, lanemap + size_t(jp.NW) * 32 * 4, 0u);
         for (int l = 0; l < jp.NW * 32; ++l) {
             int ti = lane_tile[size_t(l)];
             const bool idle = ti < 0;
@@ -339,7 +345,7 @@ int assign_lanes(const JitPlan &jp, int IS, std::vector<uint32_t> *lanemap) {
                         if (y >= t.ry0 && x >= t.rx0 && y < in.Ho && x < in.Wo)
                             mask |= 1u << (ty * jp.TX + tx);
                     }
-            uint32_t *e = lanemap->data() + size_t(l) * 4;
+            uint32_t *e = lanemap + size_t(l) * 4;
             e[0] = uint32_t(base[size_t(ti)]) * 4u;
             e[1] = (uint32_t(t.slot) << 24) | (uint32_t(t.y0) << 12) | uint32_t(t.x0);
             e[2] = mask;
@@ -620,26 +626,16 @@ std::string emit_entry(const JitPlan &jp) {
     o("mad.lo.u32 %%r4, %%r37, %%r36, %%r35;");  // item t
     o("mul.lo.u32 %%r31, %%r38, %%r36;");        // stride G
     o("add.u32 %%r5, %%r0, %d;", jp.NI - 1);
-    o("div.u32 %%r5, %%r5, %d;", jp.NI);        // image groups NIG
+    o("div.u32 %%r5, %%r5, %d;", jp.NI);        // image groups
+    o("mul.lo.u32 %%r5, %%r5, %d;", jp.NB);     // NIG = image groups x bands
     o("mul.lo.u32 %%r32, %%r5, %d;", jp.nblocks);  // items
     o("mov.u32 %%r11, skc_smem;");
     o("mov.u32 %%r34, 1;");
     if (jp.l2hint) o("createpolicy.fractional.L2::evict_first.b64 %%rd13, 1.0;");                      // first item: barriers not yet initialised
-    // lane table (item independent): {smem byte base, (slot<<24)|(y0<<12)|x0, store mask, idle}
-    o("mul.wide.u32 %%rd7, %%r3, 16;");
-    o("add.u64 %%rd7, %%rd2, %%rd7;");
-    o("ld.global.nc.v4.u32 {%%r17, %%r18, %%r33, %%r20}, [%%rd7];");
-    o("shr.u32 %%r21, %%r18, 24;");              // slot
-    o("shr.u32 %%r22, %%r18, 12;");
-    o("and.b32 %%r22, %%r22, 4095;");            // y0
-    o("and.b32 %%r23, %%r18, 4095;");            // x0
     o("add.u32 %%r24, %%r2, %%r2;");
     o("add.u32 %%r25, %%r24, %d;", in.Ho);       // Hop
     o("add.u32 %%r26, %%r24, %d;", in.Wo);       // Wop
     o("mul.lo.u32 %%r27, %%r25, %%r26;");        // Hop*Wop
-    o("add.u32 %%r29, %%r22, %%r2;");
-    o("mad.lo.u32 %%r29, %%r29, %%r26, %%r23;");
-    o("add.u32 %%r29, %%r29, %%r2;");            // (y0+opad)*Wop + x0+opad
     // output strides: canonical [N][K][Hop][Wop] (olay 0) or pair-interleaved
     // [N/2][K][Hop][Wop][2] (olay 1): element width ew = 4 or 8 bytes
     o("setp.ne.u32 %%p6, %%r39, 0;");
@@ -678,6 +674,21 @@ std::string emit_entry(const JitPlan &jp) {
         o("rem.u32 %%r6, %%r4, %%r5;");              // image group
         o("div.u32 %%r7, %%r4, %%r5;");              // block
     }
+    // image group x band -> band, image group; the lane table of the band:
+    // {smem byte base, (slot<<24)|(y0<<12)|x0, store mask, idle}
+    o("rem.u32 %%r48, %%r6, %d;", jp.NB);        // band
+    o("div.u32 %%r6, %%r6, %d;", jp.NB);         // image group
+    o("mad.lo.u32 %%r49, %%r48, %d, %%r3;", jp.NW * 32);
+    o("mul.wide.u32 %%rd7, %%r49, 16;");
+    o("add.u64 %%rd7, %%rd2, %%rd7;");
+    o("ld.global.nc.v4.u32 {%%r17, %%r18, %%r33, %%r20}, [%%rd7];");
+    o("shr.u32 %%r21, %%r18, 24;");              // slot
+    o("shr.u32 %%r22, %%r18, 12;");
+    o("and.b32 %%r22, %%r22, 4095;");            // y0
+    o("and.b32 %%r23, %%r18, 4095;");            // x0
+    o("add.u32 %%r29, %%r22, %%r2;");
+    o("mad.lo.u32 %%r29, %%r29, %%r26, %%r23;");
+    o("add.u32 %%r29, %%r29, %%r2;");            // (y0+opad)*Wop + x0+opad
     o("mul.lo.u32 %%r8, %%r6, %d;", jp.NI);      // n0
     o("sub.u32 %%r9, %%r0, %%r8;");
     o("min.u32 %%r9, %%r9, %d;", jp.NI);        // images in this item
@@ -898,7 +909,8 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
     // (a slot is an image, or an image pair in the pair-interleaved layout; both images of
     // a pair share the lane's tile and mask)
     std::vector<int> cover(size_t(NSL) * in.Ho * in.Wo, 0);
-    for (int l = 0; l < jp->NW * 32; ++l) {
+    if (jp->lanemap.size() != size_t(jp->NB) * jp->NW * 32 * 4) return bad("lane table size");
+    for (int l = 0; l < jp->NB * jp->NW * 32; ++l) {
         const uint32_t *e = jp->lanemap.data() + size_t(l) * 4;
         const int img = int(e[1] >> 24), y0 = int((e[1] >> 12) & 4095), x0 = int(e[1] & 4095);
         if (img >= NSL || y0 + TY > in.Ho || x0 + TX > in.Wo) return bad("lane tile out of range");
@@ -1057,6 +1069,8 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
         return 0;
     };
     int pair_force = -1;  // SKC_JIT_PAIR=0/1 (tuning): canonical or image-pair layout only
+    int band_force = 0;   // SKC_JIT_BANDS=n (tuning)
+    if (const char *e = std::getenv("SKC_JIT_BANDS")) band_force = std::max(1, std::atoi(e));
     if (const char *e = std::getenv("SKC_JIT_PAIR")) pair_force = std::atoi(e) ? 1 : 0;
     std::unique_ptr<JitPlan> best;
     std::vector<int> ks;
@@ -1100,7 +1114,13 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     M = std::min(M, in.Kg);
                     if (M < 1) continue;
                     const int ty_n = (in.Ho + TY - 1) / TY, tx_n = (in.Wo + TX - 1) / TX;
-                    const int tpi = ty_n * tx_n;
+                    // row bands: an image (pair) too large for one CTA's lanes is split into
+                    // NB bands of tile rows, one work item each (pair mode; NB = 1 otherwise)
+                    for (int NB = 1; NB <= (pm ? 4 : 1); ++NB) {
+                    if (NB > ty_n) break;
+                    if (band_force > 0 && NB != band_force) continue;
+                    const int tpi = ((ty_n + NB - 1) / NB) * tx_n;  // tiles of the largest band
+                    if (NB > 1 && ty_n * tx_n <= lanes_max) break;  // a whole slot fits already
                     int NSL = std::min(max_ni / sw, lanes_max / tpi);  // slots per CTA item
                     if (NSL < 1) continue;
                     int CB = 0, NS = 0, IS = 0, stage = 0;
@@ -1121,10 +1141,12 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     const int NW = (NSL * tpi + 31) / 32;
                     if (NW > nw_max) continue;
                     const int nbg = (in.Kg + M - 1) / M;
-                    // distinct blocks running at once for a batch of n_hint images
-                    const int nig = (n_hint + NI - 1) / NI;
+                    // distinct blocks running at once for a batch of n_hint images (an item
+                    // covers NI images x 1/NB of their pixels: NIe image-equivalents)
+                    const double NIe = double(NI) / NB;
+                    const int nig = (n_hint + NI - 1) / NI * NB;
                     const int conc = std::max(1, (kSMs + nig - 1) / nig);
-                    const double share = std::max(kFetchInv, NW / kIssue) / NI * conc_penalty(conc);
+                    const double share = std::max(kFetchInv, NW / kIssue) / NIe * conc_penalty(conc);
                     // lower bound (FMA instructions only; independent of the blocking) prunes
                     // most candidates before the exact count
                     if (best && double(nnz_total) * fma_per_nz(TY, TX, PX, pm) * share >= best->cost)
@@ -1140,7 +1162,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     // item and shared by its NW warps; fetch-bound below ~20 warps, issue-bound
                     // above
                     if (instr > code_cap) continue;  // code size: compile time, I-fetch footprint
-                    const double cost = instr * share + double(nbg * in.groups) / NI * kItemCycles;
+                    const double cost = instr * share + double(nbg * in.groups) / NIe * kItemCycles;
                     if (best && cost >= best->cost) continue;
                     std::unique_ptr<JitPlan> jp(new JitPlan());
                     jp->in = in;
@@ -1148,11 +1170,12 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     jp->TY = TY; jp->TX = TX; jp->PX = PX; jp->M = M;
                     jp->NW = NW; jp->NI = NI; jp->CB = CB; jp->NS = NS;
                     jp->nchunks = (in.Cg + CB - 1) / CB;
-                    jp->tiles_y = ty_n; jp->tiles_x = tx_n;
+                    jp->tiles_y = ty_n; jp->tiles_x = tx_n; jp->NB = NB;
                     jp->plane = plane; jp->img_stride = IS; jp->stage_bytes = stage;
                     jp->nbg = nbg; jp->nblocks = nbg * in.groups;
                     jp->cost = cost;
                     best = std::move(jp);
+                    }  // NB
                 }
         }
     }
@@ -1171,7 +1194,11 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
         const int IS = IS0 + 4 * t;
         const size_t smem = size_t(jp.NS) * NSL * IS * 4 + 256 + size_t(NSL) * 8;
         if (smem > size_t(kMaxSmem)) break;
-        const int e = assign_lanes(jp, IS, nullptr);
+        int e = 0;
+        for (int b = 0; b < jp.NB && e >= 0; ++b) {
+            const int eb = assign_lanes(jp, IS, b, nullptr);
+            e = eb < 0 ? -1 : e + eb;
+        }
         if (e >= 0 && (best_extra < 0 || e < best_extra)) {
             best_extra = e;
             best_is = IS;
@@ -1185,7 +1212,9 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.img_stride = best_is;
     jp.conflict = best_extra;
     jp.stage_bytes = NSL * best_is * 4;
-    assign_lanes(jp, best_is, &jp.lanemap);
+    jp.lanemap.assign(size_t(jp.NB) * jp.NW * 32 * 4, 0);
+    for (int b = 0; b < jp.NB; ++b)
+        assign_lanes(jp, best_is, b, jp.lanemap.data() + size_t(b) * jp.NW * 32 * 4);
     jp.off_bar = jp.NS * jp.stage_bytes;           // 128-byte aligned: stages are 16 B multiples
     jp.off_bar = (jp.off_bar + 15) / 16 * 16;
     jp.off_cnt = jp.off_bar + 8 * kMaxStages;
@@ -1320,6 +1349,7 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;
+    o->bands = jp->NB;
     o->compiled = jp->compiled ? 1 : 0;
 }
 

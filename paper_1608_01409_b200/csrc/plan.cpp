@@ -871,6 +871,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.jit_blocks = 0; i.jit_compiled = 0; i.jit_cache_hit = 0; i.jit_compile_s = 0;
     i.code_bytes = 0; i.model_instr_per_image = 0;
     i.layout = p->layout;
+    i.bands = 0;
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -880,6 +881,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
         i.jit_blocks = j.nblocks; i.jit_compiled = j.compiled; i.jit_cache_hit = j.cache_hit;
         i.jit_compile_s = j.compile_s; i.code_bytes = j.cubin_bytes;
         i.model_instr_per_image = j.cost;
+        i.bands = j.bands;
     }
     return ok();
 }

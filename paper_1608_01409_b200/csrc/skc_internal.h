@@ -117,6 +117,7 @@ struct JitInfo {
     double compile_s;
     int cache_hit, compiled;
     int pair;  // 1: the plan reads the image-pair interleaved padded layout
+    int bands; // row bands per image (pair) -- work items per image group
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).

@@ -132,7 +132,9 @@ def test_plan_info_configuration(L):
         info = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups).info()
         assert info["kernel"] == skc.SKC_KERNEL_JIT
         assert info["smem_bytes"] <= 227 * 1024
-        tiles = -(-layer.Ho // info["tile_h"]) * -(-layer.Wo // info["tile_w"])
+        ty = -(-layer.Ho // info["tile_h"])
+        band_rows = -(-ty // info["bands"])  # tile rows of the largest row band
+        tiles = band_rows * -(-layer.Wo // info["tile_w"])
         per_lane = 2 if info["layout"] == skc.SKC_LAYOUT_PAIRS else 1  # images per lane tile
         assert tiles * info["images_per_cta"] <= info["warps"] * 32 * per_lane
         assert info["jit_blocks"] * info["channels_per_warp"] >= layer.K
