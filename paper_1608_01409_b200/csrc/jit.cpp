@@ -68,7 +68,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 10;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 11;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -123,6 +123,7 @@ struct JitPlan {
     // block-major.  2: every block's (cold, DRAM-resident) code is fetched in parallel by the
     // first round, later rounds share one code stream chip-wide (profiles/r01_jit_order.txt)
     int order = 2;
+    int dry = 1;               // 1: instruction prefetch by dry-running code segments at start
     int nbg = 0, nblocks = 0;  // blocks per group, total blocks
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
@@ -361,11 +362,13 @@ int assign_lanes(const JitPlan &jp, int IS, int band, uint32_t *lanemap) {
 const char *kHdr = ".version 8.8\n.target sm_100a\n.address_size 64\n";
 // block function parameters: lane smem base, smem base, lane output base (image A), store
 // mask (bit 31: image B valid, pair mode), slots in this item, bias, relu, output row /
-// channel / pixel strides, byte offset of image B's output from image A's
+// channel / pixel strides, byte offset of image B's output from image A's, dry-run chunk
+// (0: a real run; k + 1: execute only chunk k's code, no waits, no stores -- instruction
+// prefetch, see emit_entry)
 const char *kBlkParams =
     "(.param .b32 q_lb, .param .b32 q_sm, .param .b64 q_out, .param .b32 q_mask, "
     ".param .b32 q_nsl, .param .b64 q_bias, .param .b32 q_relu, .param .b32 q_rs, "
-    ".param .b64 q_cs, .param .b32 q_ps, .param .b64 q_bo)";
+    ".param .b64 q_cs, .param .b32 q_ps, .param .b64 q_bo, .param .b32 q_dry)";
 
 int chunk_channels(const JitPlan &jp, int i) { return std::min(jp.CB, jp.in.Cg - i * jp.CB); }
 
@@ -386,7 +389,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o("%s", kHdr);
     o(".visible .func skc_b%d%s", b, kBlkParams);
     o("{");
-    o(".reg .pred %%p<8>;");
+    o(".reg .pred %%p<10>;");
     o(".reg .b32 %%r<24>;");
     o(".reg .b64 %%rd<12>;");
     o(".reg .b32 %%rb<%d>;", jp.NS);
@@ -419,6 +422,16 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     for (int s = 1; s < jp.NS; ++s) o("add.u32 %%rb%d, %%rb0, %d;", s, s * jp.stage_bytes);
     for (int i = 0; i < Mb * NPT; ++i) o("mov.b64 %%a%d, 0;", i);
     for (int i = 0; i < Mb * NST; ++i) o("mov.f32 %%f%d, 0f00000000;", i);
+    // dry run: jump straight to chunk k's code (no barrier wait), return after it
+    o("ld.param.b32 %%r17, [q_dry];");
+    o("setp.ne.u32 %%p8, %%r17, 0;");
+    o("@!%%p8 bra $REAL;");
+    for (int i = 0; i < jp.nchunks; ++i) {
+        o("setp.eq.u32 %%p9, %%r17, %d;", i + 1);
+        o("@%%p9 bra $B%d;", i);
+    }
+    o("bra.uni $DRYRET;");
+    o("$REAL:");
 
     Need nd;
     int since_sync = 0;
@@ -429,6 +442,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         o("mbarrier.try_wait.parity.shared::cta.b64 %%p4, [%%r1+%d], %%r%d;", jp.off_bar + 8 * s,
           par ? 8 : 7);
         o("@!%%p4 bra $W%d;", i);
+        o("$B%d:", i);
         const int cn = chunk_channels(jp, i);
         for (int cl = 0; cl < cn; ++cl) {
             const int c = i * jp.CB + cl;
@@ -489,6 +503,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
                 }
             }
         }
+        o("@%%p8 bra $DRYRET;");
         // release the stage; the last warp out refills it with chunk i + NS
         if (i + jp.NS < jp.nchunks) {
             const int nxt = i + jp.NS;
@@ -581,6 +596,8 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         }
     }
     o("ret;");
+    o("$DRYRET:");
+    o("ret;");
     o("}");
     return std::move(o.s);
 }
@@ -644,6 +661,45 @@ std::string emit_entry(const JitPlan &jp) {
     o("mul.wide.u32 %%rd10, %%r27, %%r40;");      // channel stride bytes
     o("mul.lo.u64 %%rd11, %%rd10, %d;", in.K);    // image stride bytes (canonical)
     o("selp.u64 %%rd12, 4, %%rd11, %%p6;");       // image B offset: 4 (interleaved) or K*Hop*Wop*4
+    if (jp.dry) {
+        // Instruction prefetch: the code of a layer is cold in DRAM at launch and fetching it
+        // is latency-bound per code stream.  Before the first item every CTA dry-runs a few
+        // (block, chunk) code segments -- pairs ctaid, ctaid + G, ... of nblocks x nchunks --
+        // so the whole layer's code is pulled into L2 by many parallel streams at once.
+        o("mul.wide.u32 %%rd14, %%r3, 16;");
+        o("add.u64 %%rd14, %%rd2, %%rd14;");
+        o("ld.global.nc.u32 %%r50, [%%rd14];");     // a valid lane base (band 0)
+        o("mov.u32 %%r51, %%r4;");
+        o("$DRY_LOOP:");
+        o("setp.ge.u32 %%p0, %%r51, %d;", jp.nblocks * jp.nchunks);
+        o("@%%p0 bra $DRY_DONE;");
+        o("div.u32 %%r52, %%r51, %d;", jp.nchunks);  // block
+        o("rem.u32 %%r53, %%r51, %d;", jp.nchunks);
+        o("add.u32 %%r53, %%r53, 1;");               // chunk + 1
+        for (int b = 0; b < jp.nblocks; ++b) {
+            o("setp.eq.u32 %%p3, %%r52, %d;", b);
+            o("@%%p3 bra $DC%d;", b);
+        }
+        o("bra.uni $DRY_NEXT;");
+        for (int b = 0; b < jp.nblocks; ++b) {
+            o("$DC%d:", b);
+            o("{");
+            o(".param .b32 t0;\n.param .b32 t1;\n.param .b64 t2;\n.param .b32 t3;\n.param .b32 t4;");
+            o(".param .b64 t5;\n.param .b32 t6;\n.param .b32 t7;\n.param .b64 t8;\n.param .b32 t9;");
+            o(".param .b64 t10;\n.param .b32 t11;");
+            o("st.param.b32 [t0], %%r50;\nst.param.b32 [t1], %%r11;\nst.param.b64 [t2], %%rd1;");
+            o("st.param.b32 [t3], 0;\nst.param.b32 [t4], 0;\nst.param.b64 [t5], 0;");
+            o("st.param.b32 [t6], 0;\nst.param.b32 [t7], 0;\nst.param.b64 [t8], 0;");
+            o("st.param.b32 [t9], 0;\nst.param.b64 [t10], 0;\nst.param.b32 [t11], %%r53;");
+            o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11);", b);
+            o("}");
+            o("bra.uni $DRY_NEXT;");
+        }
+        o("$DRY_NEXT:");
+        o("add.u32 %%r51, %%r51, %%r31;");
+        o("bra.uni $DRY_LOOP;");
+        o("$DRY_DONE:");
+    }
     o("$ITEM:");
     o("setp.ge.u32 %%p0, %%r4, %%r32;");
     o("@%%p0 bra $EXIT;");
@@ -790,12 +846,12 @@ std::string emit_entry(const JitPlan &jp) {
         o("{");
         o(".param .b32 t0;\n.param .b32 t1;\n.param .b64 t2;\n.param .b32 t3;\n.param .b32 t4;");
         o(".param .b64 t5;\n.param .b32 t6;\n.param .b32 t7;\n.param .b64 t8;\n.param .b32 t9;");
-        o(".param .b64 t10;");
+        o(".param .b64 t10;\n.param .b32 t11;");
         o("st.param.b32 [t0], %%r17;\nst.param.b32 [t1], %%r11;\nst.param.b64 [t2], %%rd8;");
         o("st.param.b32 [t3], %%r19;\nst.param.b32 [t4], %%r41;\nst.param.b64 [t5], %%rd3;");
         o("st.param.b32 [t6], %%r1;\nst.param.b32 [t7], %%r30;\nst.param.b64 [t8], %%rd10;");
-        o("st.param.b32 [t9], %%r40;\nst.param.b64 [t10], %%rd12;");
-        o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10);", b);
+        o("st.param.b32 [t9], %%r40;\nst.param.b64 [t10], %%rd12;\nst.param.b32 [t11], 0;");
+        o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11);", b);
         o("}");
         o("bra.uni $NEXT;");
     }
@@ -1225,6 +1281,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_SYNC")) jp.sync_every = std::max(0, std::atoi(e));
     if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
+    if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
     for (int g = 0; g < in.groups; ++g)
         for (int q = 0; q < jp.nbg; ++q) {
