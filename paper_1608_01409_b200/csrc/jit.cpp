@@ -54,6 +54,8 @@ namespace {
 
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageTarget = 72 * 1024;
+constexpr int kStage2Max = 108 * 1024;    // stage bytes when only 2 stages are used
+constexpr double kChunkInstr = 1000.0;   // minimum instructions per warp per chunk
 // cost model (clk per image): unique-code fetch ~0.12 instr/clk/SM, shared by the CTA's warps;
 // issue ~1.6 warp-instr/clk/SM (fitted to the B200 sweeps in profiles/r01_jit_*.jsonl)
 constexpr double kFetchInv = 1.0 / 0.12;
@@ -1126,6 +1128,10 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     };
     int pair_force = -1;  // SKC_JIT_PAIR=0/1 (tuning): canonical or image-pair layout only
     int band_force = 0;   // SKC_JIT_BANDS=n (tuning)
+    // staging pipeline: bytes per stage and stages (SKC_JIT_STAGE_KB, SKC_JIT_NS: tuning)
+    int stage_target = kStageTarget, ns_max = 3;
+    if (const char *e = std::getenv("SKC_JIT_STAGE_KB")) stage_target = std::max(4, std::atoi(e)) * 1024;
+    if (const char *e = std::getenv("SKC_JIT_NS")) ns_max = std::max(2, std::min(kMaxStages, std::atoi(e)));
     if (const char *e = std::getenv("SKC_JIT_BANDS")) band_force = std::max(1, std::atoi(e));
     if (const char *e = std::getenv("SKC_JIT_PAIR")) pair_force = std::atoi(e) ? 1 : 0;
     std::unique_ptr<JitPlan> best;
@@ -1182,11 +1188,11 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     int CB = 0, NS = 0, IS = 0, stage = 0;
                     size_t smem = 0;
                     for (; NSL >= 1; --NSL) {
-                        CB = kStageTarget / (NSL * plane * 4 * sw);
+                        CB = stage_target / (NSL * plane * 4 * sw);
                         CB = std::min(in.Cg, CB / cb_unit * cb_unit);
                         if (CB < cb_unit) CB = cb_unit;
                         const int nch = (in.Cg + CB - 1) / CB;
-                        NS = std::min(3, nch);
+                        NS = std::min(ns_max, nch);
                         IS = (CB * plane * sw + 3) / 4 * 4;
                         stage = NSL * IS * 4;
                         smem = size_t(NS) * stage + 256 + size_t(NSL) * 8;
@@ -1218,6 +1224,22 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     // item and shared by its NW warps; fetch-bound below ~20 warps, issue-bound
                     // above
                     if (instr > code_cap) continue;  // code size: compile time, I-fetch footprint
+                    // light chunks (few instructions per warp between stage boundaries) pay
+                    // the boundary (wait, release, refill) too often: use 2 large stages
+                    // instead (profiles/r01_jit_stages.txt)
+                    if (!std::getenv("SKC_JIT_NS") && NS == 3) {
+                        const double per_ch = instr / (double(nbg) * in.groups * in.Cg);
+                        if (per_ch * CB < kChunkInstr) {
+                            int CB2 = kStage2Max / (NSL * plane * 4 * sw);
+                            CB2 = std::min(in.Cg, CB2 / cb_unit * cb_unit);
+                            if (CB2 > CB) {
+                                CB = CB2;
+                                NS = std::min(2, (in.Cg + CB - 1) / CB);
+                                IS = (CB * plane * sw + 3) / 4 * 4;
+                                stage = NSL * IS * 4;
+                            }
+                        }
+                    }
                     const double cost = instr * share + double(nbg * in.groups) / NIe * kItemCycles;
                     if (best && cost >= best->cost) continue;
                     std::unique_ptr<JitPlan> jp(new JitPlan());
