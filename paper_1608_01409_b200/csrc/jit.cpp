@@ -1203,6 +1203,9 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     const int NW = (NSL * tpi + 31) / 32;
                     if (NW > nw_max) continue;
                     const int nbg = (in.Kg + M - 1) / M;
+                    // even blocks: M' = ceil(Kg / nbg) <= M (no small leftover block paying a
+                    // full set of window loads for a few channels)
+                    if (fm <= 0) M = (in.Kg + nbg - 1) / nbg;
                     // distinct blocks running at once for a batch of n_hint images (an item
                     // covers NI images x 1/NB of their pixels: NIe image-equivalents)
                     const double NIe = double(NI) / NB;
