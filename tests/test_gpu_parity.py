@@ -522,3 +522,30 @@ def test_jit_bitwise_equals_direct_full_batch(cfg_id):
         yj, yd, conv = run_jit_and_direct(w, x, L)
         assert conv.geom["kernel"] == skc.SKC_KERNEL_JIT
         np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32), err_msg=L.name)
+
+
+@pytest.mark.parametrize("knobs", [
+    {"SKC_JIT_ORDER": "0"}, {"SKC_JIT_ORDER": "1"}, {"SKC_JIT_DRY": "0"},
+    {"SKC_JIT_L2HINT": "0"}, {"SKC_JIT_CLUSTER": "1"}, {"SKC_JIT_CLUSTER": "4"},
+    {"SKC_JIT_PAIR": "0"}, {"SKC_JIT_PAIR": "1", "SKC_JIT_BANDS": "3"},
+    {"SKC_JIT_NS": "4", "SKC_JIT_STAGE_KB": "24"}, {"SKC_JIT_NW": "8"}, {"SKC_JIT_NW": "24"},
+    {"SKC_JIT_GRID": "7"},
+])
+def test_jit_tuning_knobs_bitwise(knobs, monkeypatch):
+    """Every JIT tuning knob (work order, dry-run prefetch, L2 policy, cluster size, layout,
+    row bands, staging depth, warps, grid size) changes scheduling only: the output must stay
+    bit-for-bit equal to the direct kernel's on ragged shapes (odd batch, 27x27 with bands,
+    grouped 13x13)."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(44)
+    for layer, N in [(wl.Layer("k1", 48, 32, 27, 27, 5, 5, 1, 2, 2, 0.85, 0.01), 7),
+                     (wl.Layer("k2", 40, 64, 13, 13, 3, 3, 1, 1, 2, 0.9, 0.01), 9)]:
+        w, x = wl.random_tensors(rng, layer, N)
+        try:
+            yj, yd, conv = run_jit_and_direct(w, x, layer)
+        except skc.SkcError as e:
+            assert e.status == -5, e
+            continue
+        np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32),
+                                      err_msg=f"{knobs} {layer.name} {conv.geom}")

@@ -8,13 +8,13 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CASES = [  # (layer, pair layout, tile "TY,TX" or "auto", warps)
-    ("conv2", "0", "auto", "12"), ("conv2", "0", "auto", "8"), ("conv2", "0", "auto", "16"),
-    ("conv2", "1", "auto", "12"), ("conv2", "1", "auto", "8"), ("conv2", "1", "auto", "16"),
-    ("conv2", "0", "auto", "20"),
-    ("conv3", "1", "auto", "24"), ("conv3", "1", "auto", "16"), ("conv3", "1", "auto", "12"),
-    ("conv3", "1", "auto", "8"), ("conv3", "0", "auto", "12"), ("conv3", "0", "auto", "20"),
-    ("conv5", "1", "auto", "24"), ("conv5", "1", "auto", "12"), ("conv5", "1", "auto", "16"),
-    ("conv5", "1", "auto", "8"),
+    ("conv2", "0", "auto", "12"), ("conv2", "0", "auto", "16"), ("conv2", "1", "auto", "12"),
+    ("conv2", "1", "auto", "16"), ("conv2", "1", "auto", "8"),
+    ("conv3", "1", "auto", "16"), ("conv3", "1", "auto", "12"), ("conv3", "1", "auto", "20"),
+    ("conv3", "0", "auto", "12"),
+    ("conv4", "1", "auto", "16"), ("conv4", "1", "auto", "12"), ("conv4", "1", "auto", "20"),
+    ("conv5", "1", "auto", "16"), ("conv5", "1", "auto", "12"), ("conv5", "1", "auto", "20"),
+    ("conv5", "0", "auto", "12"),
 ]
 for layer, pair, tile, nw in CASES:
     env = dict(os.environ, SKC_JIT_PAIR=pair, SKC_JIT_NW=nw)
