@@ -348,10 +348,22 @@ def run_ours(args, cfg, rank, world, local_rank):
     if not args.no_e2e:
         hin = [d["x_host"].pin_memory() for d in layers]
         hout = [torch.empty(d["conv"].out_shape(per_gpu)).pin_memory() for d in layers]
+        # the four layers are independent: each runs its H2D / pad + conv / D2H pipeline on
+        # its own stream (forked from and joined back into the timed stream), so one layer's
+        # output copy overlaps the next layer's input copy on the two copy engines
+        side = [torch.cuda.Stream(dev) for _ in layers]
+
         def estep():
-            for d, hi, ho in zip(layers, hin, hout):
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            for s_, d, hi, ho in zip(side, layers, hin, hout):
+                s_.wait_event(fork)
                 skc.skc_forward_host(d["conv"].plan, hi, ho, per_gpu, d["x"], d["xp"], d["out"],
-                                     stream)
+                                     s_)
+            for s_ in side:
+                j = torch.cuda.Event()
+                j.record(s_)
+                stream.wait_event(j)
         estep(); torch.cuda.synchronize()
         ems = []
         for _ in range(max(3, args.steps // 4)):
