@@ -237,10 +237,16 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     layers = []
     t_build = time.time()
+    # plan build (pack + JIT compile + upload): one-off, untimed; the JIT
+    # compiles of the layers run concurrently (host threads; ctypes releases the GIL)
+    plans = [skc.skc_pack_csr(wl.gen_weights(cfg.cfg_id, li, L), L.H, L.W, L.stride, L.pad,
+                              L.groups, kernel) for li, L in enumerate(cfg.layers)]
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=len(plans)) as ex:
+        list(ex.map(skc.skc_plan_compile, plans))
     for li, L in enumerate(cfg.layers):
         w = wl.gen_weights(cfg.cfg_id, li, L)
-        # plan build (pack + JIT compile + upload): one-off, untimed
-        conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kernel, dev)
+        conv = skc.SparseConv2d.from_plan(plans[li], dev)
         x_host = torch.from_numpy(wl.gen_input(cfg.cfg_id, li, L, n0, n1))
         x = x_host.to(dev)
         xp = torch.empty(conv.padded_shape(per_gpu), device=dev)

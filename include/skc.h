@@ -97,6 +97,7 @@ typedef struct {
     double model_instr_per_image;  /* modelled warp-instructions per image (JIT config)   */
     int layout;                    /* skc_layout of the padded input this plan reads      */
     int bands;                     /* JIT: row bands per image (pair), one CTA item each  */
+    int jit_whole;                 /* JIT: 1 = one whole-program compile (no ABI calls)   */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).

@@ -56,6 +56,7 @@ constexpr int kMaxSmem = 227 * 1024;
 constexpr int kStageTarget = 72 * 1024;
 constexpr int kStage2Max = 108 * 1024;    // stage bytes when only 2 stages are used
 constexpr double kChunkInstr = 1000.0;   // minimum instructions per warp per chunk
+constexpr double kWholeMaxInstr = 1.2e5; // largest code compiled as one whole program
 // cost model (clk per image): unique-code fetch ~0.12 instr/clk/SM, shared by the CTA's warps;
 // issue ~1.6 warp-instr/clk/SM (fitted to the B200 sweeps in profiles/r01_jit_*.jsonl)
 constexpr double kFetchInv = 1.0 / 0.12;
@@ -70,7 +71,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 11;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 12;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -126,6 +127,8 @@ struct JitPlan {
     // first round, later rounds share one code stream chip-wide (profiles/r01_jit_order.txt)
     int order = 2;
     int dry = 1;               // 1: instruction prefetch by dry-running code segments at start
+    int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
+    double code_instr = 0;     // modelled instructions of all blocks' code
     int nbg = 0, nblocks = 0;  // blocks per group, total blocks
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
@@ -870,15 +873,15 @@ std::string emit_entry(const JitPlan &jp) {
 // compile + link (PTX compiler library in a thread pool, nvJitLink), with an on-disk cache
 // ---------------------------------------------------------------------------------------
 bool compile_ptx(const std::string &ptx, const char *opt, int maxreg, std::vector<char> &obj,
-                 std::string *msg) {
+                 std::string *msg, bool relocatable = true) {
     nvPTXCompilerHandle h = nullptr;
     if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
         *msg = "nvPTXCompilerCreate failed";
         return false;
     }
     const std::string mr = "--maxrregcount=" + std::to_string(maxreg);
-    const char *opts[] = {"--gpu-name=sm_100a", "--compile-only", opt, mr.c_str()};
-    const nvPTXCompileResult r = nvPTXCompilerCompile(h, 4, opts);
+    const char *opts[] = {"--gpu-name=sm_100a", opt, mr.c_str(), "--compile-only"};
+    const nvPTXCompileResult r = nvPTXCompilerCompile(h, relocatable ? 4 : 3, opts);
     bool okr = r == NVPTXCOMPILE_SUCCESS;
     if (!okr) {
         size_t n = 0;
@@ -1255,6 +1258,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     jp->plane = plane; jp->img_stride = IS; jp->stage_bytes = stage;
                     jp->nbg = nbg; jp->nblocks = nbg * in.groups;
                     jp->cost = cost;
+                    jp->code_instr = instr;
                     best = std::move(jp);
                     }  // NB
                 }
@@ -1307,6 +1311,11 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
+    // whole-program compile (one serial ptxas run, ~10-20 s per 100k instructions) when the
+    // code is moderate; parallel per-block modules otherwise (their calls pay an ABI
+    // save/restore of callee-saved registers: -8-10% measured, profiles/r01_jit_whole.txt)
+    jp.whole = jp.code_instr <= kWholeMaxInstr ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
     for (int g = 0; g < in.groups; ++g)
         for (int q = 0; q < jp.nbg; ++q) {
@@ -1349,11 +1358,38 @@ int jit_compile(JitPlan *jp, std::string *msg) {
     uint64_t key = fnv1a(&kJitVersion, sizeof kJitVersion);
     key = fnv1a(opt, std::strlen(opt), key);
     key = fnv1a(&jp->maxreg, sizeof jp->maxreg, key);
+    key = fnv1a(&jp->whole, sizeof jp->whole, key);
     for (const auto &m : mods) key = fnv1a(m.data(), m.size(), key);
     jp->key = key;
     if (cache_read(key, jp->cubin)) {
         jp->cache_hit = 1;
         jp->compiled = true;
+        return SKC_OK;
+    }
+    if (jp->whole) {
+        // whole-program mode: one module, one compile -- ptxas sees every call site, so the
+        // block functions need no ABI save/restore of callee-saved registers (which costs a
+        // burst of local-memory stores at every call of a separately compiled block)
+        std::string all(kHdr);
+        for (size_t i = 0; i + 1 < mods.size(); ++i) all.append(mods[i], std::strlen(kHdr), std::string::npos);
+        const std::string &ent = mods.back();
+        size_t pos = std::strlen(kHdr);
+        for (;;) {
+            while (pos < ent.size() && ent[pos] == '\n') ++pos;
+            if (ent.compare(pos, 12, ".extern .fun") != 0) break;
+            pos = ent.find('\n', pos) + 1;
+        }
+        all.append(ent, pos, std::string::npos);
+        std::vector<std::string>().swap(mods);
+        std::string err;
+        if (!compile_ptx(all, opt, jp->maxreg, jp->cubin, &err, false)) {
+            *msg = err;
+            return SKC_ERR_UNSUPPORTED;
+        }
+        cache_write(key, jp->cubin);
+        jp->compiled = true;
+        jp->compile_s =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return SKC_OK;
     }
     // compile modules in parallel
@@ -1432,6 +1468,7 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;
     o->bands = jp->NB;
+    o->whole = jp->whole;
     o->compiled = jp->compiled ? 1 : 0;
 }
 

@@ -872,6 +872,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.code_bytes = 0; i.model_instr_per_image = 0;
     i.layout = p->layout;
     i.bands = 0;
+    i.jit_whole = 0;
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -882,6 +883,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
         i.jit_compile_s = j.compile_s; i.code_bytes = j.cubin_bytes;
         i.model_instr_per_image = j.cost;
         i.bands = j.bands;
+        i.jit_whole = j.whole;
     }
     return ok();
 }

@@ -50,7 +50,7 @@ class skc_info(ctypes.Structure):
         ("images_per_cta", ctypes.c_int), ("jit_blocks", ctypes.c_int),
         ("jit_compiled", ctypes.c_int), ("jit_cache_hit", ctypes.c_int),
         ("jit_compile_s", ctypes.c_double), ("code_bytes", ctypes.c_size_t),
-        ("model_instr_per_image", ctypes.c_double), ("layout", ctypes.c_int), ("bands", ctypes.c_int)]
+        ("model_instr_per_image", ctypes.c_double), ("layout", ctypes.c_int), ("bands", ctypes.c_int), ("jit_whole", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -387,6 +387,12 @@ class SparseConv2d:
     def from_dense(cls, w: np.ndarray, H: int, W: int, stride=1, pad=0, groups=1,
                    kernel=SKC_KERNEL_AUTO, device="cuda"):
         plan = skc_pack_csr(w, H, W, stride, pad, groups, kernel)
+        plan.upload(device)
+        return cls(plan, plan.info())
+
+    @classmethod
+    def from_plan(cls, plan: Plan, device="cuda"):
+        """Wrap an already packed (and possibly already compiled) plan; uploads it."""
         plan.upload(device)
         return cls(plan, plan.info())
 
