@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "regtile", "jit"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time plain launches, no CUDA graph")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -259,19 +260,42 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_build = time.time() - t_build
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step(evs=None):
+    def step_on(st, evs=None):
         for i, d in enumerate(layers):
-            skc.skc_pad_input(d["conv"].plan, d["x"], d["xp"], per_gpu, stream)
+            skc.skc_pad_input(d["conv"].plan, d["x"], d["xp"], per_gpu, st)
             if evs is not None:
-                evs[2 * i + 1].record(stream)
-            skc.skc_sparse_conv_forward(d["conv"].plan, d["xp"], d["out"], per_gpu, stream)
+                evs[2 * i + 1].record(st)
+            skc.skc_sparse_conv_forward(d["conv"].plan, d["xp"], d["out"], per_gpu, st)
             if evs is not None:
-                evs[2 * i + 2].record(stream)
+                evs[2 * i + 2].record(st)
+
+    def step(evs=None):
+        step_on(stream, evs)
 
     clk = ClockSampler(local_rank).start()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+
+    # the step's 8 launches captured once in a CUDA graph (replayed per timed step: no
+    # host launch gaps between the kernels); per-layer times come from an uncaptured pass
+    graph = None
+    if not args.no_graph:
+        try:
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cap):
+                    step_on(cap)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            graph = g
+        except Exception as e:  # noqa: BLE001 -- report and time the plain launches
+            print(f"bench.py: CUDA graph capture failed ({e}); timing plain launches",
+                  file=sys.stderr)
+            graph = None
 
     nev = 2 * len(layers) + 1
     per_kernel = np.zeros(nev - 1)
@@ -289,6 +313,16 @@ def run_ours(args, cfg, rank, world, local_rank):
             ts = [evs[i].elapsed_time(evs[i + 1]) for i in range(nev - 1)]
             per_kernel += ts
             step_ms.append(evs[0].elapsed_time(evs[-1]))
+        if graph is not None:
+            step_ms = []
+            for _ in range(args.steps):
+                flush.fill_(1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                graph.replay()
+                b.record(stream)
+                torch.cuda.synchronize()
+                step_ms.append(a.elapsed_time(b))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -432,7 +466,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "global_batch": per_gpu * world, "per_gpu_batch": per_gpu,
                    "layers": [l.name for l in cfg.layers], "parallelism": f"dp{world} (batch-sharded, no collective)",
                    "l2": "flushed between timed steps (256 MiB write)", "kernel": args.kernel,
-                   "step": "per layer: skc_pad_input + skc_sparse_conv_forward"},
+                   "step": "per layer: skc_pad_input + skc_sparse_conv_forward"
+                           + (", the step's 8 launches replayed as one CUDA graph" if graph is not None else "")},
         "dense_equiv_gflops": step_dense_flops * world / (t_step * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                      "frac": achieved / peak_fp32, "traffic": tr,

@@ -71,7 +71,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 12;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 13;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -666,6 +666,9 @@ std::string emit_entry(const JitPlan &jp) {
     o("mul.wide.u32 %%rd10, %%r27, %%r40;");      // channel stride bytes
     o("mul.lo.u64 %%rd11, %%rd10, %d;", in.K);    // image stride bytes (canonical)
     o("selp.u64 %%rd12, 4, %%rd11, %%p6;");       // image B offset: 4 (interleaved) or K*Hop*Wop*4
+    // PDL: the next grid may be scheduled as our CTAs retire; the dry run below needs no data,
+    // so it overlaps the previous grid's tail; wait for the previous grid before the first item
+    o("griddepcontrol.launch_dependents;");
     if (jp.dry) {
         // Instruction prefetch: the code of a layer is cold in DRAM at launch and fetching it
         // is latency-bound per code stream.  Before the first item every CTA dry-runs a few
@@ -705,6 +708,7 @@ std::string emit_entry(const JitPlan &jp) {
         o("bra.uni $DRY_LOOP;");
         o("$DRY_DONE:");
     }
+    o("griddepcontrol.wait;");
     o("$ITEM:");
     o("setp.ge.u32 %%p0, %%r4, %%r32;");
     o("@%%p0 bra $EXIT;");
@@ -1536,20 +1540,32 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
                      jp->smem, per_sm);
     }
     cudaLaunchConfig_t lc{};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     lc.blockDim = dim3(unsigned(jp->NW * 32));
     lc.dynamicSmemBytes = jp->smem;
     lc.stream = st;
+    static const bool pdl = [] {
+        // off by default: measured no gain on the AlexNet step (profiles/r01_jit_order.txt)
+        const char *e = std::getenv("SKC_PDL");
+        return e && e[0] == '1';
+    }();
+    int nat = 0;
+    if (pdl) {
+        at[nat].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[nat].val.programmaticStreamSerializationAllowed = 1;
+        ++nat;
+    }
     if (cs > 1) {
         if (cs > 8)
             cudaFuncSetAttribute(reinterpret_cast<const void *>(jp->kern),
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = unsigned(cs);
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
+        at[nat].id = cudaLaunchAttributeClusterDimension;
+        at[nat].val.clusterDim.x = unsigned(cs);
+        at[nat].val.clusterDim.y = 1;
+        at[nat].val.clusterDim.z = 1;
+        ++nat;
         lc.attrs = at;
-        lc.numAttrs = 1;
+        lc.numAttrs = nat;
         lc.gridDim = dim3(unsigned(cs));
         int ncl = 0;
         if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void *>(jp->kern), &lc) != cudaSuccess || ncl < 1) {
@@ -1559,6 +1575,8 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
         grid = std::min<int64_t>((items + cs - 1) / cs, ncl) * cs;
     }
     lc.gridDim = dim3(unsigned(grid));
+    lc.attrs = at;
+    lc.numAttrs = nat;
     const float *bias = epi.bias;
     unsigned un = unsigned(N), relu = unsigned(epi.relu), opad = unsigned(epi.opad);
     unsigned olay = unsigned(epi.olay);

@@ -7,8 +7,19 @@
 #include "ptx.cuh"
 #include "skc_internal.h"
 
+#include <cstdlib>
+
 namespace skc {
 namespace {
+
+// Programmatic dependent launch (launched with the programmatic-serialization attribute):
+// wait until the preceding grid has completed and its writes are visible (this pass may read
+// the previous layer's output), then let the next grid's CTAs be scheduled as SMs free up.
+// Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_wait_and_trigger() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 constexpr int kPadVec = 4;    // outputs per vector (float4 store)
 constexpr int kPadUnroll = 4; // vectors per thread per iteration: 16 loads in flight
@@ -17,6 +28,7 @@ __global__ void __launch_bounds__(256) pad_kernel(const float *__restrict__ in,
                                                   float *__restrict__ out, int C, int H, int W,
                                                   int pad, int Wp, uint32_t per_img,
                                                   FastDiv div_plane, FastDiv div_wp, int vec4) {
+    pdl_wait_and_trigger();
     const int64_t n = blockIdx.y;
     const float *src = in + n * int64_t(C) * H * W;
     float *dst = out + n * int64_t(per_img);
@@ -95,6 +107,7 @@ __global__ void __launch_bounds__(256) pad_pairs_kernel(const float *__restrict_
                                                         int W, int pad, int Wp, uint32_t per_img,
                                                         FastDiv div_plane, FastDiv div_wp,
                                                         int has_b) {
+    pdl_wait_and_trigger();
     const int64_t p = blockIdx.y;
     const int64_t img = int64_t(C) * H * W;
     const float *srcA = in + 2 * p * img;
@@ -160,6 +173,31 @@ cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, 
     return cudaGetLastError();
 }
 
+namespace {
+// Launch with programmatic stream serialization (PDL) when SKC_PDL=1.
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    static const bool on = [] {
+        // off by default: measured no gain on the AlexNet step (profiles/r01_jit_order.txt)
+        const char *e = std::getenv("SKC_PDL");
+        return e && e[0] == '1';
+    }();
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute at[1];
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = 0;
+    lc.stream = st;
+    if (on) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...);
+}
+}  // namespace
+
 cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int W, int pad,
                        cudaStream_t st) {
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
@@ -170,10 +208,11 @@ cudaError_t launch_pad(const float *in, float *out, int64_t N, int C, int H, int
     for (int64_t n0 = 0; n0 < N; n0 += 65535) {
         const int64_t nn = (N - n0) < 65535 ? (N - n0) : 65535;
         const dim3 grid{static_cast<unsigned>(bx), static_cast<unsigned>(nn), 1u};
-        pad_kernel<<<grid, threads, 0, st>>>(in + n0 * int64_t(C) * H * W,
-                                             out + n0 * int64_t(per_img), C, H, W, pad, Wp,
-                                             per_img, make_fastdiv(uint32_t(Hp * Wp)),
-                                             make_fastdiv(uint32_t(Wp)), per_img % 4 == 0);
+        cudaError_t e = pdl_launch(pad_kernel, grid, dim3(threads), st,
+                                   in + n0 * int64_t(C) * H * W, out + n0 * int64_t(per_img), C,
+                                   H, W, pad, Wp, per_img, make_fastdiv(uint32_t(Hp * Wp)),
+                                   make_fastdiv(uint32_t(Wp)), int(per_img % 4 == 0));
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
@@ -192,10 +231,12 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
         // last pair: the kernel checks p + 1 < gridDim.y)
         const int has_b = (p0 + np < P) || (N % 2 == 0);
         const dim3 grid{static_cast<unsigned>(bx), static_cast<unsigned>(np), 1u};
-        pad_pairs_kernel<<<grid, threads, 0, st>>>(in + 2 * p0 * int64_t(C) * H * W,
-                                                   out + 2 * p0 * int64_t(per_img), C, H, W, pad,
-                                                   Wp, per_img, make_fastdiv(uint32_t(Hp * Wp)),
-                                                   make_fastdiv(uint32_t(Wp)), has_b);
+        cudaError_t e = pdl_launch(pad_pairs_kernel, grid, dim3(threads), st,
+                                   in + 2 * p0 * int64_t(C) * H * W,
+                                   out + 2 * p0 * int64_t(per_img), C, H, W, pad, Wp, per_img,
+                                   make_fastdiv(uint32_t(Hp * Wp)), make_fastdiv(uint32_t(Wp)),
+                                   int(has_b));
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
