@@ -116,3 +116,36 @@ def test_jit_unsupported_alignment_is_reported():
     assert e.value.status == -5
     plan = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups)
     assert plan.info()["kernel"] != skc.SKC_KERNEL_JIT
+
+
+def test_forward_into_geometry_errors():
+    """skc_sparse_conv_forward_into checks the next plan's geometry before anything else:
+    next C must be this K and next H x W this Ho x Wo (SKC_ERR_GEOMETRY otherwise)."""
+    rng = np.random.default_rng(9)
+    a = wl.Layer("a", 16, 8, 13, 13, 3, 3, 1, 1, 1, 0.5, 1.0)
+    b_ok = wl.Layer("b", 8, 16, 13, 13, 3, 3, 1, 1, 1, 0.5, 1.0)
+    b_bad_c = wl.Layer("c", 8, 12, 13, 13, 3, 3, 1, 1, 1, 0.5, 1.0)
+    b_bad_hw = wl.Layer("d", 8, 16, 12, 13, 3, 3, 1, 1, 1, 0.5, 1.0)
+    pa = skc.skc_pack_csr(wl.random_tensors(rng, a, 1)[0], 13, 13, 1, 1, 1)
+    for bad in (b_bad_c, b_bad_hw):
+        pb = skc.skc_pack_csr(wl.random_tensors(rng, bad, 1)[0], bad.H, bad.W, 1, 1, 1)
+        st = skc.lib().skc_sparse_conv_forward_into(pa.handle, 16, pb.handle, 16, 2, None, 0, None)
+        assert st == -2, st
+    pb = skc.skc_pack_csr(wl.random_tensors(rng, b_ok, 1)[0], 13, 13, 1, 1, 1)
+    # geometry fine, plan not uploaded -> SKC_ERR_STATE (no device work attempted)
+    st = skc.lib().skc_sparse_conv_forward_into(pa.handle, 16, pb.handle, 16, 2, None, 0, None)
+    assert st == -7, st
+
+
+def test_padded_shape_per_layout():
+    """The padded-input buffer shape follows the plan's layout: NCHW for direct plans,
+    [ceil(N/2)][C][Hp][Wp][2] for pair-layout JIT plans (odd N rounds up)."""
+    rng = np.random.default_rng(10)
+    layer = wl.Layer("p", 8, 16, 13, 13, 3, 3, 1, 1, 1, 0.5, 1.0)
+    w, _ = wl.random_tensors(rng, layer, 1)
+    d = skc.skc_pack_csr(w, 13, 13, 1, 1, 1, skc.SKC_KERNEL_DIRECT).info()
+    assert d["layout"] == skc.SKC_LAYOUT_NCHW and skc.padded_shape(d, 5) == (5, 16, 15, 15)
+    j = skc.skc_pack_csr(w, 13, 13, 1, 1, 1, skc.SKC_KERNEL_JIT).info()
+    if j["layout"] == skc.SKC_LAYOUT_PAIRS:
+        assert skc.padded_shape(j, 5) == (3, 16, 15, 15, 2)
+        assert skc.padded_shape(j, 6) == (3, 16, 15, 15, 2)
