@@ -446,7 +446,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "kernel_cfg": {k: d["conv"].plan.info()[k] for k in (
                 "kernel", "band_rows", "chunk_channels", "stages", "warps", "channels_per_warp",
                 "pixels_per_lane", "smem_bytes", "tile_h", "tile_w", "images_per_cta",
-                "jit_blocks", "code_bytes", "jit_compile_s", "jit_cache_hit")},
+                "jit_blocks", "jit_split", "code_bytes", "jit_compile_s", "jit_cache_hit")},
         })
     cpu = None
     if not args.no_cpu and world >= 1:

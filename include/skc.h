@@ -98,6 +98,7 @@ typedef struct {
     int layout;                    /* skc_layout of the padded input this plan reads      */
     int bands;                     /* JIT: row bands per image (pair), one CTA item each  */
     int jit_whole;                 /* JIT: 1 = one whole-program compile (no ABI calls)   */
+    int jit_split;                 /* JIT: even blocks per group split in halves (tail)   */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).
@@ -138,7 +139,11 @@ skc_status skc_plan_perm(const skc_plan *plan, const int32_t **perm);
 
 /* Copy the plan's kernel-private arrays into a caller-owned device workspace of at least
  * skc_info.device_bytes bytes (16-byte aligned), asynchronously on `stream`.  The host
- * arrays stay owned by the plan; the workspace must outlive every launch using the plan. */
+ * arrays stay owned by the plan; the workspace must outlive every launch using the plan.
+ * A JIT plan may keep a work-item counter in the workspace (skc_info.jit_split > 0: dynamic
+ * scheduling; the last CTA of a launch resets it): launches that use one workspace must not
+ * run concurrently -- issue them on one stream (or order them with events), or upload the
+ * plan into a second workspace for a concurrent stream. */
 skc_status skc_plan_upload(skc_plan *plan, void *d_workspace, size_t bytes, void *stream);
 
 /* a2 -- padded-input layout (R1): d_in [N][C][H][W] ->

@@ -42,6 +42,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <queue>
 #include <string>
 #include <sys/stat.h>
 #include <thread>
@@ -71,7 +72,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 13;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 14;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -117,7 +118,7 @@ struct JitPlan {
     int NB = 1;                  // row bands: a work item covers tile rows of one band
                                  // (lane table per band) -- pair mode on large images
     int plane = 0, img_stride = 0, stage_bytes = 0;
-    int off_bar = 0, off_cnt = 0, off_info = 0;
+    int off_bar = 0, off_cnt = 0, off_info = 0, off_item = 0;
     size_t smem = 0;
     int maxreg = 255;          // register cap of the block functions (NW warps per SM)
     int sync_every = 0;        // FMA instructions between CTA barriers in the code (0: none)
@@ -127,9 +128,16 @@ struct JitPlan {
     // first round, later rounds share one code stream chip-wide (profiles/r01_jit_order.txt)
     int order = 2;
     int dry = 1;               // 1: instruction prefetch by dry-running code segments at start
+    int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
+                               // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
     double code_instr = 0;     // modelled instructions of all blocks' code
-    int nbg = 0, nblocks = 0;  // blocks per group, total blocks
+    int nbg = 0, nblocks = 0;  // blocks per group (even partition), total blocks
+    // block b: conv group, first index into the group's nnz-sorted channels, channel count.
+    // Blocks are numbered longest-first; the last ones may be halves of an even block (tail
+    // split: the short items fill the last round of the persistent grid)
+    std::vector<int> bgrp, blo, bcnt;
+    int split = 0;             // even blocks (per group) split into halves
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
     std::vector<int32_t> chan; // [nblocks][M] original output channel or -1
@@ -160,6 +168,15 @@ void block_channels(const JitInput &in, int M, int g, int q, std::vector<int> &k
         const int idx = q * M + m;
         if (idx < in.Kg) ks.push_back(in.perm[size_t(g) * in.Kg + size_t(idx)]);
     }
+}
+
+// Block b of a plan (explicit partition, see JitPlan::bgrp).
+void plan_block_channels(const JitInput &in, const std::vector<int> &bgrp,
+                         const std::vector<int> &blo, const std::vector<int> &bcnt, int b,
+                         std::vector<int> &ks) {
+    ks.clear();
+    for (int m = 0; m < bcnt[size_t(b)]; ++m)
+        ks.push_back(in.perm[size_t(bgrp[size_t(b)]) * in.Kg + size_t(blo[size_t(b)] + m)]);
 }
 
 // A block's nonzeros per local input channel, in CSR order per output channel.
@@ -623,7 +640,7 @@ std::string emit_entry(const JitPlan &jp) {
       ".param .u32 p_olay)");
     o("{");
     o(".reg .pred %%p<8>;");
-    o(".reg .b32 %%r<56>;");
+    o(".reg .b32 %%r<64>;");
     o(".reg .b64 %%rd<24>;");
     o("ld.param.u64 %%rd0, [p_in];");
     o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -709,9 +726,75 @@ std::string emit_entry(const JitPlan &jp) {
         o("$DRY_DONE:");
     }
     o("griddepcontrol.wait;");
+    // dynamic scheduling: thread 0 takes the next item from a global counter in the plan
+    // workspace (after the lane tables); items are numbered longest-first, so CTAs that
+    // finish early take the short tail items.  The last CTA to exit resets the counters.
+    const int ctr_off = jp.NB * jp.NW * 32 * 16;
+    // A cluster takes CS consecutive items u .. u+CS-1 (rank r: item u + r), so the CTAs of a
+    // cluster (one TPC) run the same block's code side by side, as in the static order.
+    // Thread 0 of rank 0 fetches one cluster item ahead (the atomic's latency overlaps the
+    // current item) and writes u into every rank's slot (two slots, alternating); a cluster
+    // barrier publishes it.  u >= items ends every rank of the cluster together.
+    // dyn 1: every CTA fetches its own items; dyn 2: per cluster (see above).  The first
+    // item is the static one (t = cluster item * CS + rank); the counter numbers the items
+    // after the first round (fetched value + grid size G).
+    const bool cl = jp.dyn == 2;
+    if (jp.dyn) {
+        o("add.u64 %%rd20, %%rd2, %d;", ctr_off);
+        o("mov.u32 %%r58, 0;");                        // slot parity
+        o("mov.u32 %%r60, 1;");                        // first item
+        o("setp.eq.u32 %%p0, %%r3, 0;");
+        if (cl) o("setp.eq.and.u32 %%p0, %%r35, 0, %%p0;");
+        o("@%%p0 atom.global.add.u32 %%r56, [%%rd20], %s;", cl ? "%r36" : "1");
+    }
     o("$ITEM:");
-    o("setp.ge.u32 %%p0, %%r4, %%r32;");
-    o("@%%p0 bra $EXIT;");
+    if (jp.dyn) {
+        o("mad.lo.u32 %%r57, %%r58, 4, %%r11;");
+        o("add.u32 %%r57, %%r57, %d;", jp.off_item);   // this item's slot
+        o("xor.b32 %%r58, %%r58, 1;");
+        o("setp.ne.u32 %%p0, %%r3, 0;");
+        if (cl) o("setp.ne.or.u32 %%p0, %%r35, 0, %%p0;");
+        o("setp.ne.or.u32 %%p0, %%r60, 0, %%p0;");
+        o("@%%p0 bra $FETCHED;");
+        o("add.u32 %%r61, %%r56, %%r31;");
+        o("st.shared.u32 [%%r57], %%r61;");
+        if (cl) {
+            o("mov.u32 %%r59, 1;");
+            o("$PEERS:");
+            o("setp.ge.u32 %%p1, %%r59, %%r36;");
+            o("@%%p1 bra $PEERS_DONE;");
+            o("mapa.shared::cluster.u32 %%r54, %%r57, %%r59;");
+            o("st.shared::cluster.u32 [%%r54], %%r61;");
+            o("add.u32 %%r59, %%r59, 1;");
+            o("bra.uni $PEERS;");
+            o("$PEERS_DONE:");
+        }
+        o("atom.global.add.u32 %%r56, [%%rd20], %s;", cl ? "%r36" : "1");
+        o("$FETCHED:");
+        if (cl) {
+            o("barrier.cluster.arrive.release;");
+            o("barrier.cluster.wait.acquire;");
+        } else {
+            o("bar.sync 0;");
+        }
+        o("setp.eq.u32 %%p1, %%r60, 0;");
+        o("@%%p1 ld.shared.u32 %%r4, [%%r57];");
+        if (cl) o("@%%p1 add.u32 %%r4, %%r4, %%r35;");   // t = u + rank
+        o("mov.u32 %%r60, 0;");
+        if (cl) {
+            o("sub.u32 %%r54, %%r4, %%r35;");            // u
+            o("setp.ge.u32 %%p0, %%r54, %%r32;");
+            o("@%%p0 bra $EXIT;");                       // the whole cluster ends
+            o("setp.ge.u32 %%p0, %%r4, %%r32;");
+            o("@%%p0 bra $NEXT;");                       // past the end: idle, stay in step
+        } else {
+            o("setp.ge.u32 %%p0, %%r4, %%r32;");
+            o("@%%p0 bra $EXIT;");
+        }
+    } else {
+        o("setp.ge.u32 %%p0, %%r4, %%r32;");
+        o("@%%p0 bra $EXIT;");
+    }
     if (jp.order == 1) {
         // spread: consecutive items are different blocks (every block's code is fetched
         // in parallel from the first round on)
@@ -759,8 +842,14 @@ std::string emit_entry(const JitPlan &jp) {
     o("min.u32 %%r9, %%r9, %d;", jp.NI);        // images in this item
     o("add.u32 %%r41, %%r9, %d;", sw - 1);
     o("shr.u32 %%r41, %%r41, %d;", sw - 1);      // slots in this item
-    o("div.u32 %%r10, %%r7, %d;", jp.nbg);      // conv group
-    o("bar.sync 0;");                            // every warp is done with the previous item
+    o("mov.u32 %%r10, 0;");                      // conv group of the block
+    for (int b = 0; b < jp.nblocks; ++b)
+        if (jp.bgrp[size_t(b)] != 0) {
+            o("setp.eq.u32 %%p3, %%r7, %d;", b);
+            o("@%%p3 mov.u32 %%r10, %d;", jp.bgrp[size_t(b)]);
+        }
+    if (!jp.dyn) o("bar.sync 0;");               // every warp is done with the previous item
+                                                 // (dynamic: the fetch barrier already is)
     o("setp.ne.u32 %%p0, %%r3, 0;");
     o("@%%p0 bra $INIT_DONE;");
     // barriers of the previous item have completed every phase and have no pending
@@ -865,9 +954,22 @@ std::string emit_entry(const JitPlan &jp) {
         o("bra.uni $NEXT;");
     }
     o("$NEXT:");
-    o("add.u32 %%r4, %%r4, %%r31;");
+    if (!jp.dyn) o("add.u32 %%r4, %%r4, %%r31;");
     o("bra.uni $ITEM;");
     o("$EXIT:");
+    if (jp.dyn) {
+        o("setp.ne.u32 %%p0, %%r3, 0;");
+        o("@%%p0 bra $DONE;");
+        o("fence.acq_rel.gpu;");          // our item fetches are performed before `done`
+        o("atom.global.add.u32 %%r57, [%%rd20+4], 1;");
+        o("mov.u32 %%r56, %%nctaid.x;");
+        o("sub.u32 %%r56, %%r56, 1;");
+        o("setp.ne.u32 %%p0, %%r57, %%r56;");
+        o("@%%p0 bra $DONE;");
+        o("st.global.u32 [%%rd20], 0;");   // every CTA has taken its last item: reset
+        o("st.global.u32 [%%rd20+4], 0;");
+        o("$DONE:");
+    }
     o("ret;");
     o("}");
     return std::move(o.s);
@@ -963,7 +1065,7 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
         for (int m = 0; m < jp->M; ++m) {
             const int k = jp->chan[size_t(b) * jp->M + m];
             if (k < 0) continue;
-            if (k >= in.K || k / in.Kg != b / jp->nbg) return bad("channel in the wrong block");
+            if (k >= in.K || k / in.Kg != jp->bgrp[size_t(b)]) return bad("channel in the wrong block");
             ++seen[size_t(k)];
         }
     for (int k = 0; k < in.K; ++k)
@@ -996,7 +1098,7 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
     std::vector<int> ks;
     std::vector<std::vector<JNz>> per_c;
     for (int b = 0; b < jp->nblocks; ++b) {
-        block_channels(in, jp->M, b / jp->nbg, b % jp->nbg, ks);
+        plan_block_channels(in, jp->bgrp, jp->blo, jp->bcnt, b, ks);
         block_nz(in, ks, per_c);
         const std::string code = emit_block(*jp, b, ks, per_c);
         const int Mb = int(ks.size());
@@ -1121,6 +1223,119 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
 // ---------------------------------------------------------------------------------------
 // public (library-internal) interface
 // ---------------------------------------------------------------------------------------
+// Block partition.  The even partition (nbg blocks of M channels per group) gives items of
+// equal length, so a batch whose item count is not a multiple of the persistent grid leaves a
+// partly filled last round (conv5 at N=256: 344 items on 148 CTAs, 2.32 rounds -> 3).  With
+// dynamic scheduling, splitting the last `split` blocks of every group into halves puts short
+// items at the end of the queue where they fill that round.  `split` minimises the makespan
+// of a list-scheduling simulation of the item queue at the hint batch (per-item time from the
+// same model as the configuration cost; SKC_JIT_SPLIT forces it).
+namespace {
+double item_time(const JitPlan &jp, double instr) {
+    return instr * std::max(kFetchInv, jp.NW / kIssue) + kItemCycles;
+}
+
+// item t -> block, the mapping emit_entry generates for jp.order (G = grid size)
+int item_block(const JitPlan &jp, int64_t t, int64_t nig, int64_t G) {
+    const int64_t nb = jp.nblocks;
+    if (jp.order == 1) return int(t % nb);
+    if (jp.order == 2) {
+        const int64_t F = std::min<int64_t>(G / nb, nig);
+        if (t < F * nb) return int(t % nb);
+        return int((t - F * nb) / (nig - F));
+    }
+    return int(t / nig);
+}
+
+double simulate_makespan(const JitPlan &jp, const std::vector<double> &tb, int64_t nig, int64_t P) {
+    const int64_t items = nig * jp.nblocks;
+    std::priority_queue<double, std::vector<double>, std::greater<double>> free_at;
+    for (int64_t i = 0; i < std::min(P, items); ++i) free_at.push(0.0);
+    double span = 0;
+    for (int64_t t = 0; t < items; ++t) {
+        const double s0 = free_at.top();
+        free_at.pop();
+        const double e = s0 + tb[size_t(item_block(jp, t, nig, P))];
+        span = std::max(span, e);
+        free_at.push(e);
+    }
+    return span;
+}
+
+void choose_blocks(JitPlan &jp, int n_hint) {
+    const JitInput &in = jp.in;
+    const int Mp = jp.M;
+    int force = -1;
+    if (const char *e = std::getenv("SKC_JIT_SPLIT")) force = std::atoi(e);
+    // resident CTAs per SM (shared memory, registers, threads)
+    const int per_sm = std::max(1, std::min({int(233472 / (jp.smem + 1024)),
+                                             65536 / (jp.NW * 32 * jp.maxreg),
+                                             2048 / (jp.NW * 32)}));
+    const int64_t P = int64_t(kSMs) * per_sm;
+    const int64_t nig = int64_t((n_hint + jp.NI - 1) / jp.NI) * jp.NB;
+    std::vector<int> ks;
+    std::vector<std::vector<JNz>> per_c;
+    Need nd;
+    struct Blk { int g, lo, cnt; double instr; };
+    auto instr_of = [&](int g, int lo, int cnt) {
+        std::vector<int> bg{g}, bl{lo}, bc{cnt};
+        plan_block_channels(in, bg, bl, bc, 0, ks);
+        block_nz(in, ks, per_c);
+        return block_instr(in, per_c, jp.TY, jp.TX, jp.PX, jp.pair, jp.CB, cnt, nd);
+    };
+    double best_span = 0;
+    std::vector<Blk> best;
+    const int smax = jp.dyn ? jp.nbg : 0;
+    for (int sp = 0; sp <= smax; ++sp) {
+        if (force >= 0 && sp != std::min(force, smax)) continue;
+        std::vector<Blk> full, tail;
+        for (int g = 0; g < in.groups; ++g)
+            for (int q = 0; q < jp.nbg; ++q) {
+                const int lo = q * Mp, cnt = std::min(Mp, in.Kg - lo);
+                if (cnt <= 0) continue;
+                if (q >= jp.nbg - sp && cnt >= 2) {
+                    const int c1 = (cnt + 1) / 2;
+                    tail.push_back({g, lo, c1, instr_of(g, lo, c1)});
+                    tail.push_back({g, lo + c1, cnt - c1, instr_of(g, lo + c1, cnt - c1)});
+                } else {
+                    full.push_back({g, lo, cnt, instr_of(g, lo, cnt)});
+                }
+            }
+        std::vector<Blk> blks = full;
+        blks.insert(blks.end(), tail.begin(), tail.end());
+        std::stable_sort(blks.begin(), blks.end(),
+                         [](const Blk &a, const Blk &b) { return a.instr > b.instr; });
+        std::vector<double> tb;
+        for (const Blk &b : blks) tb.push_back(item_time(jp, b.instr));
+        jp.nblocks = int(blks.size());
+        const double span = simulate_makespan(jp, tb, nig, P);
+        if (std::getenv("SKC_JIT_DEBUG"))
+            std::fprintf(stderr, "skc jit: split %d blocks %d P %lld nig %lld span %.0f ideal %.0f\n", sp,
+                         jp.nblocks, (long long)P, (long long)nig, span,
+                         [&] { double t = 0; for (double x : tb) t += x; return t * nig / P; }());
+        // a split must gain at least 1% (its halves repeat the window loads)
+        if (best.empty() || span < best_span * 0.99) {
+            best_span = span;
+            best = blks;
+            jp.split = sp;
+        }
+    }
+    // dynamic scheduling only where it splits: with equal items the static order measured
+    // as fast or faster (conv3 -2.5%: it keeps the CTAs of a TPC on the same code)
+    if (jp.split == 0 && !std::getenv("SKC_JIT_DYN")) jp.dyn = 0;
+    jp.nblocks = int(best.size());
+    jp.bgrp.clear(); jp.blo.clear(); jp.bcnt.clear();
+    double instr = 0;
+    for (const Blk &b : best) {
+        jp.bgrp.push_back(b.g);
+        jp.blo.push_back(b.lo);
+        jp.bcnt.push_back(b.cnt);
+        instr += b.instr;
+    }
+    jp.code_instr = instr;
+}
+}  // namespace
+
 int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *msg) {
     *out = nullptr;
     const int plane = in.Hp * in.Wp;
@@ -1309,24 +1524,25 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.off_cnt = jp.off_bar + 8 * kMaxStages;
     jp.off_info = jp.off_cnt + 4 * kMaxStages;
     jp.off_info = (jp.off_info + 7) / 8 * 8;
-    jp.smem = size_t(jp.off_info) + size_t(NSL) * 8;
+    jp.off_item = jp.off_info + NSL * 8;
+    jp.smem = size_t(jp.off_item) + 8;
     jp.maxreg = reg_cap(jp.NW);
     if (const char *e = std::getenv("SKC_JIT_SYNC")) jp.sync_every = std::max(0, std::atoi(e));
     if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_DYN")) jp.dyn = std::max(0, std::min(2, std::atoi(e)));
     // whole-program compile (one serial ptxas run, ~10-20 s per 100k instructions) when the
     // code is moderate; parallel per-block modules otherwise (their calls pay an ABI
     // save/restore of callee-saved registers: -8-10% measured, profiles/r01_jit_whole.txt)
+    choose_blocks(jp, n_hint);
     jp.whole = jp.code_instr <= kWholeMaxInstr ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
-    for (int g = 0; g < in.groups; ++g)
-        for (int q = 0; q < jp.nbg; ++q) {
-            block_channels(in, jp.M, g, q, ks);
-            for (size_t m = 0; m < ks.size(); ++m)
-                jp.chan[size_t(g * jp.nbg + q) * jp.M + m] = ks[m];
-        }
+    for (int b = 0; b < jp.nblocks; ++b) {
+        plan_block_channels(in, jp.bgrp, jp.blo, jp.bcnt, b, ks);
+        for (size_t m = 0; m < ks.size(); ++m) jp.chan[size_t(b) * jp.M + m] = ks[m];
+    }
     *out = best.release();
     return SKC_OK;
 }
@@ -1342,8 +1558,7 @@ int jit_compile(JitPlan *jp, std::string *msg) {
         std::vector<int> ks;
         std::vector<std::vector<JNz>> per_c;
         for (int b = 0; b < jp->nblocks; ++b) {
-            const int g = b / jp->nbg, q = b % jp->nbg;
-            block_channels(in, jp->M, g, q, ks);
+            plan_block_channels(in, jp->bgrp, jp->blo, jp->bcnt, b, ks);
             block_nz(in, ks, per_c);
             mods[size_t(b)] = emit_block(*jp, b, ks, per_c);
         }
@@ -1462,12 +1677,13 @@ int jit_compile(JitPlan *jp, std::string *msg) {
     return SKC_OK;
 }
 
-size_t jit_lanemap_bytes(const JitPlan *jp) { return jp->lanemap.size() * 4; }
+// device image: the lane tables, then 16 bytes of (zeroed) scheduling counters
+size_t jit_lanemap_bytes(const JitPlan *jp) { return jp->lanemap.size() * 4 + 16; }
 const void *jit_lanemap(const JitPlan *jp) { return jp->lanemap.data(); }
 
 void jit_info(const JitPlan *jp, JitInfo *o) {
     o->TY = jp->TY; o->TX = jp->TX; o->PX = jp->PX; o->M = jp->M; o->NW = jp->NW;
-    o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks;
+    o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks; o->split = jp->split;
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;

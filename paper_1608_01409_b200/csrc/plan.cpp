@@ -763,8 +763,8 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
         const int r = jit_configure(ji, max_ni == 1 ? 1 : 64, &p->jit, &msg);
         if (r == SKC_OK) {
             p->kernel = SKC_KERNEL_JIT;
-            p->image.resize(jit_lanemap_bytes(p->jit));
-            std::memcpy(p->image.data(), jit_lanemap(p->jit), p->image.size());
+            p->image.assign(jit_lanemap_bytes(p->jit), 0);   // lane tables + zeroed counters
+            std::memcpy(p->image.data(), jit_lanemap(p->jit), jit_lanemap_bytes(p->jit) - 16);
             p->off_lanemap = 0;
             JitInfo ji2{};
             jit_info(p->jit, &ji2);
@@ -873,6 +873,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.layout = p->layout;
     i.bands = 0;
     i.jit_whole = 0;
+    i.jit_split = 0;
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -884,6 +885,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
         i.model_instr_per_image = j.cost;
         i.bands = j.bands;
         i.jit_whole = j.whole;
+        i.jit_split = j.split;
     }
     return ok();
 }

@@ -119,6 +119,7 @@ struct JitInfo {
     int pair;  // 1: the plan reads the image-pair interleaved padded layout
     int bands; // row bands per image (pair) -- work items per image group
     int whole; // 1: compiled as one whole program
+    int split; // even blocks per group split into halves
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).

@@ -100,7 +100,7 @@ def main():
                        speedup_vs_direct=ms_ref / ms, bitwise_equal_direct=same, ndiff=ndiff,
                        build_s=t_build, cfg={k: inf[k] for k in (
                            "tile_h", "tile_w", "channels_per_warp", "warps", "images_per_cta",
-                           "chunk_channels", "stages", "smem_bytes", "jit_blocks", "code_bytes",
+                           "chunk_channels", "stages", "smem_bytes", "jit_blocks", "jit_split", "code_bytes",
                            "jit_compile_s", "jit_cache_hit", "model_instr_per_image", "layout")})
             lines.append(rec)
             print(json.dumps(rec), flush=True)
