@@ -68,6 +68,9 @@ constexpr double kIssue = 1.6;
 // profiles/r01_jit_cfg_sweep.jsonl
 constexpr double kItemCycles = 4000.0;
 constexpr int kSMs = 148;
+// position-major code keeps few window positions live: registers the configuration reserves
+// for them (pair layout; profiles/r01_jit_pmajor.txt)
+constexpr int kPmajorWregs = 8;
 double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
@@ -128,6 +131,7 @@ struct JitPlan {
     // first round, later rounds share one code stream chip-wide (profiles/r01_jit_order.txt)
     int order = 2;
     int dry = 1;               // 1: instruction prefetch by dry-running code segments at start
+    int pmajor = 1;            // 1: position-major FMA order within a channel (pair layout)
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
@@ -479,6 +483,24 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             window_need(nz, TY, TX, PX, st, WRw, WCw, pm, nd);
             const int cbase = cl * jp.plane;
             auto off = [&](int u) { return (cbase + (u / WCw) * in.Wp + (u % WCw)) * 4 * sw; };
+            if (pm && jp.pmajor) {
+                // position-major: load window position u, then every FMA reading it (per
+                // accumulator the (r, s) order is unchanged: u grows with (r, s) for a fixed
+                // pixel), so only a few window registers are live
+                for (int u : nd.pairs) {
+                    o("ld.volatile.shared.b64 %%wp%d, [%%rb%d+%d];", u, s, off(u));
+                    for (const JNz &z : nz)
+                        for (int ty = 0; ty < TY; ++ty)
+                            for (int tx = 0; tx < TX; ++tx) {
+                                if ((ty * st + z.r) * WCw + tx * st + z.s != u) continue;
+                                const uint32_t wb = fbits(z.w);
+                                const int a = z.m * NPT + ty * TX + tx;
+                                o("mov.b64 %%wt, 0x%08X%08X;", wb, wb);
+                                o("fma.rn.f32x2 %%a%d, %%wt, %%wp%d, %%a%d;", a, u, a);
+                            }
+                }
+                continue;
+            }
             if (pm) {
                 // one aligned 8-byte load = the same input element of images A and B
                 for (int u : nd.pairs) o("ld.volatile.shared.b64 %%wp%d, [%%rb%d+%d];", u, s, off(u));
@@ -1350,6 +1372,10 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     };
     int pair_force = -1;  // SKC_JIT_PAIR=0/1 (tuning): canonical or image-pair layout only
     int band_force = 0;   // SKC_JIT_BANDS=n (tuning)
+    int pmajor = 1;       // SKC_JIT_PMAJOR: position-major code (few live window registers)
+    int wr_cap = kPmajorWregs;  // SKC_JIT_WREGS: window registers assumed live (position-major)
+    if (const char *e = std::getenv("SKC_JIT_PMAJOR")) pmajor = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_WREGS")) wr_cap = std::atoi(e);
     // staging pipeline: bytes per stage and stages (SKC_JIT_STAGE_KB, SKC_JIT_NS: tuning)
     int stage_target = kStageTarget, ns_max = 3;
     if (const char *e = std::getenv("SKC_JIT_STAGE_KB")) stage_target = std::max(4, std::atoi(e)) * 1024;
@@ -1392,7 +1418,8 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     const int T = TY * TX;
                     if (TY > in.Ho || TX > in.Wo || T > (pm ? 31 : 32) || T < (pm ? 1 : 2)) continue;
                     const int PX = pm ? 0 : TX / 2;
-                    const int wr = window_regs(TY, TX, PX, in.R, in.S, in.stride, pm);
+                    int wr = window_regs(TY, TX, PX, in.R, in.S, in.stride, pm);
+                    if (pm && pmajor && wr_cap > 0) wr = std::min(wr, wr_cap);
                     int M = (reg_budget - wr - 12) / (T * (pm ? 2 : 1));
                     if (fm > 0) M = fm;
                     M = std::min(M, in.Kg);
@@ -1424,7 +1451,14 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     const int NI = NSL * sw;
                     const int NW = (NSL * tpi + 31) / 32;
                     if (NW > nw_max) continue;
-                    const int nbg = (in.Kg + M - 1) / M;
+                    // one or two more blocks than the registers need: smaller items, a
+                    // different fill of the last round
+                    const int M0 = M, CB0 = CB, NS0 = NS, IS0c = IS, stage0 = stage;
+                    for (int xb = 0; xb <= 2; ++xb) {
+                    const int nbg0 = (in.Kg + M0 - 1) / M0;
+                    const int nbg = nbg0 + xb;
+                    if (nbg > in.Kg || (xb > 0 && fm > 0)) continue;
+                    int M = M0, CB = CB0, NS = NS0, IS = IS0c, stage = stage0;
                     // even blocks: M' = ceil(Kg / nbg) <= M (no small leftover block paying a
                     // full set of window loads for a few channels)
                     if (fm <= 0) M = (in.Kg + nbg - 1) / nbg;
@@ -1465,7 +1499,17 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                             }
                         }
                     }
-                    const double cost = instr * share + double(nbg * in.groups) / NIe * kItemCycles;
+                    // whole rounds of the persistent grid at the hint batch: items are equal
+                    // (even blocks), so a partly filled last round costs a full one
+                    // (profiles/r01_jit_pmajor.txt: conv3 M=43 in 2.61 rounds is slower than
+                    // M=39 in 2.9)
+                    const double per_img = instr * share + double(nbg * in.groups) / NIe * kItemCycles;
+                    const int per_sm = std::max(1, std::min({int(233472 / (smem + 1024 + 256)),
+                                                             65536 / (NW * 32 * reg_cap(nw_max)),
+                                                             2048 / (NW * 32)}));
+                    const double items = double(nbg) * in.groups * nig;
+                    const double P = double(kSMs) * per_sm;
+                    const double cost = per_img * (std::ceil(items / P) * P / items);
                     if (best && cost >= best->cost) continue;
                     std::unique_ptr<JitPlan> jp(new JitPlan());
                     jp->in = in;
@@ -1479,6 +1523,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     jp->cost = cost;
                     jp->code_instr = instr;
                     best = std::move(jp);
+                    }  // xb
                     }  // NB
                 }
         }
@@ -1531,6 +1576,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_PMAJOR")) jp.pmajor = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_DYN")) jp.dyn = std::max(0, std::min(2, std::atoi(e)));
     // whole-program compile (one serial ptxas run, ~10-20 s per 100k instructions) when the
     // code is moderate; parallel per-block modules otherwise (their calls pay an ABI
