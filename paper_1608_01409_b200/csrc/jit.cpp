@@ -75,18 +75,26 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 14;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 15;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
     std::string s;
     void operator()(const char *fmt, ...) __attribute__((format(printf, 2, 3))) {
-        char buf[320];
+        char buf[512];
         va_list ap;
         va_start(ap, fmt);
         const int n = vsnprintf(buf, sizeof buf, fmt, ap);
         va_end(ap);
-        s.append(buf, size_t(std::max(0, std::min<int>(n, int(sizeof buf) - 1))));
+        if (n >= int(sizeof buf)) {  // long line (e.g. a parameter list): format again
+            std::vector<char> big(size_t(n) + 1);
+            va_start(ap, fmt);
+            vsnprintf(big.data(), big.size(), fmt, ap);
+            va_end(ap);
+            s.append(big.data(), size_t(n));
+        } else {
+            s.append(buf, size_t(std::max(0, n)));
+        }
         s.push_back('\n');
     }
 };
@@ -132,6 +140,10 @@ struct JitPlan {
     int order = 2;
     int dry = 1;               // 1: instruction prefetch by dry-running code segments at start
     int pmajor = 1;            // 1: position-major FMA order within a channel (pair layout)
+    // 1: an item's last chunks stage the next item's first chunks (rotated stages, barriers
+    // live across items).  Measured -1..-2% on conv3/4 (profiles/r01_jit_xpf.txt): the item
+    // start was not waiting on its first stage; off by default
+    int xpf = 0;
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
@@ -390,11 +402,15 @@ const char *kHdr = ".version 8.8\n.target sm_100a\n.address_size 64\n";
 // mask (bit 31: image B valid, pair mode), slots in this item, bias, relu, output row /
 // channel / pixel strides, byte offset of image B's output from image A's, dry-run chunk
 // (0: a real run; k + 1: execute only chunk k's code, no waits, no stores -- instruction
-// prefetch, see emit_entry)
+// prefetch, see emit_entry), stage phase/rotation (bits 0-7: parity base of logical stage s,
+// bits 8-15: rotation -- logical stage s is physical stage (s + rot) % NS), smem offsets of
+// this item's and the next item's slot-source tables, the next item's slot count (0: none;
+// else the last chunks' releases stage the next item's first chunks)
 const char *kBlkParams =
     "(.param .b32 q_lb, .param .b32 q_sm, .param .b64 q_out, .param .b32 q_mask, "
     ".param .b32 q_nsl, .param .b64 q_bias, .param .b32 q_relu, .param .b32 q_rs, "
-    ".param .b64 q_cs, .param .b32 q_ps, .param .b64 q_bo, .param .b32 q_dry)";
+    ".param .b64 q_cs, .param .b32 q_ps, .param .b64 q_bo, .param .b32 q_dry, "
+    ".param .b32 q_ph, .param .b32 q_info, .param .b32 q_ninfo, .param .b32 q_nnsl)";
 
 int chunk_channels(const JitPlan &jp, int i) { return std::min(jp.CB, jp.in.Cg - i * jp.CB); }
 
@@ -416,9 +432,12 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o(".visible .func skc_b%d%s", b, kBlkParams);
     o("{");
     o(".reg .pred %%p<10>;");
-    o(".reg .b32 %%r<24>;");
+    o(".reg .b32 %%r<32>;");
     o(".reg .b64 %%rd<12>;");
     o(".reg .b32 %%rb<%d>;", jp.NS);
+    o(".reg .b32 %%rs<%d>;", jp.NS);
+    o(".reg .b32 %%rw<%d>;", jp.NS);
+    o(".reg .b32 %%rq<%d>;", 2 * jp.NS);
     o(".reg .b64 %%a<%d>;", std::max(1, Mb * NPT));
     o(".reg .f32 %%f<%d>;", std::max(1, Mb * NST));
     o(".reg .f32 %%wl<%d>;", NWIN);
@@ -444,8 +463,25 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o("mov.u32 %%r8, 1;");
     // activations stream through L2 (evict first) so the straight-line code stays resident
     if (jp.l2hint) o("createpolicy.fractional.L2::evict_first.b64 %%rd10, 1.0;");
-    o("add.u32 %%rb0, %%r1, %%r0;");
-    for (int s = 1; s < jp.NS; ++s) o("add.u32 %%rb%d, %%rb0, %d;", s, s * jp.stage_bytes);
+    // logical stage s = physical stage (s + rot) % NS: stage base (rs), lane base (rb),
+    // barrier (rw), wait parities (rq: base, base ^ 1)
+    o("ld.param.b32 %%r18, [q_ph];");
+    o("ld.param.b32 %%r19, [q_info];");
+    o("add.u32 %%r19, %%r19, %%r1;");
+    o("ld.param.b32 %%r20, [q_ninfo];");
+    o("add.u32 %%r20, %%r20, %%r1;");
+    o("ld.param.b32 %%r21, [q_nnsl];");
+    o("bfe.u32 %%r22, %%r18, 8, 8;");
+    for (int s = 0; s < jp.NS; ++s) {
+        o("add.u32 %%r23, %%r22, %d;", s);
+        o("rem.u32 %%r23, %%r23, %d;", jp.NS);
+        o("mad.lo.u32 %%rs%d, %%r23, %d, %%r1;", s, jp.stage_bytes);
+        o("add.u32 %%rb%d, %%rs%d, %%r0;", s, s);
+        o("mad.lo.u32 %%rw%d, %%r23, 8, %%r1;", s);
+        o("add.u32 %%rw%d, %%rw%d, %d;", s, s, jp.off_bar);
+        o("bfe.u32 %%rq%d, %%r18, %d, 1;", 2 * s, s);
+        o("xor.b32 %%rq%d, %%rq%d, 1;", 2 * s + 1, 2 * s);
+    }
     for (int i = 0; i < Mb * NPT; ++i) o("mov.b64 %%a%d, 0;", i);
     for (int i = 0; i < Mb * NST; ++i) o("mov.f32 %%f%d, 0f00000000;", i);
     // dry run: jump straight to chunk k's code (no barrier wait), return after it
@@ -465,8 +501,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         const int s = i % jp.NS;
         const int par = (i / jp.NS) & 1;
         o("$W%d:", i);
-        o("mbarrier.try_wait.parity.shared::cta.b64 %%p4, [%%r1+%d], %%r%d;", jp.off_bar + 8 * s,
-          par ? 8 : 7);
+        o("mbarrier.try_wait.parity.shared::cta.b64 %%p4, [%%rw%d], %%rq%d;", s, 2 * s + par);
         o("@!%%p4 bra $W%d;", i);
         o("$B%d:", i);
         const int cn = chunk_channels(jp, i);
@@ -559,17 +594,16 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             o("setp.ne.u32 %%p5, %%r10, %d;", jp.NW * (i / jp.NS + 1) - 1);
             o("@%%p5 bra $R%d;", i);
             o("fence.proxy.async.shared::cta;");
-            o("add.u32 %%r15, %%r1, %d;", jp.off_bar + 8 * s);
+            o("mov.u32 %%r15, %%rw%d;", s);
             o("mul.lo.u32 %%r11, %%r3, %d;", bytes);
             o("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%%r15], %%r11;");
             o("mov.u32 %%r12, 0;");
             o("$L%d:", i);
             o("shl.b32 %%r13, %%r12, 3;");
-            o("add.u32 %%r13, %%r13, %%r1;");
-            o("ld.shared.u64 %%rd6, [%%r13+%d];", jp.off_info);
+            o("add.u32 %%r13, %%r13, %%r19;");
+            o("ld.shared.u64 %%rd6, [%%r13];");
             o("add.u64 %%rd6, %%rd6, %lld;", (long long)nxt * jp.CB * jp.plane * 4 * sw);
-            o("mad.lo.u32 %%r14, %%r12, %d, %%r1;", jp.img_stride * 4);
-            o("add.u32 %%r14, %%r14, %d;", s * jp.stage_bytes);
+            o("mad.lo.u32 %%r14, %%r12, %d, %%rs%d;", jp.img_stride * 4, s);
             if (jp.l2hint)
                 o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
                   "[%%r14], [%%rd6], %d, [%%r15], %%rd10;", bytes);
@@ -579,6 +613,41 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             o("add.u32 %%r12, %%r12, 1;");
             o("setp.lt.u32 %%p6, %%r12, %%r3;");
             o("@%%p6 bra $L%d;", i);
+            o("$R%d:", i);
+        } else if (jp.xpf) {
+            // the stage's last use in this item: the last warp out stages the NEXT item's
+            // chunk i + NS - nchunks into it (same physical stage by the rotation), so the
+            // next item starts on data already in shared memory
+            const int nxt = i + jp.NS - jp.nchunks;
+            const int bytes = chunk_channels(jp, nxt) * jp.plane * 4 * sw;
+            o("bar.warp.sync -1;");
+            o("@!%%p0 bra $R%d;", i);
+            o("fence.acq_rel.cta;");
+            o("atom.shared.add.u32 %%r10, [%%r1+%d], 1;", jp.off_cnt + 4 * s);
+            o("setp.ne.u32 %%p5, %%r10, %d;", jp.NW * (i / jp.NS + 1) - 1);
+            o("@%%p5 bra $R%d;", i);
+            o("setp.eq.u32 %%p5, %%r21, 0;");
+            o("@%%p5 bra $R%d;", i);
+            o("fence.proxy.async.shared::cta;");
+            o("mov.u32 %%r15, %%rw%d;", s);
+            o("mul.lo.u32 %%r11, %%r21, %d;", bytes);
+            o("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%%r15], %%r11;");
+            o("mov.u32 %%r12, 0;");
+            o("$LN%d:", i);
+            o("shl.b32 %%r13, %%r12, 3;");
+            o("add.u32 %%r13, %%r13, %%r20;");
+            o("ld.shared.u64 %%rd6, [%%r13];");
+            o("add.u64 %%rd6, %%rd6, %lld;", (long long)nxt * jp.CB * jp.plane * 4 * sw);
+            o("mad.lo.u32 %%r14, %%r12, %d, %%rs%d;", jp.img_stride * 4, s);
+            if (jp.l2hint)
+                o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+                  "[%%r14], [%%rd6], %d, [%%r15], %%rd10;", bytes);
+            else
+                o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%%r14], [%%rd6], "
+                  "%d, [%%r15];", bytes);
+            o("add.u32 %%r12, %%r12, 1;");
+            o("setp.lt.u32 %%p6, %%r12, %%r21;");
+            o("@%%p6 bra $LN%d;", i);
             o("$R%d:", i);
         }
     }
@@ -650,6 +719,39 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
 // image group ig of NI images = NI / sw slots), CTA j taking items j, j + G, j + 2G, ...  At
 // any moment the CTAs of the grid therefore run the SAME block's code, started together, so
 // the straight-line code is fetched once for many SMs (instruction fetch is the limit).
+// item t (register tr) -> block (rb) and image group x band index (rc), the work order of
+// jp.order; NIG in %r5, grid size G in %r31; ta/tb/tc are scratch registers
+void emit_decode(Out &o, const JitPlan &jp, const char *tr, const char *rb, const char *rc,
+                 const char *ta, const char *tb, const char *tc, const char *tag) {
+    if (jp.order == 1) {
+        // spread: consecutive items are different blocks (every block's code is fetched
+        // in parallel from the first round on)
+        o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
+        o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
+    } else if (jp.order == 2) {
+        // first round spread (image groups 0..F-1 of every block, F = floor(G / nblocks):
+        // all blocks' code is pulled from DRAM in parallel), then block-major over the rest
+        o("div.u32 %s, %%r31, %d;", ta, jp.nblocks);   // F
+        o("min.u32 %s, %s, %%r5;", ta, ta);
+        o("mul.lo.u32 %s, %s, %d;", tb, ta, jp.nblocks); // F * nblocks
+        o("setp.lt.u32 %%p3, %s, %s;", tr, tb);
+        o("@!%%p3 bra $ORD_REST%s;", tag);
+        o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
+        o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
+        o("bra.uni $ORD_DONE%s;", tag);
+        o("$ORD_REST%s:", tag);
+        o("sub.u32 %s, %s, %s;", rc, tr, tb);           // t' = t - F*nb
+        o("sub.u32 %s, %%r5, %s;", rb, ta);             // NIG - F (> 0 here)
+        o("rem.u32 %s, %s, %s;", tc, rc, rb);
+        o("div.u32 %s, %s, %s;", rb, rc, rb);           // block
+        o("add.u32 %s, %s, %s;", rc, tc, ta);           // image group
+        o("$ORD_DONE%s:", tag);
+    } else {
+        o("rem.u32 %s, %s, %%r5;", rc, tr);             // image group
+        o("div.u32 %s, %s, %%r5;", rb, tr);             // block
+    }
+}
+
 std::string emit_entry(const JitPlan &jp) {
     const JitInput &in = jp.in;
     const int sw = jp.pair ? 2 : 1;
@@ -662,7 +764,7 @@ std::string emit_entry(const JitPlan &jp) {
       ".param .u32 p_olay)");
     o("{");
     o(".reg .pred %%p<8>;");
-    o(".reg .b32 %%r<64>;");
+    o(".reg .b32 %%r<80>;");
     o(".reg .b64 %%rd<24>;");
     o("ld.param.u64 %%rd0, [p_in];");
     o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -733,12 +835,16 @@ std::string emit_entry(const JitPlan &jp) {
             o("{");
             o(".param .b32 t0;\n.param .b32 t1;\n.param .b64 t2;\n.param .b32 t3;\n.param .b32 t4;");
             o(".param .b64 t5;\n.param .b32 t6;\n.param .b32 t7;\n.param .b64 t8;\n.param .b32 t9;");
-            o(".param .b64 t10;\n.param .b32 t11;");
+            o(".param .b64 t10;\n.param .b32 t11;\n.param .b32 t12;\n.param .b32 t13;");
+            o(".param .b32 t14;\n.param .b32 t15;");
             o("st.param.b32 [t0], %%r50;\nst.param.b32 [t1], %%r11;\nst.param.b64 [t2], %%rd1;");
             o("st.param.b32 [t3], 0;\nst.param.b32 [t4], 0;\nst.param.b64 [t5], 0;");
             o("st.param.b32 [t6], 0;\nst.param.b32 [t7], 0;\nst.param.b64 [t8], 0;");
             o("st.param.b32 [t9], 0;\nst.param.b64 [t10], 0;\nst.param.b32 [t11], %%r53;");
-            o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11);", b);
+            o("st.param.b32 [t12], 0;\nst.param.b32 [t13], %d;", jp.off_info);
+            o("st.param.b32 [t14], %d;\nst.param.b32 [t15], 0;", jp.off_info);
+            o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, "
+              "t14, t15);", b);
             o("}");
             o("bra.uni $DRY_NEXT;");
         }
@@ -768,6 +874,17 @@ std::string emit_entry(const JitPlan &jp) {
         o("setp.eq.u32 %%p0, %%r3, 0;");
         if (cl) o("setp.eq.and.u32 %%p0, %%r35, 0, %%p0;");
         o("@%%p0 atom.global.add.u32 %%r56, [%%rd20], %s;", cl ? "%r36" : "1");
+    }
+    const int NSL = jp.NI / sw;
+    if (jp.xpf) {
+        // cross-item staging: the barriers live for the whole kernel (phases continue from
+        // item to item), so they are initialised once here
+        o("setp.ne.u32 %%p0, %%r3, 0;");
+        o("@%%p0 bra $BINIT_DONE;");
+        for (int s = 0; s < jp.NS; ++s) o("mbarrier.init.shared::cta.b64 [%%r11+%d], 1;", jp.off_bar + 8 * s);
+        o("fence.mbarrier_init.release.cluster;");
+        o("$BINIT_DONE:");
+        o("mov.u32 %%r64, 0;");                      // item ordinal k of this CTA
     }
     o("$ITEM:");
     if (jp.dyn) {
@@ -817,33 +934,7 @@ std::string emit_entry(const JitPlan &jp) {
         o("setp.ge.u32 %%p0, %%r4, %%r32;");
         o("@%%p0 bra $EXIT;");
     }
-    if (jp.order == 1) {
-        // spread: consecutive items are different blocks (every block's code is fetched
-        // in parallel from the first round on)
-        o("rem.u32 %%r7, %%r4, %d;", jp.nblocks);  // block
-        o("div.u32 %%r6, %%r4, %d;", jp.nblocks);  // image group
-    } else if (jp.order == 2) {
-        // first round spread (image groups 0..F-1 of every block, F = floor(G / nblocks):
-        // all blocks' code is pulled from DRAM in parallel), then block-major over the rest
-        o("div.u32 %%r46, %%r31, %d;", jp.nblocks);   // F
-        o("min.u32 %%r46, %%r46, %%r5;");
-        o("mul.lo.u32 %%r47, %%r46, %d;", jp.nblocks); // F * nblocks
-        o("setp.lt.u32 %%p3, %%r4, %%r47;");
-        o("@!%%p3 bra $ORD_REST;");
-        o("rem.u32 %%r7, %%r4, %d;", jp.nblocks);
-        o("div.u32 %%r6, %%r4, %d;", jp.nblocks);
-        o("bra.uni $ORD_DONE;");
-        o("$ORD_REST:");
-        o("sub.u32 %%r6, %%r4, %%r47;");               // t' = t - F*nb
-        o("sub.u32 %%r7, %%r5, %%r46;");               // NIG - F (> 0 here)
-        o("rem.u32 %%r14, %%r6, %%r7;");
-        o("div.u32 %%r7, %%r6, %%r7;");                // block
-        o("add.u32 %%r6, %%r14, %%r46;");              // image group
-        o("$ORD_DONE:");
-    } else {
-        o("rem.u32 %%r6, %%r4, %%r5;");              // image group
-        o("div.u32 %%r7, %%r4, %%r5;");              // block
-    }
+    emit_decode(o, jp, "%r4", "%r7", "%r6", "%r46", "%r47", "%r14", "");
     // image group x band -> band, image group; the lane table of the band:
     // {smem byte base, (slot<<24)|(y0<<12)|x0, store mask, idle}
     o("rem.u32 %%r48, %%r6, %d;", jp.NB);        // band
@@ -874,33 +965,47 @@ std::string emit_entry(const JitPlan &jp) {
                                                  // (dynamic: the fetch barrier already is)
     o("setp.ne.u32 %%p0, %%r3, 0;");
     o("@%%p0 bra $INIT_DONE;");
-    // barriers of the previous item have completed every phase and have no pending
-    // transfers: invalidate and re-initialise them (phase parity restarts at 0)
-    o("setp.eq.u32 %%p4, %%r34, 0;");
-    for (int s = 0; s < jp.NS; ++s) {
-        o("@%%p4 mbarrier.inval.shared::cta.b64 [%%r11+%d];", jp.off_bar + 8 * s);
-        o("mbarrier.init.shared::cta.b64 [%%r11+%d], 1;", jp.off_bar + 8 * s);
-        o("st.shared.u32 [%%r11+%d], 0;", jp.off_cnt + 4 * s);
-    }
-    o("mov.u32 %%r34, 0;");
-    // per-slot source base: in + ((n0/sw + j) * C + g * Cg) * plane * sw * 4
     const long long slot_bytes = (long long)in.C * jp.plane * 4 * sw;
-    o("shr.u32 %%r42, %%r8, %d;", sw - 1);
-    o("cvt.u64.u32 %%rd4, %%r42;");
-    o("mul.lo.u64 %%rd4, %%rd4, %lld;", slot_bytes);
-    o("cvt.u64.u32 %%rd5, %%r10;");
-    o("mul.lo.u64 %%rd5, %%rd5, %lld;", (long long)in.Cg * jp.plane * 4 * sw);
-    o("add.u64 %%rd4, %%rd4, %%rd5;");
-    o("add.u64 %%rd4, %%rd0, %%rd4;");
-    o("mov.u32 %%r12, 0;");
-    o("add.u32 %%r13, %%r11, %d;", jp.off_info);
-    o("$INFO:");
-    o("st.shared.u64 [%%r13], %%rd4;");
-    o("add.u64 %%rd4, %%rd4, %lld;", slot_bytes);
-    o("add.u32 %%r13, %%r13, 8;");
-    o("add.u32 %%r12, %%r12, 1;");
-    o("setp.lt.u32 %%p1, %%r12, %%r41;");
-    o("@%%p1 bra $INFO;");
+    // per-slot source base of image n0 in conv group g: in + ((n0/sw + j) * C + g * Cg) *
+    // plane * sw * 4, written to the slot table at smem offset `tab`
+    auto emit_info = [&](const char *n0, const char *g, const char *nsl, const char *tab,
+                         const char *tag) {
+        o("shr.u32 %%r42, %s, %d;", n0, sw - 1);
+        o("cvt.u64.u32 %%rd4, %%r42;");
+        o("mul.lo.u64 %%rd4, %%rd4, %lld;", slot_bytes);
+        o("cvt.u64.u32 %%rd5, %s;", g);
+        o("mul.lo.u64 %%rd5, %%rd5, %lld;", (long long)in.Cg * jp.plane * 4 * sw);
+        o("add.u64 %%rd4, %%rd4, %%rd5;");
+        o("add.u64 %%rd4, %%rd0, %%rd4;");
+        o("mov.u32 %%r12, 0;");
+        o("add.u32 %%r13, %%r11, %s;", tab);
+        o("$INFO%s:", tag);
+        o("st.shared.u64 [%%r13], %%rd4;");
+        o("add.u64 %%rd4, %%rd4, %lld;", slot_bytes);
+        o("add.u32 %%r13, %%r13, 8;");
+        o("add.u32 %%r12, %%r12, 1;");
+        o("setp.lt.u32 %%p1, %%r12, %s;", nsl);
+        o("@%%p1 bra $INFO%s;", tag);
+    };
+    char tab0[32];
+    std::snprintf(tab0, sizeof tab0, "%d", jp.off_info);
+    if (jp.xpf) {
+        for (int s = 0; s < jp.NS; ++s) o("st.shared.u32 [%%r11+%d], 0;", jp.off_cnt + 4 * s);
+        // the first item stages its own first chunks; later items find them staged
+        o("setp.ne.u32 %%p4, %%r64, 0;");
+        o("@%%p4 bra $FILLS_DONE;");
+    } else {
+        // barriers of the previous item have completed every phase and have no pending
+        // transfers: invalidate and re-initialise them (phase parity restarts at 0)
+        o("setp.eq.u32 %%p4, %%r34, 0;");
+        for (int s = 0; s < jp.NS; ++s) {
+            o("@%%p4 mbarrier.inval.shared::cta.b64 [%%r11+%d];", jp.off_bar + 8 * s);
+            o("mbarrier.init.shared::cta.b64 [%%r11+%d], 1;", jp.off_bar + 8 * s);
+            o("st.shared.u32 [%%r11+%d], 0;", jp.off_cnt + 4 * s);
+        }
+        o("mov.u32 %%r34, 0;");
+    }
+    emit_info("%r8", "%r10", "%r41", tab0, "");
     o("fence.mbarrier_init.release.cluster;");
     o("fence.proxy.async.shared::cta;");
     for (int i = 0; i < std::min(jp.NS, jp.nchunks); ++i) {
@@ -926,8 +1031,64 @@ std::string emit_entry(const JitPlan &jp) {
         o("setp.lt.u32 %%p1, %%r12, %%r41;");
         o("@%%p1 bra $F%d;", i);
     }
+    if (jp.xpf) {
+        o("$FILLS_DONE:");
+        // the next item of this CTA (t + G): its slot table into the other buffer and its
+        // slot count for the block (0: none)
+        o("add.u32 %%r65, %%r4, %%r31;");
+        o("mov.u32 %%r67, 0;");
+        o("setp.ge.u32 %%p4, %%r65, %%r32;");
+        o("@%%p4 bra $NX_DONE;");
+        emit_decode(o, jp, "%r65", "%r68", "%r69", "%r70", "%r71", "%r72", "_NX");
+        o("div.u32 %%r69, %%r69, %d;", jp.NB);       // image group
+        o("mul.lo.u32 %%r70, %%r69, %d;", jp.NI);    // n0
+        o("sub.u32 %%r71, %%r0, %%r70;");
+        o("min.u32 %%r71, %%r71, %d;", jp.NI);
+        o("add.u32 %%r67, %%r71, %d;", sw - 1);
+        o("shr.u32 %%r67, %%r67, %d;", sw - 1);      // slots of the next item
+        o("mov.u32 %%r72, 0;");                      // its conv group
+        for (int b = 0; b < jp.nblocks; ++b)
+            if (jp.bgrp[size_t(b)] != 0) {
+                o("setp.eq.u32 %%p3, %%r68, %d;", b);
+                o("@%%p3 mov.u32 %%r72, %d;", jp.bgrp[size_t(b)]);
+            }
+        o("and.b32 %%r73, %%r64, 1;");
+        o("xor.b32 %%r73, %%r73, 1;");
+        o("mad.lo.u32 %%r73, %%r73, %d, %d;", NSL * 8, jp.off_info);
+        emit_info("%r70", "%r72", "%r67", "%r73", "_NX");
+        o("$NX_DONE:");
+        o("st.shared.u32 [%%r11+%d], %%r67;", jp.off_item);
+    }
     o("$INIT_DONE:");
     o("bar.sync 0;");
+    // stage phases (r74), slot tables (r76 this item, r77 next), next item's slots (r75)
+    if (jp.xpf) {
+        // global chunk g = k * nchunks + j runs on physical stage g % NS, fill ordinal g / NS:
+        // logical stage s of item k has parity base ((k*nchunks + s) / NS) & 1 and rotation
+        // (k * nchunks) % NS
+        o("mov.u32 %%r74, 0;");
+        for (int s = 0; s < jp.NS; ++s) {
+            o("mad.lo.u32 %%r78, %%r64, %d, %d;", jp.nchunks, s);
+            o("div.u32 %%r78, %%r78, %d;", jp.NS);
+            o("and.b32 %%r78, %%r78, 1;");
+            o("shl.b32 %%r78, %%r78, %d;", s);
+            o("or.b32 %%r74, %%r74, %%r78;");
+        }
+        o("mul.lo.u32 %%r78, %%r64, %d;", jp.nchunks);
+        o("rem.u32 %%r78, %%r78, %d;", jp.NS);
+        o("shl.b32 %%r78, %%r78, 8;");
+        o("or.b32 %%r74, %%r74, %%r78;");
+        o("and.b32 %%r76, %%r64, 1;");
+        o("xor.b32 %%r77, %%r76, 1;");
+        o("mad.lo.u32 %%r76, %%r76, %d, %d;", NSL * 8, jp.off_info);
+        o("mad.lo.u32 %%r77, %%r77, %d, %d;", NSL * 8, jp.off_info);
+        o("ld.shared.u32 %%r75, [%%r11+%d];", jp.off_item);
+    } else {
+        o("mov.u32 %%r74, 0;");
+        o("mov.u32 %%r76, %d;", jp.off_info);
+        o("mov.u32 %%r77, %d;", jp.off_info);
+        o("mov.u32 %%r75, 0;");
+    }
     // store mask: none for a slot past the batch; pair mode: bit 31 = image B exists
     o("mov.u32 %%r19, %%r33;");
     o("setp.ge.u32 %%p2, %%r21, %%r41;");
@@ -966,17 +1127,22 @@ std::string emit_entry(const JitPlan &jp) {
         o("{");
         o(".param .b32 t0;\n.param .b32 t1;\n.param .b64 t2;\n.param .b32 t3;\n.param .b32 t4;");
         o(".param .b64 t5;\n.param .b32 t6;\n.param .b32 t7;\n.param .b64 t8;\n.param .b32 t9;");
-        o(".param .b64 t10;\n.param .b32 t11;");
+        o(".param .b64 t10;\n.param .b32 t11;\n.param .b32 t12;\n.param .b32 t13;");
+        o(".param .b32 t14;\n.param .b32 t15;");
         o("st.param.b32 [t0], %%r17;\nst.param.b32 [t1], %%r11;\nst.param.b64 [t2], %%rd8;");
         o("st.param.b32 [t3], %%r19;\nst.param.b32 [t4], %%r41;\nst.param.b64 [t5], %%rd3;");
         o("st.param.b32 [t6], %%r1;\nst.param.b32 [t7], %%r30;\nst.param.b64 [t8], %%rd10;");
         o("st.param.b32 [t9], %%r40;\nst.param.b64 [t10], %%rd12;\nst.param.b32 [t11], 0;");
-        o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11);", b);
+        o("st.param.b32 [t12], %%r74;\nst.param.b32 [t13], %%r76;");
+        o("st.param.b32 [t14], %%r77;\nst.param.b32 [t15], %%r75;");
+        o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, "
+          "t14, t15);", b);
         o("}");
         o("bra.uni $NEXT;");
     }
     o("$NEXT:");
     if (!jp.dyn) o("add.u32 %%r4, %%r4, %%r31;");
+    if (jp.xpf) o("add.u32 %%r64, %%r64, 1;");
     o("bra.uni $ITEM;");
     o("$EXIT:");
     if (jp.dyn) {
@@ -1444,7 +1610,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                         NS = std::min(ns_max, nch);
                         IS = (CB * plane * sw + 3) / 4 * 4;
                         stage = NSL * IS * 4;
-                        smem = size_t(NS) * stage + 256 + size_t(NSL) * 8;
+                        smem = size_t(NS) * stage + 264 + size_t(NSL) * 16;
                         if (smem <= size_t(kMaxSmem)) break;
                     }
                     if (NSL < 1) continue;
@@ -1541,7 +1707,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     int best_extra = -1, best_is = IS0;
     for (int t = 0; t < 8; ++t) {
         const int IS = IS0 + 4 * t;
-        const size_t smem = size_t(jp.NS) * NSL * IS * 4 + 256 + size_t(NSL) * 8;
+        const size_t smem = size_t(jp.NS) * NSL * IS * 4 + 264 + size_t(NSL) * 16;
         if (smem > size_t(kMaxSmem)) break;
         int e = 0;
         for (int b = 0; b < jp.NB && e >= 0; ++b) {
@@ -1569,7 +1735,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.off_cnt = jp.off_bar + 8 * kMaxStages;
     jp.off_info = jp.off_cnt + 4 * kMaxStages;
     jp.off_info = (jp.off_info + 7) / 8 * 8;
-    jp.off_item = jp.off_info + NSL * 8;
+    jp.off_item = jp.off_info + 2 * NSL * 8;      // two slot tables (this item, next item)
     jp.smem = size_t(jp.off_item) + 8;
     jp.maxreg = reg_cap(jp.NW);
     if (const char *e = std::getenv("SKC_JIT_SYNC")) jp.sync_every = std::max(0, std::atoi(e));
@@ -1577,11 +1743,13 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_PMAJOR")) jp.pmajor = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_XPF")) jp.xpf = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_DYN")) jp.dyn = std::max(0, std::min(2, std::atoi(e)));
     // whole-program compile (one serial ptxas run, ~10-20 s per 100k instructions) when the
     // code is moderate; parallel per-block modules otherwise (their calls pay an ABI
     // save/restore of callee-saved registers: -8-10% measured, profiles/r01_jit_whole.txt)
     choose_blocks(jp, n_hint);
+    if (jp.dyn) jp.xpf = 0;  // the next item must be known an item ahead (static order)
     jp.whole = jp.code_instr <= kWholeMaxInstr ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
