@@ -133,7 +133,8 @@ struct JitPlan {
     size_t smem = 0;
     int maxreg = 255;          // register cap of the block functions (NW warps per SM)
     int sync_every = 0;        // FMA instructions between CTA barriers in the code (0: none)
-    int l2hint = 1;            // 1: evict-first TMA loads + streaming stores (code stays in L2)
+    int l2hint = 3;            // bit 0: streaming (.cs) output stores, bit 1: evict-first TMA
+                               // loads -- the activations do not push the code out of L2
     // work-item order: 0 block-major, 1 spread (blocks interleaved), 2 first round spread then
     // block-major.  2: every block's (cold, DRAM-resident) code is fetched in parallel by the
     // first round, later rounds share one code stream chip-wide (profiles/r01_jit_order.txt)
@@ -462,7 +463,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o("mov.u32 %%r7, 0;");
     o("mov.u32 %%r8, 1;");
     // activations stream through L2 (evict first) so the straight-line code stays resident
-    if (jp.l2hint) o("createpolicy.fractional.L2::evict_first.b64 %%rd10, 1.0;");
+    if (jp.l2hint & 2) o("createpolicy.fractional.L2::evict_first.b64 %%rd10, 1.0;");
     // logical stage s = physical stage (s + rot) % NS: stage base (rs), lane base (rb),
     // barrier (rw), wait parities (rq: base, base ^ 1)
     o("ld.param.b32 %%r18, [q_ph];");
@@ -604,7 +605,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             o("ld.shared.u64 %%rd6, [%%r13];");
             o("add.u64 %%rd6, %%rd6, %lld;", (long long)nxt * jp.CB * jp.plane * 4 * sw);
             o("mad.lo.u32 %%r14, %%r12, %d, %%rs%d;", jp.img_stride * 4, s);
-            if (jp.l2hint)
+            if (jp.l2hint & 2)
                 o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
                   "[%%r14], [%%rd6], %d, [%%r15], %%rd10;", bytes);
             else
@@ -639,7 +640,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             o("ld.shared.u64 %%rd6, [%%r13];");
             o("add.u64 %%rd6, %%rd6, %lld;", (long long)nxt * jp.CB * jp.plane * 4 * sw);
             o("mad.lo.u32 %%r14, %%r12, %d, %%rs%d;", jp.img_stride * 4, s);
-            if (jp.l2hint)
+            if (jp.l2hint & 2)
                 o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
                   "[%%r14], [%%rd6], %d, [%%r15], %%rd10;", bytes);
             else
@@ -689,12 +690,12 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
                     o("mov.b64 {%%e0, %%e1}, %%a%d;", m * NPT + ty * TX + tx);
                     o("add.f32 %%e3, %%e0, %%e2;");
                     o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
-                    o(jp.l2hint ? "@%%p3 st.global.cs.f32 [%%rd5], %%e3;" : "@%%p3 st.global.f32 [%%rd5], %%e3;");
+                    o((jp.l2hint & 1) ? "@%%p3 st.global.cs.f32 [%%rd5], %%e3;" : "@%%p3 st.global.f32 [%%rd5], %%e3;");
                     o("add.f32 %%e3, %%e1, %%e2;");
                     o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
                     o("and.pred %%p3, %%p3, %%p7;");
                     o("add.u64 %%rd6, %%rd5, %%rd7;");
-                    o(jp.l2hint ? "@%%p3 st.global.cs.f32 [%%rd6], %%e3;" : "@%%p3 st.global.f32 [%%rd6], %%e3;");
+                    o((jp.l2hint & 1) ? "@%%p3 st.global.cs.f32 [%%rd6], %%e3;" : "@%%p3 st.global.f32 [%%rd6], %%e3;");
                     continue;
                 }
                 if (tx < 2 * PX) {
@@ -704,7 +705,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
                     o("add.f32 %%e3, %%f%d, %%e2;", m * NST + ty * (TX - 2 * PX) + tx - 2 * PX);
                 }
                 o("@%%p2 max.f32 %%e3, %%e3, 0f00000000;");
-                o(jp.l2hint ? "@%%p3 st.global.cs.f32 [%%rd5], %%e3;" : "@%%p3 st.global.f32 [%%rd5], %%e3;");
+                o((jp.l2hint & 1) ? "@%%p3 st.global.cs.f32 [%%rd5], %%e3;" : "@%%p3 st.global.f32 [%%rd5], %%e3;");
             }
         }
     }
@@ -794,7 +795,7 @@ std::string emit_entry(const JitPlan &jp) {
     o("mul.lo.u32 %%r32, %%r5, %d;", jp.nblocks);  // items
     o("mov.u32 %%r11, skc_smem;");
     o("mov.u32 %%r34, 1;");
-    if (jp.l2hint) o("createpolicy.fractional.L2::evict_first.b64 %%rd13, 1.0;");                      // first item: barriers not yet initialised
+    if (jp.l2hint & 2) o("createpolicy.fractional.L2::evict_first.b64 %%rd13, 1.0;");                      // first item: barriers not yet initialised
     o("add.u32 %%r24, %%r2, %%r2;");
     o("add.u32 %%r25, %%r24, %d;", in.Ho);       // Hop
     o("add.u32 %%r26, %%r24, %d;", in.Wo);       // Wop
@@ -1021,7 +1022,7 @@ std::string emit_entry(const JitPlan &jp) {
         o("add.u64 %%rd6, %%rd6, %lld;", (long long)i * jp.CB * jp.plane * 4 * sw);
         o("mad.lo.u32 %%r16, %%r12, %d, %%r11;", jp.img_stride * 4);
         o("add.u32 %%r16, %%r16, %d;", i * jp.stage_bytes);
-        if (jp.l2hint)
+        if (jp.l2hint & 2)
             o("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
               "[%%r16], [%%rd6], %d, [%%r15], %%rd13;", bytes);
         else
@@ -1739,7 +1740,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.smem = size_t(jp.off_item) + 8;
     jp.maxreg = reg_cap(jp.NW);
     if (const char *e = std::getenv("SKC_JIT_SYNC")) jp.sync_every = std::max(0, std::atoi(e));
-    if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) & 3;
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_PMAJOR")) jp.pmajor = std::atoi(e) ? 1 : 0;
