@@ -1474,7 +1474,7 @@ void choose_blocks(JitPlan &jp, int n_hint) {
     };
     double best_span = 0;
     std::vector<Blk> best;
-    const int smax = jp.dyn ? jp.nbg : 0;
+    const int smax = jp.dyn ? std::min(jp.nbg, (in.Kg + Mp - 1) / Mp) : 0;
     for (int sp = 0; sp <= smax; ++sp) {
         if (force >= 0 && sp != std::min(force, smax)) continue;
         std::vector<Blk> full, tail;
@@ -1629,6 +1629,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     // even blocks: M' = ceil(Kg / nbg) <= M (no small leftover block paying a
                     // full set of window loads for a few channels)
                     if (fm <= 0) M = (in.Kg + nbg - 1) / nbg;
+                    if (xb > 0 && (in.Kg + M - 1) / M != nbg) continue;  // no real extra block
                     // distinct blocks running at once for a batch of n_hint images (an item
                     // covers NI images x 1/NB of their pixels: NIe image-equivalents)
                     const double NIe = double(NI) / NB;

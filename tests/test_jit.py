@@ -149,3 +149,37 @@ def test_padded_shape_per_layout():
     if j["layout"] == skc.SKC_LAYOUT_PAIRS:
         assert skc.padded_shape(j, 5) == (3, 16, 15, 15, 2)
         assert skc.padded_shape(j, 6) == (3, 16, 15, 15, 2)
+
+
+@pytest.mark.parametrize("knobs", [
+    {"SKC_JIT_DYN": "1", "SKC_JIT_SPLIT": "2"},
+    {"SKC_JIT_DYN": "1", "SKC_JIT_SPLIT": "9"},
+    {"SKC_JIT_XPF": "1"},
+    {"SKC_JIT_PMAJOR": "0"},
+    {"SKC_JIT_PAIR": "0"},
+])
+def test_jit_scheduling_variants_verify(knobs, monkeypatch):
+    """Tail split (halved blocks at the end of the queue), cross-item staging, code order and
+    layout variants: every plan still decodes to exactly the CSR (skc_plan_verify checks that
+    each output channel sits in exactly one block of its own group, and every block's code
+    against its channels' CSR rows), and the split count is reported."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(8)
+    n_ok = 0
+    for it in range(40):
+        layer = wl.random_layer(rng, max_c=32, max_hw=20, rs=(1, 3, 5), groups=(1, 2))
+        w, _ = wl.random_tensors(rng, layer, 1)
+        try:
+            plan = pack_jit(w, layer)
+        except skc.SkcError as e:
+            assert e.status == -5, e
+            continue
+        skc.skc_plan_verify(plan)
+        info = plan.info()
+        if "SKC_JIT_SPLIT" in knobs:
+            nbg = -(-layer.K // layer.groups // info["channels_per_warp"])  # even blocks per group
+            assert 0 <= info["jit_split"] <= nbg
+            assert info["jit_blocks"] >= layer.groups * nbg
+        n_ok += 1
+    assert n_ok >= 15, n_ok
