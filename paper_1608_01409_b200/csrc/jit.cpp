@@ -446,6 +446,8 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o(".reg .f32 %%ws<%d>;", NWIN);
     o(".reg .b64 %%wp<%d>;", NWIN);
     o(".reg .b64 %%wt;");
+    o(".reg .pred %%pe<8>;");
+    o(".reg .b64 %%rdp<4>;");
     o(".reg .f32 %%e<4>;");
     o("ld.param.b32 %%r0, [q_lb];");
     o("ld.param.b32 %%r1, [q_sm];");
@@ -663,6 +665,50 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         o("and.b32 %%r9, %%r2, %u;", 0x80000000u);
         o("setp.ne.u32 %%p7, %%r9, 0;");
     }
+    const int T = TY * TX;
+    const bool fast_epi = pm && T <= 3;
+    if (fast_epi) {
+        // without bias (the common case) the epilogue is address + store per accumulator:
+        // the pixel predicates and offsets are hoisted out of the channel loop and the relu /
+        // no-relu variants are separate code (one runs), so no predicated-off add / max issues
+        for (int i = 0; i < T; ++i) {
+            const int ty = i / TX, tx = i % TX;
+            o("and.b32 %%r9, %%r2, %u;", 1u << i);
+            o("setp.ne.u32 %%pe%d, %%r9, 0;", 2 * i);
+            o("and.pred %%pe%d, %%pe%d, %%p7;", 2 * i + 1, 2 * i);
+            if (i == 0) continue;
+            o("mul.wide.u32 %%rdp%d, %%r5, %d;", i, ty);
+            o("mul.wide.u32 %%rd6, %%r16, %d;", tx);
+            o("add.u64 %%rdp%d, %%rdp%d, %%rd6;", i, i);
+        }
+        o("@%%p1 bra $EPI_B;");
+        for (int relu = 0; relu < 2; ++relu) {
+            o("$EPI_%c:", relu ? 'R' : 'N');
+            if (!relu) o("@%%p2 bra $EPI_R;");
+            for (int m = 0; m < Mb; ++m) {
+                const int k = ks[size_t(m)];
+                o("mul.lo.u64 %%rd3, %%rd2, %d;", k);
+                o("add.u64 %%rd3, %%rd0, %%rd3;");
+                for (int i = 0; i < T; ++i) {
+                    const char *ad = "%rd3";
+                    if (i) {
+                        o("add.u64 %%rd5, %%rd3, %%rdp%d;", i);
+                        ad = "%rd5";
+                    }
+                    o("mov.b64 {%%e0, %%e1}, %%a%d;", m * NPT + i);
+                    if (relu) {
+                        o("max.f32 %%e0, %%e0, 0f00000000;");
+                        o("max.f32 %%e1, %%e1, 0f00000000;");
+                    }
+                    o("@%%pe%d st.global%s.f32 [%s], %%e0;", 2 * i, (jp.l2hint & 1) ? ".cs" : "", ad);
+                    o("add.u64 %%rd6, %s, %%rd7;", ad);
+                    o("@%%pe%d st.global%s.f32 [%%rd6], %%e1;", 2 * i + 1, (jp.l2hint & 1) ? ".cs" : "");
+                }
+            }
+            o("bra.uni $EPI_END;");
+        }
+        o("$EPI_B:");
+    }
     for (int m = 0; m < Mb; ++m) {
         const int k = ks[size_t(m)];
         o("mov.f32 %%e2, 0f00000000;");
@@ -709,6 +755,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             }
         }
     }
+    if (fast_epi) o("$EPI_END:");
     o("ret;");
     o("$DRYRET:");
     o("ret;");

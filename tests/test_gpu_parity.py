@@ -312,15 +312,19 @@ def test_fused_epilogue(kernel):
         skc.skc_pad_input(conv.plan, torch.from_numpy(x).cuda(), xp, 3)
         ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
         db = torch.from_numpy(bias).cuda()
-        for relu in (False, True):
+        zero = np.zeros_like(bias)
+        # with and without a bias: the JIT kernel has separate epilogue code for each
+        for relu, use_bias in ((False, True), (True, True), (False, False), (True, False)):
             for op in (0, 1, 2):
                 out = torch.full((3, layer.K, layer.Ho + 2 * op, layer.Wo + 2 * op), 7.0,
                                  device="cuda")
-                skc.skc_sparse_conv_forward_ex(conv.plan, xp, out, 3, db, relu, op)
+                skc.skc_sparse_conv_forward_ex(conv.plan, xp, out, 3, db if use_bias else None,
+                                               relu, op)
                 torch.cuda.synchronize()
                 o = out.cpu().numpy()
                 inner = o[:, :, op:op + layer.Ho, op:op + layer.Wo]
-                check_epi(inner, ref, bound, bias, relu, f"{layer.name} relu={relu} pad={op}")
+                check_epi(inner, ref, bound, bias if use_bias else zero, relu,
+                          f"{layer.name} relu={relu} bias={use_bias} pad={op}")
                 halo = o.copy()
                 halo[:, :, op:op + layer.Ho, op:op + layer.Wo] = 7.0
                 assert np.all(halo == 7.0), "halo written"
