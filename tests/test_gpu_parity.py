@@ -563,3 +563,48 @@ def test_jit_tuning_knobs_bitwise(knobs, monkeypatch):
             continue
         np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32),
                                       err_msg=f"{knobs} {layer.name} {conv.geom}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dyn", ["1", "2"])
+def test_jit_dynamic_counter_resets_across_launches(dyn, monkeypatch):
+    """Dynamic scheduling keeps a work-item counter in the plan workspace that the last CTA of
+    every launch resets: back-to-back launches of ONE plan with different batch sizes (and
+    grid sizes), and replays of a captured CUDA graph, must each compute every item exactly
+    once -- bitwise equal to the direct kernel every time."""
+    monkeypatch.setenv("SKC_JIT_DYN", dyn)
+    monkeypatch.setenv("SKC_JIT_SPLIT", "2")
+    rng = np.random.default_rng(46)
+    layer = wl.Layer("d1", 48, 32, 13, 13, 3, 3, 1, 1, 2, 0.85, 0.01)
+    w, x = wl.random_tensors(rng, layer, 40)
+    jit = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                      skc.SKC_KERNEL_JIT)
+    direct = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                         layer.groups, skc.SKC_KERNEL_DIRECT)
+    assert jit.plan.info()["jit_split"] > 0
+    xd = torch.from_numpy(x).cuda()
+    xpj = torch.empty(jit.padded_shape(40), device="cuda")
+    skc.skc_pad_input(jit.plan, xd, xpj, 40)
+    xpd = torch.empty(direct.padded_shape(40), device="cuda")
+    skc.skc_pad_input(direct.plan, xd, xpd, 40)
+    yd = direct.forward_padded(xpd).cpu().numpy()
+    for N in (40, 7, 1, 33, 40, 2, 40):
+        yj = torch.full(jit.out_shape(N), float("nan"), device="cuda")
+        jit.forward_padded(xpj, yj)  # the first N images (pairs are image-major)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(yj.cpu().numpy().view(np.uint32), yd[:N].view(np.uint32),
+                                      err_msg=f"N={N}")
+    # graph replays of the same launch
+    yj = torch.full(jit.out_shape(40), float("nan"), device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            jit.forward_padded(xpj, yj, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(4):
+        yj.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(yj.cpu().numpy().view(np.uint32), yd.view(np.uint32))
