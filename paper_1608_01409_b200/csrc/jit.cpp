@@ -75,7 +75,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 15;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 16;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -776,16 +776,23 @@ void emit_decode(Out &o, const JitPlan &jp, const char *tr, const char *rb, cons
         // in parallel from the first round on)
         o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
         o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
-    } else if (jp.order == 2) {
+    } else if (jp.order == 2 || jp.order == 3) {
         // first round spread (image groups 0..F-1 of every block, F = floor(G / nblocks):
-        // all blocks' code is pulled from DRAM in parallel), then block-major over the rest
+        // all blocks' code is pulled from DRAM in parallel), then block-major over the rest.
+        // Order 3: the first round is block-major too (item t < F*nb: block t / F), so with
+        // GPC-major item numbers the CTAs of a GPC start on one or two blocks
         o("div.u32 %s, %%r31, %d;", ta, jp.nblocks);   // F
         o("min.u32 %s, %s, %%r5;", ta, ta);
         o("mul.lo.u32 %s, %s, %d;", tb, ta, jp.nblocks); // F * nblocks
         o("setp.lt.u32 %%p3, %s, %s;", tr, tb);
         o("@!%%p3 bra $ORD_REST%s;", tag);
-        o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
-        o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
+        if (jp.order == 3) {
+            o("div.u32 %s, %s, %s;", rb, tr, ta);
+            o("rem.u32 %s, %s, %s;", rc, tr, ta);
+        } else {
+            o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
+            o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
+        }
         o("bra.uni $ORD_DONE%s;", tag);
         o("$ORD_REST%s:", tag);
         o("sub.u32 %s, %s, %s;", rc, tr, tb);           // t' = t - F*nb
@@ -809,7 +816,7 @@ std::string emit_entry(const JitPlan &jp) {
     o(".extern .shared .align 128 .b8 skc_smem[];");
     o(".visible .entry skc_jit_kernel(.param .u64 p_in, .param .u64 p_out, .param .u64 p_lm, "
       ".param .u64 p_bias, .param .u32 p_N, .param .u32 p_relu, .param .u32 p_opad, "
-      ".param .u32 p_olay)");
+      ".param .u32 p_olay, .param .u64 p_vid)");
     o("{");
     o(".reg .pred %%p<8>;");
     o(".reg .b32 %%r<80>;");
@@ -836,6 +843,20 @@ std::string emit_entry(const JitPlan &jp) {
     o("mov.u32 %%r38, %%nclusterid.x;");
     o("mad.lo.u32 %%r4, %%r37, %%r36, %%r35;");  // item t
     o("mul.lo.u32 %%r31, %%r38, %%r36;");        // stride G
+    // GPC-major item numbering (one CTA per SM, grid = all SMs): the first item of the CTA on
+    // SM s is vid[s], the SM's position in a GPC-major order (topo.cu), so the CTAs of one GPC
+    // take neighbouring items -- the same channel block -- and share the GPC's instruction
+    // cache.  p_vid = 0: item t = cluster-major CTA rank.
+    o("ld.param.u64 %%rd21, [p_vid];");
+    o("setp.eq.u64 %%p0, %%rd21, 0;");
+    o("@%%p0 bra $VID_DONE;");
+    o("cvta.to.global.u64 %%rd21, %%rd21;");
+    o("mov.u32 %%r79, %%smid;");
+    o("mul.wide.u32 %%rd22, %%r79, 2;");
+    o("add.u64 %%rd22, %%rd21, %%rd22;");
+    o("ld.global.nc.u16 %%r79, [%%rd22];");
+    o("mov.u32 %%r4, %%r79;");
+    o("$VID_DONE:");
     o("add.u32 %%r5, %%r0, %d;", jp.NI - 1);
     o("div.u32 %%r5, %%r5, %d;", jp.NI);        // image groups
     o("mul.lo.u32 %%r5, %%r5, %d;", jp.NB);     // NIG = image groups x bands
@@ -1475,9 +1496,9 @@ double item_time(const JitPlan &jp, double instr) {
 int item_block(const JitPlan &jp, int64_t t, int64_t nig, int64_t G) {
     const int64_t nb = jp.nblocks;
     if (jp.order == 1) return int(t % nb);
-    if (jp.order == 2) {
+    if (jp.order == 2 || jp.order == 3) {
         const int64_t F = std::min<int64_t>(G / nb, nig);
-        if (t < F * nb) return int(t % nb);
+        if (t < F * nb) return int(jp.order == 3 ? t / F : t % nb);
         return int((t - F * nb) / (nig - F));
     }
     return int(t / nig);
@@ -2059,8 +2080,19 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
     const float *bias = epi.bias;
     unsigned un = unsigned(N), relu = unsigned(epi.relu), opad = unsigned(epi.opad);
     unsigned olay = unsigned(epi.olay);
+    // GPC-major item numbering needs exactly one CTA on every SM (SKC_JIT_VID=0: off)
+    static const bool vid_on = [] {
+        const char *e = std::getenv("SKC_JIT_VID");
+        return !e || std::atoi(e) != 0;
+    }();
+    const void *vid = nullptr;
+    if (vid_on && per_sm == 1 && grid == nsm && jp->dyn != 2 && cs <= 2)
+        vid = sm_gpc_order_device(dev, true);
+    if (std::getenv("SKC_JIT_DEBUG"))
+        std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
+                     vid ? "on" : "off");
     void *args[] = {(void *)&in, (void *)&out, (void *)&d_lanemap, (void *)&bias,
-                    (void *)&un, (void *)&relu, (void *)&opad, (void *)&olay};
+                    (void *)&un, (void *)&relu, (void *)&opad, (void *)&olay, (void *)&vid};
     return cudaLaunchKernelExC(&lc, reinterpret_cast<const void *>(jp->kern), args);
 }
 

@@ -1153,6 +1153,8 @@ skc_status skc_plan_upload(skc_plan *p, void *d_ws, size_t bytes, void *stream) 
         std::string msg;
         const int r = jit_compile(p->jit, &msg);
         if (r != SKC_OK) return fail(skc_status(r), "JIT compile: %s", msg.c_str());
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) sm_gpc_order_device(dev, false);  // SM topology, once
     }
     cudaError_t e = cudaMemcpyAsync(d_ws, p->image.data(), p->image.size(),
                                     cudaMemcpyHostToDevice, (cudaStream_t)stream);

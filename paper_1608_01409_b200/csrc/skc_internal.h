@@ -134,6 +134,9 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
                        const Epilogue &epi, cudaStream_t st, std::string *msg);
 // Static check: tables + the emitted code decoded back to the canonical CSR (host).
 int jit_verify_code(const JitPlan *jp, std::string *msg);
+// GPC-major SM order (topo.cu): vid[smid], empty when unknown.  Synchronous, once per device.
+const std::vector<uint16_t> &sm_gpc_order(int dev);
+const uint16_t *sm_gpc_order_device(int dev, bool peek);
 void jit_destroy(JitPlan *jp);
 
 cudaError_t bench_ffma(void *scratch, int blocks, int iters, float *ms, double *flops);
