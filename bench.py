@@ -243,8 +243,14 @@ def run_ours(args, cfg, rank, world, local_rank):
     plans = [skc.skc_pack_csr(wl.gen_weights(cfg.cfg_id, li, L), L.H, L.W, L.stride, L.pad,
                               L.groups, kernel) for li, L in enumerate(cfg.layers)]
     import concurrent.futures as cf
+    # N ranks of one node: local rank 0 compiles first and fills the on-disk JIT cache, the
+    # others then load the same code from it instead of N concurrent compiles
+    if world > 1 and local_rank != 0:
+        dist.barrier()
     with cf.ThreadPoolExecutor(max_workers=len(plans)) as ex:
         list(ex.map(skc.skc_plan_compile, plans))
+    if world > 1 and local_rank == 0:
+        dist.barrier()
     for li, L in enumerate(cfg.layers):
         w = wl.gen_weights(cfg.cfg_id, li, L)
         conv = skc.SparseConv2d.from_plan(plans[li], dev)
