@@ -254,6 +254,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     for li, L in enumerate(cfg.layers):
         w = wl.gen_weights(cfg.cfg_id, li, L)
         conv = skc.SparseConv2d.from_plan(plans[li], dev)
+        # launch-schedule tuning for this batch on this device (setup, untimed; outputs are
+        # bitwise unaffected -- DESIGN.md Sec. 7.4)
+        if os.environ.get("SKC_TUNE", "1") != "0":
+            conv.tune(per_gpu)
         x_host = torch.from_numpy(wl.gen_input(cfg.cfg_id, li, L, n0, n1))
         x = x_host.to(dev)
         xp = torch.empty(conv.padded_shape(per_gpu), device=dev)
@@ -452,7 +456,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "kernel_cfg": {k: d["conv"].plan.info()[k] for k in (
                 "kernel", "band_rows", "chunk_channels", "stages", "warps", "channels_per_warp",
                 "pixels_per_lane", "smem_bytes", "tile_h", "tile_w", "images_per_cta",
-                "jit_blocks", "jit_split", "code_bytes", "jit_compile_s", "jit_cache_hit")},
+                "jit_blocks", "jit_split", "jit_sched", "code_bytes", "jit_compile_s", "jit_cache_hit")},
         })
     cpu = None
     if not args.no_cpu and world >= 1:

@@ -99,6 +99,9 @@ typedef struct {
     int bands;                     /* JIT: row bands per image (pair), one CTA item each  */
     int jit_whole;                 /* JIT: 1 = one whole-program compile (no ABI calls)   */
     int jit_split;                 /* JIT: even blocks per group split in halves (tail)   */
+    int jit_sched;                 /* JIT launch schedule from skc_plan_tune: -1 untuned,
+                                      else bit 0 first round block-major, bit 1 GPC-major
+                                      item numbers, bits 4-7 cluster size                 */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).
@@ -220,6 +223,18 @@ int64_t skc_layout_offset(const skc_plan *plan, int c, int y, int x);
  * Errors: SKC_ERR_ARG (NULL), SKC_ERR_UNSUPPORTED (compile or link failed; message in
  * skc_last_error). */
 skc_status skc_plan_compile(skc_plan *plan);
+
+/* JIT kernel only: measure the launch-schedule variants of the plan's kernel on this device and
+ * keep the fastest (first round of work items spread over the channel blocks or block-major;
+ * work items numbered GPC-major or by cluster rank; clusters of 2 CTAs or none -- DESIGN.md
+ * Sec. 7.4).  Times each variant 3x on zero-filled scratch buffers of N images that it
+ * allocates and frees (input in the plan's layout + output + a 256 MiB L2 flush buffer, which
+ * is written before every timed launch); synchronous on `stream`.  Every variant computes
+ * bit-identical outputs, so tuning changes speed only.  Requires skc_plan_upload; call it
+ * outside stream capture.  *best_ms (may be NULL) receives the chosen variant's time.  No-op
+ * for other kernels.  Errors: SKC_ERR_ARG (NULL plan, N < 1), SKC_ERR_STATE (not uploaded),
+ * SKC_ERR_CUDA (allocation or launch failed). */
+skc_status skc_plan_tune(skc_plan *plan, int N, void *stream, double *best_ms);
 
 /* Static self-check of a plan (host only, no GPU): every kernel-private index the kernels
  * will dereference -- shared-memory windows and pixel slots against the stage and allocation

@@ -75,7 +75,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 16;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 17;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -145,6 +145,9 @@ struct JitPlan {
     // live across items).  Measured -1..-2% on conv3/4 (profiles/r01_jit_xpf.txt): the item
     // start was not waiting on its first stage; off by default
     int xpf = 0;
+    // launch schedule chosen by jit_tune (-1: default): first round block-major (order 3),
+    // GPC-major item numbers, cluster size
+    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1};
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
@@ -786,13 +789,14 @@ void emit_decode(Out &o, const JitPlan &jp, const char *tr, const char *rb, cons
         o("mul.lo.u32 %s, %s, %d;", tb, ta, jp.nblocks); // F * nblocks
         o("setp.lt.u32 %%p3, %s, %s;", tr, tb);
         o("@!%%p3 bra $ORD_REST%s;", tag);
-        if (jp.order == 3) {
-            o("div.u32 %s, %s, %s;", rb, tr, ta);
-            o("rem.u32 %s, %s, %s;", rc, tr, ta);
-        } else {
-            o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
-            o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
-        }
+        // p8: first round block-major (order 3, a launch-time choice: p_sched bit 0)
+        o("@%%p8 bra $FR3%s;", tag);
+        o("rem.u32 %s, %s, %d;", rb, tr, jp.nblocks);
+        o("div.u32 %s, %s, %d;", rc, tr, jp.nblocks);
+        o("bra.uni $ORD_DONE%s;", tag);
+        o("$FR3%s:", tag);
+        o("div.u32 %s, %s, %s;", rb, tr, ta);
+        o("rem.u32 %s, %s, %s;", rc, tr, ta);
         o("bra.uni $ORD_DONE%s;", tag);
         o("$ORD_REST%s:", tag);
         o("sub.u32 %s, %s, %s;", rc, tr, tb);           // t' = t - F*nb
@@ -816,9 +820,9 @@ std::string emit_entry(const JitPlan &jp) {
     o(".extern .shared .align 128 .b8 skc_smem[];");
     o(".visible .entry skc_jit_kernel(.param .u64 p_in, .param .u64 p_out, .param .u64 p_lm, "
       ".param .u64 p_bias, .param .u32 p_N, .param .u32 p_relu, .param .u32 p_opad, "
-      ".param .u32 p_olay, .param .u64 p_vid)");
+      ".param .u32 p_olay, .param .u64 p_vid, .param .u32 p_sched)");
     o("{");
-    o(".reg .pred %%p<8>;");
+    o(".reg .pred %%p<10>;");
     o(".reg .b32 %%r<80>;");
     o(".reg .b64 %%rd<24>;");
     o("ld.param.u64 %%rd0, [p_in];");
@@ -847,6 +851,9 @@ std::string emit_entry(const JitPlan &jp) {
     // SM s is vid[s], the SM's position in a GPC-major order (topo.cu), so the CTAs of one GPC
     // take neighbouring items -- the same channel block -- and share the GPC's instruction
     // cache.  p_vid = 0: item t = cluster-major CTA rank.
+    o("ld.param.u32 %%r63, [p_sched];");
+    o("and.b32 %%r63, %%r63, 1;");
+    o("setp.ne.u32 %%p8, %%r63, 0;");
     o("ld.param.u64 %%rd21, [p_vid];");
     o("setp.eq.u64 %%p0, %%rd21, 0;");
     o("@%%p0 bra $VID_DONE;");
@@ -1968,6 +1975,8 @@ const void *jit_lanemap(const JitPlan *jp) { return jp->lanemap.data(); }
 void jit_info(const JitPlan *jp, JitInfo *o) {
     o->TY = jp->TY; o->TX = jp->TX; o->PX = jp->PX; o->M = jp->M; o->NW = jp->NW;
     o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks; o->split = jp->split;
+    o->sched = jp->t_order3.load() < 0 ? -1
+                                       : (jp->t_order3.load() | (jp->t_vid.load() << 1) | (jp->t_cs.load() << 4));
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;
@@ -2027,7 +2036,7 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
     // on neighbouring image groups, so they share instruction-cache lines (B200 packs 148 SMs
     // into 74 pairs exactly; +2-7% measured, profiles/r01_jit_cluster.txt).  SKC_JIT_CLUSTER
     // overrides (1 = no clusters).
-    int cs = 2;
+    int cs = jp->t_cs.load() > 0 ? jp->t_cs.load() : 2;
     if (const char *e = std::getenv("SKC_JIT_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(e)));
     if (items < 2 * cs) cs = 1;
     int64_t grid = std::min<int64_t>(items, int64_t(nsm) * per_sm);
@@ -2086,14 +2095,85 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
         return !e || std::atoi(e) != 0;
     }();
     const void *vid = nullptr;
-    if (vid_on && per_sm == 1 && grid == nsm && jp->dyn != 2 && cs <= 2)
+    const bool vid_want = jp->t_vid.load() >= 0 ? jp->t_vid.load() != 0 : vid_on;
+    if (vid_want && per_sm == 1 && grid == nsm && jp->dyn != 2 && cs <= 2)
         vid = sm_gpc_order_device(dev, true);
+    unsigned sched = jp->t_order3.load() >= 0 ? unsigned(jp->t_order3.load()) : (jp->order == 3 ? 1u : 0u);
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
                      vid ? "on" : "off");
     void *args[] = {(void *)&in, (void *)&out, (void *)&d_lanemap, (void *)&bias,
-                    (void *)&un, (void *)&relu, (void *)&opad, (void *)&olay, (void *)&vid};
+                    (void *)&un, (void *)&relu, (void *)&opad, (void *)&olay, (void *)&vid,
+                    (void *)&sched};
     return cudaLaunchKernelExC(&lc, reinterpret_cast<const void *>(jp->kern), args);
+}
+
+// Launch-schedule tuning: time the variants (first round spread / block-major, GPC-major item
+// numbers on / off, clusters of 2 / none) of this plan's kernel on zero-filled scratch buffers
+// of N images, with the L2 flushed before every timed launch (code and data start cold, as in
+// bench.py), and keep the fastest.  Every variant computes bit-identical outputs (scheduling
+// only; tests/test_gpu_parity.py::test_jit_tuning_knobs_bitwise).  Synchronous on `st`.
+int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double *best_ms,
+             std::string *msg) {
+    const JitInput &in = jp->in;
+    const int sw = jp->pair ? 2 : 1;
+    const size_t in_bytes = size_t((N + sw - 1) / sw) * size_t(in.C) * in.Hp * in.Wp * sw * 4;
+    const size_t out_bytes = size_t(N) * size_t(in.K) * in.Ho * in.Wo * 4;
+    const size_t flush_bytes = size_t(256) << 20;
+    float *d_in = nullptr, *d_out = nullptr;
+    void *d_flush = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto cleanup = [&] {
+        if (d_in) cudaFree(d_in);
+        if (d_out) cudaFree(d_out);
+        if (d_flush) cudaFree(d_flush);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    };
+    if (cudaMalloc(&d_in, in_bytes) != cudaSuccess || cudaMalloc(&d_out, out_bytes) != cudaSuccess ||
+        cudaMalloc(&d_flush, flush_bytes) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+        cudaEventCreate(&e1) != cudaSuccess || cudaMemsetAsync(d_in, 0, in_bytes, st) != cudaSuccess) {
+        *msg = std::string("tune setup: ") + cudaGetErrorString(cudaGetLastError());
+        cleanup();
+        return SKC_ERR_CUDA;
+    }
+    const Epilogue epi{};
+    double best = -1;
+    int bo = 0, bv = 1, bc = 2;
+    for (int o3 = 0; o3 < 2; ++o3)
+        for (int v = 1; v >= 0; --v)
+            for (int c = 2; c >= 1; --c) {
+                jp->t_order3 = o3;
+                jp->t_vid = v;
+                jp->t_cs = c;
+                double tot = 0;
+                for (int rep = 0; rep < 4; ++rep) {
+                    cudaMemsetAsync(d_flush, rep, flush_bytes, st);
+                    cudaEventRecord(e0, st);
+                    cudaError_t e = jit_launch(jp, d_in, d_out, d_lanemap, N, epi, st, msg);
+                    cudaEventRecord(e1, st);
+                    if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
+                        *msg = std::string("tune launch: ") + cudaGetErrorString(e);
+                        cleanup();
+                        return SKC_ERR_CUDA;
+                    }
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    if (rep) tot += ms;  // the first launch is a warm-up
+                }
+                if (best < 0 || tot < best) {
+                    best = tot;
+                    bo = o3; bv = v; bc = c;
+                }
+            }
+    jp->t_order3 = bo;
+    jp->t_vid = bv;
+    jp->t_cs = bc;
+    if (best_ms) *best_ms = best / 3;
+    if (std::getenv("SKC_JIT_DEBUG"))
+        std::fprintf(stderr, "skc jit tune: order3 %d vid %d cluster %d: %.4f ms\n", bo, bv, bc, best / 3);
+    cleanup();
+    return SKC_OK;
 }
 
 int jit_verify_code(const JitPlan *jp, std::string *msg) { return jit_verify(jp, msg); }

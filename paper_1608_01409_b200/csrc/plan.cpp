@@ -874,6 +874,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.bands = 0;
     i.jit_whole = 0;
     i.jit_split = 0;
+    i.jit_sched = -1;
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -886,6 +887,7 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
         i.bands = j.bands;
         i.jit_whole = j.whole;
         i.jit_split = j.split;
+        i.jit_sched = j.sched;
     }
     return ok();
 }
@@ -1132,6 +1134,18 @@ skc_status skc_plan_compile(skc_plan *p) {
     std::string msg;
     const int r = jit_compile(p->jit, &msg);
     if (r != SKC_OK) return fail(skc_status(r), "JIT compile: %s", msg.c_str());
+    return ok();
+}
+
+skc_status skc_plan_tune(skc_plan *p, int N, void *stream, double *best_ms) {
+    if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (N < 1) return fail(SKC_ERR_ARG, "N = %d < 1", N);
+    if (p->kernel != SKC_KERNEL_JIT) return ok();
+    if (!p->d_ws) return fail(SKC_ERR_STATE, "plan not uploaded (call skc_plan_upload)");
+    std::string msg;
+    const char *ws = static_cast<const char *>(p->d_ws);
+    const int r = jit_tune(p->jit, ws + p->off_lanemap, N, (cudaStream_t)stream, best_ms, &msg);
+    if (r != SKC_OK) return fail(skc_status(r), "tune: %s", msg.c_str());
     return ok();
 }
 

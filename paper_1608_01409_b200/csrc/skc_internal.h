@@ -120,6 +120,7 @@ struct JitInfo {
     int bands; // row bands per image (pair) -- work items per image group
     int whole; // 1: compiled as one whole program
     int split; // even blocks per group split into halves
+    int sched; // tuned launch schedule (skc_info.jit_sched), -1 untuned
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).
@@ -135,6 +136,8 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
 // Static check: tables + the emitted code decoded back to the canonical CSR (host).
 int jit_verify_code(const JitPlan *jp, std::string *msg);
 // GPC-major SM order (topo.cu): vid[smid], empty when unknown.  Synchronous, once per device.
+int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double *best_ms,
+             std::string *msg);
 const std::vector<uint16_t> &sm_gpc_order(int dev);
 const uint16_t *sm_gpc_order_device(int dev, bool peek);
 void jit_destroy(JitPlan *jp);

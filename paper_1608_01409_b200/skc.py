@@ -29,7 +29,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
            "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc",
-           "skc_plan_compile", "skc_sparse_conv_forward_into")
+           "skc_plan_compile", "skc_sparse_conv_forward_into", "skc_plan_tune")
 
 
 class SkcError(RuntimeError):
@@ -51,7 +51,7 @@ class skc_info(ctypes.Structure):
         ("jit_compiled", ctypes.c_int), ("jit_cache_hit", ctypes.c_int),
         ("jit_compile_s", ctypes.c_double), ("code_bytes", ctypes.c_size_t),
         ("model_instr_per_image", ctypes.c_double), ("layout", ctypes.c_int), ("bands", ctypes.c_int), ("jit_whole", ctypes.c_int),
-        ("jit_split", ctypes.c_int)]
+        ("jit_split", ctypes.c_int), ("jit_sched", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -96,6 +96,7 @@ def lib():
             "skc_plan_info": [_P, ctypes.POINTER(skc_info)],
             "skc_plan_verify": [_P],
             "skc_plan_compile": [_P],
+            "skc_plan_tune": [_P, _I, _P, ctypes.POINTER(ctypes.c_double)],
             "skc_plan_csr": [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
             "skc_plan_perm": [_P, ctypes.POINTER(_P)],
             "skc_plan_upload": [_P, _P, ctypes.c_size_t, _P],
@@ -225,6 +226,14 @@ def skc_plan_verify(plan: Plan):
 def skc_plan_compile(plan: Plan):
     """JIT kernel: generate + compile + link the plan's code now (host only, no GPU)."""
     _check(lib().skc_plan_compile(plan.handle))
+
+
+def skc_plan_tune(plan: Plan, N: int, stream=None) -> float:
+    """JIT kernel: time the launch-schedule variants on N scratch images, keep the fastest;
+    returns its time in ms (0.0 for other kernels).  Outputs are bitwise unaffected."""
+    ms = ctypes.c_double(0.0)
+    _check(lib().skc_plan_tune(plan.handle, int(N), _stream(stream), ctypes.byref(ms)))
+    return ms.value
 
 
 def skc_plan_upload(plan: Plan, workspace, stream=None):
@@ -404,6 +413,11 @@ class SparseConv2d:
     def padded_shape(self, N):
         """Padded-input buffer shape in the plan's layout (NCHW, or image pairs)."""
         return padded_shape(self.geom, N)
+
+    def tune(self, N: int = 256, stream=None) -> float:
+        """JIT plans: pick the fastest launch schedule for batches of N on this device
+        (skc_plan_tune); returns the chosen variant's time in ms."""
+        return skc_plan_tune(self.plan, N, stream)
 
     def forward_padded(self, xp, out=None, stream=None, N=None):
         """Conv of a padded input in the plan's layout.  N defaults to out's batch, else to

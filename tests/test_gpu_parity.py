@@ -608,3 +608,28 @@ def test_jit_dynamic_counter_resets_across_launches(dyn, monkeypatch):
         g.replay()
         torch.cuda.synchronize()
         np.testing.assert_array_equal(yj.cpu().numpy().view(np.uint32), yd.view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_plan_tune_keeps_outputs_bitwise():
+    """skc_plan_tune times the launch-schedule variants on scratch buffers and keeps the
+    fastest; the plan's outputs before and after tuning are bit-identical, and tuning a
+    non-JIT plan is a no-op."""
+    rng = np.random.default_rng(47)
+    layer = wl.Layer("t1", 64, 48, 13, 13, 3, 3, 1, 1, 2, 0.9, 0.01)
+    w, x = wl.random_tensors(rng, layer, 37)
+    jit = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                      skc.SKC_KERNEL_JIT)
+    xd = torch.from_numpy(x).cuda()
+    xp = torch.empty(jit.padded_shape(37), device="cuda")
+    skc.skc_pad_input(jit.plan, xd, xp, 37)
+    y0 = jit.forward_padded(xp).cpu().numpy()
+    ms = jit.tune(37)
+    assert ms > 0
+    y1 = jit.forward_padded(xp).cpu().numpy()
+    np.testing.assert_array_equal(y0.view(np.uint32), y1.view(np.uint32))
+    direct = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                         layer.groups, skc.SKC_KERNEL_DIRECT)
+    assert direct.tune(37) == 0.0
+    with pytest.raises(skc.SkcError):
+        skc.skc_plan_tune(jit.plan, 0)
