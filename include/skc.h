@@ -227,7 +227,7 @@ skc_status skc_plan_compile(skc_plan *plan);
 /* JIT kernel only: measure the launch-schedule variants of the plan's kernel on this device and
  * keep the fastest (first round of work items spread over the channel blocks or block-major;
  * work items numbered GPC-major or by cluster rank; clusters of 2 CTAs or none -- DESIGN.md
- * Sec. 7.4).  Times each variant 3x on zero-filled scratch buffers of N images that it
+ * Sec. 7.4).  Times each variant 5x on zero-filled scratch buffers of N images that it
  * allocates and frees (input in the plan's layout + output + a 256 MiB L2 flush buffer, which
  * is written before every timed launch); synchronous on `stream`.  Every variant computes
  * bit-identical outputs, so tuning changes speed only.  Requires skc_plan_upload; call it

@@ -2147,7 +2147,7 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 jp->t_vid = v;
                 jp->t_cs = c;
                 double tot = 0;
-                for (int rep = 0; rep < 4; ++rep) {
+                for (int rep = 0; rep < 6; ++rep) {
                     cudaMemsetAsync(d_flush, rep, flush_bytes, st);
                     cudaEventRecord(e0, st);
                     cudaError_t e = jit_launch(jp, d_in, d_out, d_lanemap, N, epi, st, msg);
@@ -2169,9 +2169,9 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
     jp->t_order3 = bo;
     jp->t_vid = bv;
     jp->t_cs = bc;
-    if (best_ms) *best_ms = best / 3;
+    if (best_ms) *best_ms = best / 5;
     if (std::getenv("SKC_JIT_DEBUG"))
-        std::fprintf(stderr, "skc jit tune: order3 %d vid %d cluster %d: %.4f ms\n", bo, bv, bc, best / 3);
+        std::fprintf(stderr, "skc jit tune: order3 %d vid %d cluster %d: %.4f ms\n", bo, bv, bc, best / 5);
     cleanup();
     return SKC_OK;
 }
