@@ -272,6 +272,14 @@ skc_status skc_model_window(const skc_layer_cost *cost, const skc_platform *p, s
  * memory word bandwidth; the analogue of the paper's SGEMM / STREAM calibration,
  * PAPER.md:531-532).  d_scratch: >= 4 MiB device buffer.  Each writes the elapsed
  * device milliseconds and the operation count it performed.  Synchronous. */
+/* Diagnostic: the GPC-major SM order the JIT kernel numbers its work items by (topo.cu;
+ * DESIGN.md Sec. 7.4) for the current device: vid[smid] = position of SM smid when the SMs are
+ * listed GPC by GPC, learned by launching thread-block clusters (which never span GPCs).
+ * vid: host array of `cap` ints; *nsm receives the SM count.  Runs the probe kernels on the
+ * first call per device (synchronous).  Errors: SKC_ERR_ARG (NULL, cap < SM count),
+ * SKC_ERR_UNSUPPORTED (the probe could not group the SMs). */
+skc_status skc_sm_topology(int *vid, int cap, int *nsm);
+
 skc_status skc_bench_ffma(void *d_scratch, int blocks, int iters, double *ms, double *flops);
 skc_status skc_bench_lds(void *d_scratch, int blocks, int iters, double *ms, double *bytes);
 

@@ -1137,6 +1137,18 @@ skc_status skc_plan_compile(skc_plan *p) {
     return ok();
 }
 
+skc_status skc_sm_topology(int *vid, int cap, int *nsm) {
+    if (!vid || !nsm) return fail(SKC_ERR_ARG, "NULL pointer");
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(SKC_ERR_CUDA, "no CUDA device");
+    const std::vector<uint16_t> &v = sm_gpc_order(dev);
+    if (v.empty()) return fail(SKC_ERR_UNSUPPORTED, "SM topology probe failed");
+    *nsm = int(v.size());
+    if (cap < int(v.size())) return fail(SKC_ERR_ARG, "cap %d < %zu SMs", cap, v.size());
+    for (size_t i = 0; i < v.size(); ++i) vid[i] = int(v[i]);
+    return ok();
+}
+
 skc_status skc_plan_tune(skc_plan *p, int N, void *stream, double *best_ms) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
     if (N < 1) return fail(SKC_ERR_ARG, "N = %d < 1", N);

@@ -29,7 +29,8 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
            "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc",
-           "skc_plan_compile", "skc_sparse_conv_forward_into", "skc_plan_tune")
+           "skc_plan_compile", "skc_sparse_conv_forward_into", "skc_plan_tune",
+           "skc_sm_topology")
 
 
 class SkcError(RuntimeError):
@@ -97,6 +98,7 @@ def lib():
             "skc_plan_verify": [_P],
             "skc_plan_compile": [_P],
             "skc_plan_tune": [_P, _I, _P, ctypes.POINTER(ctypes.c_double)],
+            "skc_sm_topology": [ctypes.POINTER(_I), _I, ctypes.POINTER(_I)],
             "skc_plan_csr": [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
             "skc_plan_perm": [_P, ctypes.POINTER(_P)],
             "skc_plan_upload": [_P, _P, ctypes.c_size_t, _P],
@@ -226,6 +228,14 @@ def skc_plan_verify(plan: Plan):
 def skc_plan_compile(plan: Plan):
     """JIT kernel: generate + compile + link the plan's code now (host only, no GPU)."""
     _check(lib().skc_plan_compile(plan.handle))
+
+
+def skc_sm_topology(cap: int = 1024):
+    """GPC-major SM order of the current device: list vid[smid] (diagnostic)."""
+    arr = (ctypes.c_int * cap)()
+    n = ctypes.c_int(0)
+    _check(lib().skc_sm_topology(arr, cap, ctypes.byref(n)))
+    return list(arr[:n.value])
 
 
 def skc_plan_tune(plan: Plan, N: int, stream=None) -> float:

@@ -659,3 +659,16 @@ def test_plan_tune_keeps_outputs_bitwise():
     assert direct.tune(37) == 0.0
     with pytest.raises(skc.SkcError):
         skc.skc_plan_tune(jit.plan, 0)
+
+
+@pytest.mark.gpu
+def test_sm_topology_is_a_gpc_major_permutation():
+    """The topology probe (clusters never span a GPC) yields a permutation of the SM ids in
+    which every cluster-mate group is contiguous: the two SMs of a 2-CTA cluster (one TPC)
+    always get neighbouring positions."""
+    vid = skc.skc_sm_topology()
+    n = torch.cuda.get_device_properties(0).multi_processor_count
+    assert len(vid) == n
+    assert sorted(vid) == list(range(n))
+    tpc_adjacent = sum(vid[2 * k + 1] == vid[2 * k] + 1 for k in range(n // 2))
+    assert tpc_adjacent >= 0.9 * (n // 2), tpc_adjacent
