@@ -260,7 +260,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             conv.tune(per_gpu)
         x_host = torch.from_numpy(wl.gen_input(cfg.cfg_id, li, L, n0, n1))
         x = x_host.to(dev)
-        xp = torch.empty(conv.padded_shape(per_gpu), device=dev)
+        # (the raw layout is the NCHW input itself: the kernel pads while staging, and
+        # skc_pad_input on the same buffer is a no-op)
+        xp = x if conv.geom["layout"] == skc.SKC_LAYOUT_RAW else torch.empty(conv.padded_shape(per_gpu), device=dev)
         out = torch.empty(conv.out_shape(per_gpu), device=dev)
         layers.append(dict(L=L, w=w, conv=conv, x=x, xp=xp, out=out, x_host=x_host,
                            nnz=int(conv.geom["nnz"])))

@@ -72,8 +72,11 @@ typedef enum {
  *   SKC_LAYOUT_PAIRS  [ceil(N/2)][C][Hp][Wp][2]: images 2p and 2p+1 interleaved element by
  *                     element, so one aligned 8-byte load feeds a packed FFMA2 over both
  *                     images (JIT kernel); an odd batch's last pair has a zero second image.
+ *   SKC_LAYOUT_RAW    [N][C][H][W], unpadded: the JIT kernel pads and pair-interleaves while
+ *                     staging (SKC_JIT_RAW=1), so no pad pass is needed; skc_pad_input copies
+ *                     (or, in place, does nothing).
  * skc_info.layout says which one a plan reads; skc_pad_input writes it. */
-typedef enum { SKC_LAYOUT_NCHW = 0, SKC_LAYOUT_PAIRS = 1 } skc_layout;
+typedef enum { SKC_LAYOUT_NCHW = 0, SKC_LAYOUT_PAIRS = 1, SKC_LAYOUT_RAW = 2 } skc_layout;
 
 typedef struct {
     int K, C, R, S, H, W, stride, pad, groups;

@@ -145,6 +145,13 @@ struct JitPlan {
     // live across items).  Measured -1..-2% on conv3/4 (profiles/r01_jit_xpf.txt): the item
     // start was not waiting on its first stage; off by default
     int xpf = 0;
+    // raw staging (SKC_JIT_RAW): the kernel reads the unpadded NCHW input; every thread
+    // cp.async-copies its fixed input positions (stab) of each chunk into the padded,
+    // pair-interleaved stage, whose halo is zeroed once -- no pad pass
+    int raw = 0;
+    int kmax = 0;                  // staged positions per thread per (slot, channel)
+    std::vector<uint32_t> stab;    // [NB][NW*32][kmax][2]: raw offset (img*C*H*W + y*W + x, or
+                                   // ~0 = none), stage offset (((y+pad)*Wp + x+pad)*2 + img)
     // launch schedule chosen by jit_tune (-1: default): first round block-major (order 3),
     // GPC-major item numbers, cluster size
     std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1};
@@ -414,9 +421,29 @@ const char *kBlkParams =
     "(.param .b32 q_lb, .param .b32 q_sm, .param .b64 q_out, .param .b32 q_mask, "
     ".param .b32 q_nsl, .param .b64 q_bias, .param .b32 q_relu, .param .b32 q_rs, "
     ".param .b64 q_cs, .param .b32 q_ps, .param .b64 q_bo, .param .b32 q_dry, "
-    ".param .b32 q_ph, .param .b32 q_info, .param .b32 q_ninfo, .param .b32 q_nnsl)";
+    ".param .b32 q_ph, .param .b32 q_info, .param .b32 q_ninfo, .param .b32 q_nnsl, "
+    ".param .b64 q_gin, .param .b32 q_nimg, .param .b64 q_stab)";
 
 int chunk_channels(const JitPlan &jp, int i) { return std::min(jp.CB, jp.in.Cg - i * jp.CB); }
+
+// Raw staging of chunk i into (logical) stage s: every thread copies its kmax positions of
+// every (slot, channel) with 4-byte cp.async (zero-filled when the image is past the batch),
+// then arrives on the stage's barrier once its copies land (count = all threads).
+void emit_raw_fill(Out &o, const JitPlan &jp, int i, int s) {
+    const JitInput &in = jp.in;
+    const int H = in.Hp - 2 * in.pad, W = in.Wp - 2 * in.pad, NSL = jp.NI / 2;
+    const int cn = chunk_channels(jp, i);
+    for (int j = 0; j < NSL; ++j)
+        for (int cl = 0; cl < cn; ++cl)
+            for (int k = 0; k < jp.kmax; ++k) {
+                const long long goff =
+                    ((long long)(i * jp.CB + cl) * H * W + (long long)j * 2 * in.C * H * W) * 4;
+                const long long soff = ((long long)j * jp.img_stride + (long long)cl * jp.plane * 2) * 4;
+                o("cp.async.ca.shared.global [%%rak%d+%lld], [%%rgk%d+%lld], 4, %%rz%d;",
+                  s * jp.kmax + k, soff, k, goff, j * jp.kmax + k);
+            }
+    o("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%%rw%d];", s);
+}
 
 std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
                        const std::vector<std::vector<JNz>> &per_c) {
@@ -451,6 +478,16 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o(".reg .b64 %%wt;");
     o(".reg .pred %%pe<8>;");
     o(".reg .b64 %%rdp<4>;");
+    if (jp.raw) {
+        o(".reg .b64 %%rgin, %%rstab;");
+        o(".reg .b64 %%rgk<%d>;", jp.kmax);
+        o(".reg .b32 %%rgo<%d>;", jp.kmax);
+        o(".reg .b32 %%rso<%d>;", jp.kmax);
+        o(".reg .b32 %%rz<%d>;", (jp.NI / 2) * jp.kmax);
+        o(".reg .b32 %%rak<%d>;", jp.NS * jp.kmax);
+        o(".reg .b32 %%rnimg, %%rimg, %%rtt;");
+        o(".reg .pred %%ppk, %%ppt;");
+    }
     o(".reg .f32 %%e<4>;");
     o("ld.param.b32 %%r0, [q_lb];");
     o("ld.param.b32 %%r1, [q_sm];");
@@ -500,6 +537,28 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     }
     o("bra.uni $DRYRET;");
     o("$REAL:");
+    if (jp.raw) {
+        // this thread's staged positions (raw offset, stage offset) and per-slot copy sizes
+        o("ld.param.b64 %%rgin, [q_gin];");
+        o("ld.param.b32 %%rnimg, [q_nimg];");
+        o("ld.param.b64 %%rstab, [q_stab];");
+        for (int k = 0; k < jp.kmax; ++k) {
+            o("ld.global.nc.v2.u32 {%%rgo%d, %%rso%d}, [%%rstab+%d];", k, k, 8 * k);
+            o("setp.ne.u32 %%ppk, %%rgo%d, -1;", k);
+            o("mul.wide.u32 %%rgk%d, %%rgo%d, 4;", k, k);
+            o("add.u64 %%rgk%d, %%rgk%d, %%rgin;", k, k);
+            o("and.b32 %%rimg, %%rso%d, 1;", k);
+            for (int j = 0; j < jp.NI / 2; ++j) {
+                o("add.u32 %%rtt, %%rimg, %d;", 2 * j);
+                o("setp.lt.u32 %%ppt, %%rtt, %%rnimg;");
+                o("and.pred %%ppt, %%ppt, %%ppk;");
+                o("selp.u32 %%rz%d, 4, 0, %%ppt;", j * jp.kmax + k);
+            }
+            o("shl.b32 %%rso%d, %%rso%d, 2;", k, k);
+            for (int s = 0; s < jp.NS; ++s) o("add.u32 %%rak%d, %%rs%d, %%rso%d;", s * jp.kmax + k, s, k);
+        }
+        for (int i = 0; i < std::min(jp.NS, jp.nchunks); ++i) emit_raw_fill(o, jp, i, i);
+    }
 
     Need nd;
     int since_sync = 0;
@@ -589,6 +648,14 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             }
         }
         o("@%%p8 bra $DRYRET;");
+        if (jp.raw) {
+            // every warp is done with the stage: all threads stage chunk i + NS into it
+            if (i + jp.NS < jp.nchunks) {
+                o("bar.sync 1, %d;", jp.NW * 32);
+                emit_raw_fill(o, jp, i + jp.NS, s);
+            }
+            continue;
+        }
         // release the stage; the last warp out refills it with chunk i + NS
         if (i + jp.NS < jp.nchunks) {
             const int nxt = i + jp.NS;
@@ -919,8 +986,10 @@ std::string emit_entry(const JitPlan &jp) {
             o("st.param.b32 [t9], 0;\nst.param.b64 [t10], 0;\nst.param.b32 [t11], %%r53;");
             o("st.param.b32 [t12], 0;\nst.param.b32 [t13], %d;", jp.off_info);
             o("st.param.b32 [t14], %d;\nst.param.b32 [t15], 0;", jp.off_info);
+            o(".param .b64 t16;\n.param .b32 t17;\n.param .b64 t18;");
+            o("st.param.b64 [t16], 0;\nst.param.b32 [t17], 0;\nst.param.b64 [t18], 0;");
             o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, "
-              "t14, t15);", b);
+              "t14, t15, t16, t17, t18);", b);
             o("}");
             o("bra.uni $DRY_NEXT;");
         }
@@ -952,6 +1021,20 @@ std::string emit_entry(const JitPlan &jp) {
         o("@%%p0 atom.global.add.u32 %%r56, [%%rd20], %s;", cl ? "%r36" : "1");
     }
     const int NSL = jp.NI / sw;
+    if (jp.raw) {
+        // the stages' halo (and every position no thread stages) stays zero for the whole
+        // kernel: zero all stage memory once
+        o("shl.b32 %%r62, %%r3, 4;");
+        o("$ZERO:");
+        o("setp.ge.u32 %%p0, %%r62, %d;", jp.NS * jp.stage_bytes);
+        o("@%%p0 bra $ZERO_DONE;");
+        o("add.u32 %%r61, %%r11, %%r62;");
+        o("st.shared.v4.u32 [%%r61], {0, 0, 0, 0};");
+        o("add.u32 %%r62, %%r62, %d;", jp.NW * 32 * 16);
+        o("bra.uni $ZERO;");
+        o("$ZERO_DONE:");
+        o("bar.sync 0;");
+    }
     if (jp.xpf) {
         // cross-item staging: the barriers live for the whole kernel (phases continue from
         // item to item), so they are initialised once here
@@ -1037,6 +1120,24 @@ std::string emit_entry(const JitPlan &jp) {
             o("setp.eq.u32 %%p3, %%r7, %d;", b);
             o("@%%p3 mov.u32 %%r10, %d;", jp.bgrp[size_t(b)]);
         }
+    if (jp.raw) {
+        // raw input of image n0, channel g*Cg: in + (n0*C + g*Cg)*H*W*4; this thread's
+        // staging entries: after the lane tables and counters, [band][thread][kmax]
+        const long long HW = (long long)(in.Hp - 2 * in.pad) * (in.Wp - 2 * in.pad);
+        o("cvt.u64.u32 %%rd16, %%r8;");
+        o("mul.lo.u64 %%rd16, %%rd16, %lld;", (long long)in.C * HW * 4);
+        o("cvt.u64.u32 %%rd18, %%r10;");
+        o("mul.lo.u64 %%rd18, %%rd18, %lld;", (long long)in.Cg * HW * 4);
+        o("add.u64 %%rd16, %%rd16, %%rd18;");
+        o("add.u64 %%rd16, %%rd0, %%rd16;");
+        o("mad.lo.u32 %%r62, %%r48, %d, %%r3;", jp.NW * 32);
+        o("mul.wide.u32 %%rd17, %%r62, %d;", jp.kmax * 8);
+        o("add.u64 %%rd17, %%rd17, %%rd2;");
+        o("add.u64 %%rd17, %%rd17, %d;", jp.NB * jp.NW * 32 * 16 + 16);
+    } else {
+        o("mov.u64 %%rd16, 0;");
+        o("mov.u64 %%rd17, 0;");
+    }
     if (!jp.dyn) o("bar.sync 0;");               // every warp is done with the previous item
                                                  // (dynamic: the fetch barrier already is)
     o("setp.ne.u32 %%p0, %%r3, 0;");
@@ -1076,10 +1177,15 @@ std::string emit_entry(const JitPlan &jp) {
         o("setp.eq.u32 %%p4, %%r34, 0;");
         for (int s = 0; s < jp.NS; ++s) {
             o("@%%p4 mbarrier.inval.shared::cta.b64 [%%r11+%d];", jp.off_bar + 8 * s);
-            o("mbarrier.init.shared::cta.b64 [%%r11+%d], 1;", jp.off_bar + 8 * s);
+            // raw staging: every thread arrives once per fill (cp.async ... arrive.noinc)
+            o("mbarrier.init.shared::cta.b64 [%%r11+%d], %d;", jp.off_bar + 8 * s, jp.raw ? jp.NW * 32 : 1);
             o("st.shared.u32 [%%r11+%d], 0;", jp.off_cnt + 4 * s);
         }
         o("mov.u32 %%r34, 0;");
+    }
+    if (jp.raw) {
+        o("fence.mbarrier_init.release.cluster;");
+        o("bra.uni $INIT_DONE;");                   // the block stages its own chunks
     }
     emit_info("%r8", "%r10", "%r41", tab0, "");
     o("fence.mbarrier_init.release.cluster;");
@@ -1211,8 +1317,10 @@ std::string emit_entry(const JitPlan &jp) {
         o("st.param.b32 [t9], %%r40;\nst.param.b64 [t10], %%rd12;\nst.param.b32 [t11], 0;");
         o("st.param.b32 [t12], %%r74;\nst.param.b32 [t13], %%r76;");
         o("st.param.b32 [t14], %%r77;\nst.param.b32 [t15], %%r75;");
+        o(".param .b64 t16;\n.param .b32 t17;\n.param .b64 t18;");
+        o("st.param.b64 [t16], %%rd16;\nst.param.b32 [t17], %%r9;\nst.param.b64 [t18], %%rd17;");
         o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, "
-          "t14, t15);", b);
+          "t14, t15, t16, t17, t18);", b);
         o("}");
         o("bra.uni $NEXT;");
     }
@@ -1827,6 +1935,46 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     // save/restore of callee-saved registers: -8-10% measured, profiles/r01_jit_whole.txt)
     choose_blocks(jp, n_hint);
     if (jp.dyn) jp.xpf = 0;  // the next item must be known an item ahead (static order)
+    // raw staging (SKC_JIT_RAW=1, pair layout): per band, the padded input rows its lanes'
+    // windows read; their interior positions (image, row, column) dealt to the CTA's threads
+    // round-robin, (column, image) fastest so a warp's copies are consecutive stage words
+    if (const char *e = std::getenv("SKC_JIT_RAW")) jp.raw = (std::atoi(e) && jp.pair) ? 1 : 0;
+    if (jp.raw) {
+        jp.xpf = 0;
+        const int H = in.Hp - 2 * in.pad, W = in.Wp - 2 * in.pad, T = jp.NW * 32;
+        std::vector<std::vector<uint32_t>> pos(size_t(jp.NB));
+        for (int b = 0; b < jp.NB; ++b) {
+            int lo = in.Hp, hi = 0;
+            for (int l = 0; l < T; ++l) {
+                const uint32_t *e = jp.lanemap.data() + (size_t(b) * T + size_t(l)) * 4;
+                const int y0 = int((e[1] >> 12) & 4095);
+                lo = std::min(lo, y0 * in.stride);
+                hi = std::max(hi, (y0 + jp.TY - 1) * in.stride + in.R);
+            }
+            for (int r = std::max(lo, in.pad); r < std::min(hi, in.pad + H); ++r)
+                for (int x = 0; x < W; ++x)
+                    for (int img = 0; img < 2; ++img) {
+                        pos[size_t(b)].push_back(uint32_t(img) * uint32_t(in.C * H * W) +
+                                                 uint32_t((r - in.pad) * W + x));
+                        pos[size_t(b)].push_back(uint32_t((r * in.Wp + x + in.pad) * 2 + img));
+                    }
+            jp.kmax = std::max(jp.kmax, int((pos[size_t(b)].size() / 2 + T - 1) / T));
+        }
+        jp.stab.assign(size_t(jp.NB) * T * jp.kmax * 2, 0u);
+        for (int b = 0; b < jp.NB; ++b)
+            for (int t = 0; t < T; ++t)
+                for (int k = 0; k < jp.kmax; ++k) {
+                    uint32_t *e = jp.stab.data() + ((size_t(b) * T + size_t(t)) * jp.kmax + size_t(k)) * 2;
+                    const size_t q = size_t(t) + size_t(k) * T;
+                    if (q < pos[size_t(b)].size() / 2) {
+                        e[0] = pos[size_t(b)][2 * q];
+                        e[1] = pos[size_t(b)][2 * q + 1];
+                    } else {
+                        e[0] = 0xffffffffu;  // no position
+                        e[1] = 0;
+                    }
+                }
+    }
     jp.whole = jp.code_instr <= kWholeMaxInstr ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
@@ -1968,13 +2116,19 @@ int jit_compile(JitPlan *jp, std::string *msg) {
     return SKC_OK;
 }
 
-// device image: the lane tables, then 16 bytes of (zeroed) scheduling counters
-size_t jit_lanemap_bytes(const JitPlan *jp) { return jp->lanemap.size() * 4 + 16; }
-const void *jit_lanemap(const JitPlan *jp) { return jp->lanemap.data(); }
+// device image: the lane tables, 16 bytes of (zeroed) scheduling counters, then (raw staging)
+// the per-thread staging tables
+size_t jit_image_bytes(const JitPlan *jp) { return jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4; }
+void jit_image(const JitPlan *jp, void *dst) {
+    char *d = static_cast<char *>(dst);
+    std::memcpy(d, jp->lanemap.data(), jp->lanemap.size() * 4);
+    std::memset(d + jp->lanemap.size() * 4, 0, 16);
+    if (!jp->stab.empty()) std::memcpy(d + jp->lanemap.size() * 4 + 16, jp->stab.data(), jp->stab.size() * 4);
+}
 
 void jit_info(const JitPlan *jp, JitInfo *o) {
     o->TY = jp->TY; o->TX = jp->TX; o->PX = jp->PX; o->M = jp->M; o->NW = jp->NW;
-    o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks; o->split = jp->split;
+    o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks; o->split = jp->split; o->raw = jp->raw;
     o->sched = jp->t_order3.load() < 0 ? -1
                                        : (jp->t_order3.load() | (jp->t_vid.load() << 1) | (jp->t_cs.load() << 4));
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;

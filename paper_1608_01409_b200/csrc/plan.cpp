@@ -757,19 +757,19 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
     // code would be millions of instructions for ~one CTA item per block)
     if (kernel == SKC_KERNEL_JIT ||
         (kernel == SKC_KERNEL_AUTO && max_ni > 1 && !(nojit && nojit[0] == '1'))) {
-        const JitInput ji{K, C, R, S, p->Hp, p->Wp, p->Ho, p->Wo, stride, groups, p->Kg, p->Cg,
+        const JitInput ji{K, C, R, S, p->Hp, p->Wp, p->Ho, p->Wo, stride, groups, p->Kg, p->Cg, pad,
                           p->rowptr.data(), p->colidx.data(), p->perm.data(), p->values.data()};
         std::string msg;
         const int r = jit_configure(ji, max_ni == 1 ? 1 : 64, &p->jit, &msg);
         if (r == SKC_OK) {
             p->kernel = SKC_KERNEL_JIT;
-            p->image.assign(jit_lanemap_bytes(p->jit), 0);   // lane tables + zeroed counters
-            std::memcpy(p->image.data(), jit_lanemap(p->jit), jit_lanemap_bytes(p->jit) - 16);
+            p->image.assign(jit_image_bytes(p->jit), 0);   // lane tables, counters, staging
+            jit_image(p->jit, p->image.data());
             p->off_lanemap = 0;
             JitInfo ji2{};
             jit_info(p->jit, &ji2);
             p->smem = ji2.smem;
-            p->layout = ji2.pair ? SKC_LAYOUT_PAIRS : SKC_LAYOUT_NCHW;
+            p->layout = ji2.raw ? SKC_LAYOUT_RAW : ji2.pair ? SKC_LAYOUT_PAIRS : SKC_LAYOUT_NCHW;
             *out = p;
             return ok();
         }
@@ -1197,6 +1197,13 @@ skc_status skc_pad_input(const skc_plan *p, const float *d_in, float *d_pad, int
     if (!d_in || !d_pad) return fail(SKC_ERR_ARG, "NULL device pointer");
     if (!aligned16(d_in) || !aligned16(d_pad))
         return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
+    if (p->layout == SKC_LAYOUT_RAW) {  // the kernel pads while staging: a copy at most
+        if (d_in == d_pad) return ok();
+        cudaError_t e = cudaMemcpyAsync(d_pad, d_in, size_t(N) * p->C * p->H * p->W * 4,
+                                        cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+        if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "raw copy: %s", cudaGetErrorString(e));
+        return ok();
+    }
     cudaError_t e = p->layout == SKC_LAYOUT_PAIRS
                         ? launch_pad_pairs(d_in, d_pad, N, p->C, p->H, p->W, p->pad, (cudaStream_t)stream)
                         : launch_pad(d_in, d_pad, N, p->C, p->H, p->W, p->pad, (cudaStream_t)stream);
@@ -1234,6 +1241,8 @@ skc_status skc_sparse_conv_forward_into(const skc_plan *p, const float *d_in,
     if (next->C != p->K || next->H != p->Ho || next->W != p->Wo)
         return fail(SKC_ERR_GEOMETRY, "next plan expects C=%d H=%d W=%d, this layer gives %d x %d x %d",
                     next->C, next->H, next->W, p->K, p->Ho, p->Wo);
+    if (next->layout == SKC_LAYOUT_RAW)  // unpadded NCHW
+        return forward_epi(p, d_in, d_next_in, N, d_bias, relu, 0, SKC_LAYOUT_NCHW, stream);
     return forward_epi(p, d_in, d_next_in, N, d_bias, relu, next->pad, next->layout, stream);
 }
 
@@ -1305,7 +1314,7 @@ skc_status skc_forward_host(const skc_plan *p, const float *h_in, float *h_out, 
     // waits for the last D2H, so completion semantics are those of one stream.
     cudaStream_t st = (cudaStream_t)stream;
     const size_t in_img = size_t(p->C) * p->H * p->W;
-    const size_t pad_img = size_t(p->C) * p->Hp * p->Wp;
+    const size_t pad_img = p->layout == SKC_LAYOUT_RAW ? in_img : size_t(p->C) * p->Hp * p->Wp;
     const size_t out_img = size_t(p->K) * p->Ho * p->Wo;
     // chunks: a few per call, whole images, >= 8 images each
     int nchunk = std::max(1, std::min(8, N / 8));

@@ -105,7 +105,7 @@ cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_
 int regtile_shapes(RegtileShape *out, int max);
 // "Compiled weights" kernel (jit.cpp).  JitInput points into the plan's canonical CSR.
 struct JitInput {
-    int K, C, R, S, Hp, Wp, Ho, Wo, stride, groups, Kg, Cg;
+    int K, C, R, S, Hp, Wp, Ho, Wo, stride, groups, Kg, Cg, pad;
     const int32_t *rowptr, *colidx, *perm;
     const float *values;
 };
@@ -121,14 +121,17 @@ struct JitInfo {
     int whole; // 1: compiled as one whole program
     int split; // even blocks per group split into halves
     int sched; // tuned launch schedule (skc_info.jit_sched), -1 untuned
+    int raw;   // 1: reads the unpadded NCHW input (halo filled while staging)
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).
 int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *msg);
 // Generate + compile + link the code (host; thread pool; on-disk cache).
 int jit_compile(JitPlan *jp, std::string *msg);
-size_t jit_lanemap_bytes(const JitPlan *jp);
-const void *jit_lanemap(const JitPlan *jp);
+// device image of the plan's kernel-private tables (lane tables, scheduling counters, raw
+// staging tables); jit_image fills `bytes` = jit_image_bytes(jp)
+size_t jit_image_bytes(const JitPlan *jp);
+void jit_image(const JitPlan *jp, void *dst);
 void jit_info(const JitPlan *jp, JitInfo *o);
 const std::vector<int32_t> &jit_chan(const JitPlan *jp);
 cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_lanemap, int N,

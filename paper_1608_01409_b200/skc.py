@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libskc.so")
 
 SKC_KERNEL_AUTO, SKC_KERNEL_DIRECT, SKC_KERNEL_REGTILE, SKC_KERNEL_JIT = 0, 1, 2, 3
-SKC_LAYOUT_NCHW, SKC_LAYOUT_PAIRS = 0, 1
+SKC_LAYOUT_NCHW, SKC_LAYOUT_PAIRS, SKC_LAYOUT_RAW = 0, 1, 2
 STATUS = {0: "SKC_OK", -1: "SKC_ERR_ARG", -2: "SKC_ERR_GEOMETRY", -3: "SKC_ERR_NONFINITE",
           -4: "SKC_ERR_OVERFLOW", -5: "SKC_ERR_UNSUPPORTED", -6: "SKC_ERR_ALIGN",
           -7: "SKC_ERR_STATE", -8: "SKC_ERR_CUDA"}
@@ -282,6 +282,8 @@ def padded_shape(info: dict, N: int) -> tuple:
     """Shape of the padded-input buffer of N images in the plan's layout (skc_info.layout)."""
     if info["layout"] == SKC_LAYOUT_PAIRS:
         return ((N + 1) // 2, info["C"], info["Hp"], info["Wp"], 2)
+    if info["layout"] == SKC_LAYOUT_RAW:  # unpadded: the kernel pads while staging
+        return (N, info["C"], info["H"], info["W"])
     return (N, info["C"], info["Hp"], info["Wp"])
 
 
@@ -447,6 +449,9 @@ class SparseConv2d:
         import torch
         N = x.shape[0]
         if xp is None:
-            xp = torch.empty(self.padded_shape(N), dtype=torch.float32, device=x.device)
+            if self.geom["layout"] == SKC_LAYOUT_RAW and x.is_contiguous():
+                xp = x  # the kernel pads while staging
+            else:
+                xp = torch.empty(self.padded_shape(N), dtype=torch.float32, device=x.device)
         skc_pad_input(self.plan, x, xp, N, stream)
         return self.forward_padded(xp, out, stream, N)
