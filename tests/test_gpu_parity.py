@@ -673,3 +673,25 @@ def test_sm_topology_is_a_gpc_major_permutation():
     assert sorted(vid) == list(range(n))
     tpc_adjacent = sum(vid[2 * k + 1] == vid[2 * k] + 1 for k in range(n // 2))
     assert tpc_adjacent >= 0.9 * (n // 2), tpc_adjacent
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("li", [0, 3])
+def test_tuned_plan_full_batch_bitwise(li):
+    """The launch configuration bench.py times: a config-2 layer's plan tuned for the full
+    batch (skc_plan_tune picks the schedule), then the full batch of 256 -- bitwise equal to
+    the direct kernel, whose output the oracle checks in test_config_parity."""
+    cfg = wl.CONFIGS[2]
+    L = cfg.layers[li]
+    w = wl.gen_weights(2, li, L)
+    x = wl.gen_input(2, li, L, 0, cfg.batch)
+    jit = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_AUTO)
+    assert jit.geom["kernel"] == skc.SKC_KERNEL_JIT
+    assert jit.tune(cfg.batch) > 0
+    assert jit.plan.info()["jit_sched"] >= 0
+    direct = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups,
+                                         skc.SKC_KERNEL_DIRECT)
+    xd = torch.from_numpy(x).cuda()
+    yj = jit.forward(xd).cpu().numpy()
+    yd = direct.forward(xd).cpu().numpy()
+    np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32))
