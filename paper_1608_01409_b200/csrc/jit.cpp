@@ -163,7 +163,8 @@ struct JitPlan {
     // block b: conv group, first index into the group's nnz-sorted channels, channel count.
     // Blocks are numbered longest-first; the last ones may be halves of an even block (tail
     // split: the short items fill the last round of the persistent grid)
-    std::vector<int> bgrp, blo, bcnt;
+    std::vector<int> bgrp;
+    std::vector<std::vector<int>> bidx;  // positions in the group's nnz-sorted channel list
     int split = 0;             // even blocks (per group) split into halves
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
@@ -197,13 +198,11 @@ void block_channels(const JitInput &in, int M, int g, int q, std::vector<int> &k
     }
 }
 
-// Block b of a plan (explicit partition, see JitPlan::bgrp).
-void plan_block_channels(const JitInput &in, const std::vector<int> &bgrp,
-                         const std::vector<int> &blo, const std::vector<int> &bcnt, int b,
+// Block b of a plan (explicit partition, see JitPlan::bgrp / bidx).
+void plan_block_channels(const JitInput &in, int g, const std::vector<int> &idx,
                          std::vector<int> &ks) {
     ks.clear();
-    for (int m = 0; m < bcnt[size_t(b)]; ++m)
-        ks.push_back(in.perm[size_t(bgrp[size_t(b)]) * in.Kg + size_t(blo[size_t(b)] + m)]);
+    for (int i : idx) ks.push_back(in.perm[size_t(g) * in.Kg + size_t(i)]);
 }
 
 // A block's nonzeros per local input channel, in CSR order per output channel.
@@ -1470,7 +1469,7 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
     std::vector<int> ks;
     std::vector<std::vector<JNz>> per_c;
     for (int b = 0; b < jp->nblocks; ++b) {
-        plan_block_channels(in, jp->bgrp, jp->blo, jp->bcnt, b, ks);
+        plan_block_channels(in, jp->bgrp[size_t(b)], jp->bidx[size_t(b)], ks);
         block_nz(in, ks, per_c);
         const std::string code = emit_block(*jp, b, ks, per_c);
         const int Mb = int(ks.size());
@@ -1648,13 +1647,27 @@ void choose_blocks(JitPlan &jp, int n_hint) {
     std::vector<int> ks;
     std::vector<std::vector<JNz>> per_c;
     Need nd;
-    struct Blk { int g, lo, cnt; double instr; };
-    auto instr_of = [&](int g, int lo, int cnt) {
-        std::vector<int> bg{g}, bl{lo}, bc{cnt};
-        plan_block_channels(in, bg, bl, bc, 0, ks);
+    struct Blk { int g; std::vector<int> idx; double instr; };
+    auto instr_of = [&](int g, const std::vector<int> &idx) {
+        plan_block_channels(in, g, idx, ks);
         block_nz(in, ks, per_c);
-        return block_instr(in, per_c, jp.TY, jp.TX, jp.PX, jp.pair, jp.CB, cnt, nd);
+        return block_instr(in, per_c, jp.TY, jp.TX, jp.PX, jp.pair, jp.CB, int(idx.size()), nd);
     };
+    // channels of even block q (of nbg): contiguous ranges of the nnz-sorted list (default),
+    // or dealt in snake order (SKC_JIT_DEAL=1: every block gets heavy and light channels
+    // alike, equal item times).  Measured neutral on the step (conv2 +0.8%, conv4 -1.5%;
+    // profiles/r01_jit_deal.txt)
+    int deal = 0;
+    if (const char *e = std::getenv("SKC_JIT_DEAL")) deal = std::atoi(e) ? 1 : 0;
+    std::vector<std::vector<int>> even(size_t(jp.nbg));
+    for (int k = 0; k < in.Kg; ++k) {
+        int q = k / Mp;
+        if (deal) {
+            const int r = k / jp.nbg, c = k % jp.nbg;
+            q = (r & 1) ? jp.nbg - 1 - c : c;
+        }
+        if (q < jp.nbg) even[size_t(q)].push_back(k);
+    }
     double best_span = 0;
     std::vector<Blk> best;
     const int smax = jp.dyn ? std::min(jp.nbg, (in.Kg + Mp - 1) / Mp) : 0;
@@ -1663,14 +1676,16 @@ void choose_blocks(JitPlan &jp, int n_hint) {
         std::vector<Blk> full, tail;
         for (int g = 0; g < in.groups; ++g)
             for (int q = 0; q < jp.nbg; ++q) {
-                const int lo = q * Mp, cnt = std::min(Mp, in.Kg - lo);
+                const std::vector<int> &ch = even[size_t(q)];
+                const int cnt = int(ch.size());
                 if (cnt <= 0) continue;
                 if (q >= jp.nbg - sp && cnt >= 2) {
-                    const int c1 = (cnt + 1) / 2;
-                    tail.push_back({g, lo, c1, instr_of(g, lo, c1)});
-                    tail.push_back({g, lo + c1, cnt - c1, instr_of(g, lo + c1, cnt - c1)});
+                    std::vector<int> h0, h1;  // alternate: both halves balanced
+                    for (int m = 0; m < cnt; ++m) (m & 1 ? h1 : h0).push_back(ch[size_t(m)]);
+                    tail.push_back({g, h0, instr_of(g, h0)});
+                    tail.push_back({g, h1, instr_of(g, h1)});
                 } else {
-                    full.push_back({g, lo, cnt, instr_of(g, lo, cnt)});
+                    full.push_back({g, ch, instr_of(g, ch)});
                 }
             }
         std::vector<Blk> blks = full;
@@ -1696,12 +1711,11 @@ void choose_blocks(JitPlan &jp, int n_hint) {
     // as fast or faster (conv3 -2.5%: it keeps the CTAs of a TPC on the same code)
     if (jp.split == 0 && !std::getenv("SKC_JIT_DYN")) jp.dyn = 0;
     jp.nblocks = int(best.size());
-    jp.bgrp.clear(); jp.blo.clear(); jp.bcnt.clear();
+    jp.bgrp.clear(); jp.bidx.clear();
     double instr = 0;
     for (const Blk &b : best) {
         jp.bgrp.push_back(b.g);
-        jp.blo.push_back(b.lo);
-        jp.bcnt.push_back(b.cnt);
+        jp.bidx.push_back(b.idx);
         instr += b.instr;
     }
     jp.code_instr = instr;
@@ -1979,7 +1993,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
     for (int b = 0; b < jp.nblocks; ++b) {
-        plan_block_channels(in, jp.bgrp, jp.blo, jp.bcnt, b, ks);
+        plan_block_channels(in, jp.bgrp[size_t(b)], jp.bidx[size_t(b)], ks);
         for (size_t m = 0; m < ks.size(); ++m) jp.chan[size_t(b) * jp.M + m] = ks[m];
     }
     *out = best.release();
@@ -1997,7 +2011,7 @@ int jit_compile(JitPlan *jp, std::string *msg) {
         std::vector<int> ks;
         std::vector<std::vector<JNz>> per_c;
         for (int b = 0; b < jp->nblocks; ++b) {
-            plan_block_channels(in, jp->bgrp, jp->blo, jp->bcnt, b, ks);
+            plan_block_channels(in, jp->bgrp[size_t(b)], jp->bidx[size_t(b)], ks);
             block_nz(in, ks, per_c);
             mods[size_t(b)] = emit_block(*jp, b, ks, per_c);
         }
