@@ -75,7 +75,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 17;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 18;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -154,7 +154,7 @@ struct JitPlan {
                                    // ~0 = none), stage offset (((y+pad)*Wp + x+pad)*2 + img)
     // launch schedule chosen by jit_tune (-1: default): first round block-major (order 3),
     // GPC-major item numbers, cluster size
-    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1};
+    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1}, t_nodry{-1};
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
@@ -918,6 +918,8 @@ std::string emit_entry(const JitPlan &jp) {
     // take neighbouring items -- the same channel block -- and share the GPC's instruction
     // cache.  p_vid = 0: item t = cluster-major CTA rank.
     o("ld.param.u32 %%r63, [p_sched];");
+    o("and.b32 %%r62, %%r63, 4;");
+    o("setp.ne.u32 %%p9, %%r62, 0;");              // p9: skip the dry-run prefetch
     o("and.b32 %%r63, %%r63, 1;");
     o("setp.ne.u32 %%p8, %%r63, 0;");
     o("ld.param.u64 %%rd21, [p_vid];");
@@ -961,6 +963,7 @@ std::string emit_entry(const JitPlan &jp) {
         o("add.u64 %%rd14, %%rd2, %%rd14;");
         o("ld.global.nc.u32 %%r50, [%%rd14];");     // a valid lane base (band 0)
         o("mov.u32 %%r51, %%r4;");
+        o("@%%p9 bra $DRY_DONE;");
         o("$DRY_LOOP:");
         o("setp.ge.u32 %%p0, %%r51, %d;", jp.nblocks * jp.nchunks);
         o("@%%p0 bra $DRY_DONE;");
@@ -2144,7 +2147,8 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
     o->TY = jp->TY; o->TX = jp->TX; o->PX = jp->PX; o->M = jp->M; o->NW = jp->NW;
     o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks; o->split = jp->split; o->raw = jp->raw;
     o->sched = jp->t_order3.load() < 0 ? -1
-                                       : (jp->t_order3.load() | (jp->t_vid.load() << 1) | (jp->t_cs.load() << 4));
+                                       : (jp->t_order3.load() | (jp->t_vid.load() << 1) |
+                                          (std::max(0, jp->t_nodry.load()) << 2) | (jp->t_cs.load() << 4));
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;
@@ -2267,6 +2271,7 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
     if (vid_want && per_sm == 1 && grid == nsm && jp->dyn != 2 && cs <= 2)
         vid = sm_gpc_order_device(dev, true);
     unsigned sched = jp->t_order3.load() >= 0 ? unsigned(jp->t_order3.load()) : (jp->order == 3 ? 1u : 0u);
+    if (jp->t_nodry.load() > 0) sched |= 4u;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
                      vid ? "on" : "off");
@@ -2307,13 +2312,17 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
     }
     const Epilogue epi{};
     double best = -1;
-    int bo = 0, bv = 1, bc = 2;
+    int bo = 0, bv = 1, bc = 2, bd = 0;
+    // the dry-run prefetch was never worth dropping (r01_jit_tune.txt): only tried on request
+    const int nd_max = (jp->dry && std::getenv("SKC_TUNE_DRY")) ? 2 : 1;
+    for (int nd = 0; nd < nd_max; ++nd)
     for (int o3 = 0; o3 < 2; ++o3)
         for (int v = 1; v >= 0; --v)
             for (int c = 2; c >= 1; --c) {
                 jp->t_order3 = o3;
                 jp->t_vid = v;
                 jp->t_cs = c;
+                jp->t_nodry = nd;
                 double tot = 0;
                 for (int rep = 0; rep < 6; ++rep) {
                     cudaMemsetAsync(d_flush, rep, flush_bytes, st);
@@ -2331,12 +2340,13 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 }
                 if (best < 0 || tot < best) {
                     best = tot;
-                    bo = o3; bv = v; bc = c;
+                    bo = o3; bv = v; bc = c; bd = nd;
                 }
             }
     jp->t_order3 = bo;
     jp->t_vid = bv;
     jp->t_cs = bc;
+    jp->t_nodry = bd;
     if (best_ms) *best_ms = best / 5;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit tune: order3 %d vid %d cluster %d: %.4f ms\n", bo, bv, bc, best / 5);
