@@ -24,8 +24,21 @@
 //
 // Code layout: one PTX module per channel block (a .func holding the block's whole walk and
 // its epilogue), compiled in parallel with the PTX compiler library and linked by nvJitLink
-// with an entry module (stage setup, lane tables, dispatch on the CTA's block).  Loaded with
-// cudaLibraryLoadData at the first launch, launched with cudaLaunchKernel.
+// with an entry module (stage setup, lane tables, dispatch on the CTA's block) -- or, for
+// moderate code, all of it as one whole-program module.  Loaded with cudaLibraryLoadData at
+// the first launch, launched with cudaLaunchKernelExC.
+//
+// Map of this file (DESIGN.md Sec. 7.4 has the measurements behind each choice):
+//   emit_block   a block's code: image-pair window loads in position-major order, immediate-
+//                weight FFMA2, the staging ring's waits / last-warp-out TMA refills (or raw
+//                cp.async staging), bias-free and general epilogues, the dry-run entry points
+//   emit_entry   the persistent CTA loop: item numbering (cluster rank or GPC-major via the
+//                topology table), work order (first round spread / block-major), static or
+//                dynamic (counter) scheduling, per-item barrier / slot-table setup, dispatch
+//   jit_configure  the configuration search (tile, channels per block, warps, bands, staging)
+//                under the cost model, whole-round costing, block partition / tail split
+//   jit_verify   decodes the emitted PTX back to the CSR (independent of the generator)
+//   jit_compile / jit_launch / jit_tune  build (cached), launch, and launch-schedule tuning
 #include "skc.h"
 #include "skc_internal.h"
 
