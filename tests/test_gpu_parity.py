@@ -696,3 +696,30 @@ def test_tuned_plan_full_batch_bitwise(li):
     yj = jit.forward(xd).cpu().numpy()
     yd = direct.forward(xd).cpu().numpy()
     np.testing.assert_array_equal(yj.view(np.uint32), yd.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [1, 3, 64])
+def test_tune_small_layers_and_batches(N):
+    """Tuning on tiny layers (several CTAs per SM, grid != #SMs: the GPC-major numbering must
+    switch itself off) and small / odd batches: outputs stay bitwise equal to the direct
+    kernel before and after tuning."""
+    rng = np.random.default_rng(48 + N)
+    for layer in (wl.Layer("s1", 8, 8, 6, 6, 3, 3, 1, 1, 1, 0.5, 0.01),
+                  wl.Layer("s2", 24, 16, 9, 7, 1, 1, 1, 0, 2, 0.7, 0.01)):
+        w, x = wl.random_tensors(rng, layer, N)
+        try:
+            jit = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                              layer.groups, skc.SKC_KERNEL_JIT)
+        except skc.SkcError as e:
+            assert e.status == -5
+            continue
+        direct = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                             layer.groups, skc.SKC_KERNEL_DIRECT)
+        xd = torch.from_numpy(x).cuda()
+        yd = direct.forward(xd).cpu().numpy()
+        y0 = jit.forward(xd).cpu().numpy()
+        jit.tune(N)
+        y1 = jit.forward(xd).cpu().numpy()
+        np.testing.assert_array_equal(y0.view(np.uint32), yd.view(np.uint32), err_msg=layer.name)
+        np.testing.assert_array_equal(y1.view(np.uint32), yd.view(np.uint32), err_msg=layer.name)
