@@ -88,7 +88,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 18;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 19;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -167,7 +167,7 @@ struct JitPlan {
                                    // ~0 = none), stage offset (((y+pad)*Wp + x+pad)*2 + img)
     // launch schedule chosen by jit_tune (-1: default): first round block-major (order 3),
     // GPC-major item numbers, cluster size
-    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1}, t_nodry{-1};
+    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1}, t_nodry{-1}, t_lanes{-1};
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
@@ -183,6 +183,9 @@ struct JitPlan {
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
     std::vector<int32_t> chan; // [nblocks][M] original output channel or -1
     std::vector<uint32_t> lanemap;  // [NB][NW*32][4]: lane smem byte base, pos, store mask, idle
+    // second lane table, tiles dealt to lanes row-major (a warp stores runs of consecutive
+    // pixels; bank conflicts accepted): chosen per launch by skc_plan_tune (sched bit 3)
+    std::vector<uint32_t> lanemap_c;
     // compiled code
     std::vector<char> cubin;
     uint64_t key = 0;
@@ -341,7 +344,7 @@ struct Tile {
 // Tile rows of band b of NB: [b*tiles_y/NB, (b+1)*tiles_y/NB).
 int band_lo(int tiles_y, int NB, int b) { return int((int64_t(b) * tiles_y) / NB); }
 
-int assign_lanes(const JitPlan &jp, int IS, int band, uint32_t *lanemap) {
+int assign_lanes(const JitPlan &jp, int IS, int band, uint32_t *lanemap, int lanes_mode = 0) {
     const JitInput &in = jp.in;
     const int st = in.stride, sw = jp.pair ? 2 : 1;
     const int nslot = jp.NI / sw;
@@ -366,6 +369,23 @@ int assign_lanes(const JitPlan &jp, int IS, int band, uint32_t *lanemap) {
     size_t left = tiles.size();
     int extra = 0;
     const int ngroups = jp.NW * groups;
+    if (lanes_mode == 1 && tiles.size() <= size_t(jp.NW) * 32) {
+        // contiguous: lane l takes tile l (row-major), so a warp's output stores are runs of
+        // consecutive pixels; the bank conflicts this costs are counted, not avoided
+        for (size_t i = 0; i < tiles.size(); ++i) {
+            lane_tile[i] = int(i);
+            used[i] = 1;
+        }
+        left = 0;
+        for (int gi = 0; gi < ngroups; ++gi) {
+            int cnt[32] = {0}, mx = 0;
+            for (int l = 0; l < glanes; ++l) {
+                const int ti = lane_tile[size_t(gi) * glanes + size_t(l)];
+                if (ti >= 0) mx = std::max(mx, ++cnt[res[size_t(ti)]]);
+            }
+            extra += std::max(0, mx - 1);
+        }
+    }
     for (int gi = 0; gi < ngroups && left; ++gi) {
         int cnt[32] = {0};
         int filled = 0;
@@ -931,6 +951,13 @@ std::string emit_entry(const JitPlan &jp) {
     // take neighbouring items -- the same channel block -- and share the GPC's instruction
     // cache.  p_vid = 0: item t = cluster-major CTA rank.
     o("ld.param.u32 %%r63, [p_sched];");
+    {
+        // sched bit 3: read the contiguous lane table (after counters and staging tables)
+        const long long lc_off = (long long)jp.lanemap.size() * 4 + 16 + (long long)jp.stab.size() * 4;
+        o("and.b32 %%r62, %%r63, 8;");
+        o("setp.ne.u32 %%p0, %%r62, 0;");
+        o("selp.u64 %%rd19, %lld, 0, %%p0;", jp.lanemap_c.empty() ? 0LL : lc_off);
+    }
     o("and.b32 %%r62, %%r63, 4;");
     o("setp.ne.u32 %%p9, %%r62, 0;");              // p9: skip the dry-run prefetch
     o("and.b32 %%r63, %%r63, 1;");
@@ -974,6 +1001,7 @@ std::string emit_entry(const JitPlan &jp) {
         // so the whole layer's code is pulled into L2 by many parallel streams at once.
         o("mul.wide.u32 %%rd14, %%r3, 16;");
         o("add.u64 %%rd14, %%rd2, %%rd14;");
+        o("add.u64 %%rd14, %%rd14, %%rd19;");
         o("ld.global.nc.u32 %%r50, [%%rd14];");     // a valid lane base (band 0)
         o("mov.u32 %%r51, %%r4;");
         o("@%%p9 bra $DRY_DONE;");
@@ -1116,6 +1144,7 @@ std::string emit_entry(const JitPlan &jp) {
     o("mad.lo.u32 %%r49, %%r48, %d, %%r3;", jp.NW * 32);
     o("mul.wide.u32 %%rd7, %%r49, 16;");
     o("add.u64 %%rd7, %%rd2, %%rd7;");
+    o("add.u64 %%rd7, %%rd7, %%rd19;");
     o("ld.global.nc.v4.u32 {%%r17, %%r18, %%r33, %%r20}, [%%rd7];");
     o("shr.u32 %%r21, %%r18, 24;");              // slot
     o("shr.u32 %%r22, %%r18, 12;");
@@ -1462,10 +1491,13 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
     // stored by exactly one (lane, pixel)
     // (a slot is an image, or an image pair in the pair-interleaved layout; both images of
     // a pair share the lane's tile and mask)
+    // (both lane tables: bank-residue first fit and the contiguous one)
+    for (const std::vector<uint32_t> *tab : {&jp->lanemap, &jp->lanemap_c}) {
+    if (tab == &jp->lanemap_c && tab->empty()) continue;
     std::vector<int> cover(size_t(NSL) * in.Ho * in.Wo, 0);
-    if (jp->lanemap.size() != size_t(jp->NB) * jp->NW * 32 * 4) return bad("lane table size");
+    if (tab->size() != size_t(jp->NB) * jp->NW * 32 * 4) return bad("lane table size");
     for (int l = 0; l < jp->NB * jp->NW * 32; ++l) {
-        const uint32_t *e = jp->lanemap.data() + size_t(l) * 4;
+        const uint32_t *e = tab->data() + size_t(l) * 4;
         const int img = int(e[1] >> 24), y0 = int((e[1] >> 12) & 4095), x0 = int(e[1] & 4095);
         if (img >= NSL || y0 + TY > in.Ho || x0 + TX > in.Wo) return bad("lane tile out of range");
         if (e[0] != uint32_t(img * jp->img_stride + (y0 * st * in.Wp + x0 * st) * sw) * 4u)
@@ -1477,6 +1509,7 @@ int jit_verify(const JitPlan *jp, std::string *msg) {
     }
     for (int v : cover)
         if (v != 1) return bad("output pixel stored " + std::to_string(v) + " times");
+    }
     if (size_t(jp->off_info) + size_t(NSL) * 8 > jp->smem ||
         size_t(jp->NS) * jp->stage_bytes > size_t(jp->off_bar) || jp->smem > size_t(kMaxSmem))
         return bad("shared-memory layout");
@@ -1942,6 +1975,12 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.img_stride = best_is;
     jp.conflict = best_extra;
     jp.stage_bytes = NSL * best_is * 4;
+    jp.lanemap_c.assign(size_t(jp.NB) * jp.NW * 32 * 4, 0);
+    for (int b = 0; b < jp.NB; ++b)
+        if (assign_lanes(jp, best_is, b, jp.lanemap_c.data() + size_t(b) * jp.NW * 32 * 4, 1) < 0) {
+            jp.lanemap_c.clear();
+            break;
+        }
     jp.lanemap.assign(size_t(jp.NB) * jp.NW * 32 * 4, 0);
     for (int b = 0; b < jp.NB; ++b)
         assign_lanes(jp, best_is, b, jp.lanemap.data() + size_t(b) * jp.NW * 32 * 4);
@@ -2148,12 +2187,17 @@ int jit_compile(JitPlan *jp, std::string *msg) {
 
 // device image: the lane tables, 16 bytes of (zeroed) scheduling counters, then (raw staging)
 // the per-thread staging tables
-size_t jit_image_bytes(const JitPlan *jp) { return jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4; }
+size_t jit_image_bytes(const JitPlan *jp) {
+    return jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4 + jp->lanemap_c.size() * 4;
+}
 void jit_image(const JitPlan *jp, void *dst) {
     char *d = static_cast<char *>(dst);
     std::memcpy(d, jp->lanemap.data(), jp->lanemap.size() * 4);
     std::memset(d + jp->lanemap.size() * 4, 0, 16);
     if (!jp->stab.empty()) std::memcpy(d + jp->lanemap.size() * 4 + 16, jp->stab.data(), jp->stab.size() * 4);
+    if (!jp->lanemap_c.empty())
+        std::memcpy(d + jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4, jp->lanemap_c.data(),
+                    jp->lanemap_c.size() * 4);
 }
 
 void jit_info(const JitPlan *jp, JitInfo *o) {
@@ -2161,7 +2205,8 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
     o->NI = jp->NI; o->CB = jp->CB; o->NS = jp->NS; o->nblocks = jp->nblocks; o->split = jp->split; o->raw = jp->raw;
     o->sched = jp->t_order3.load() < 0 ? -1
                                        : (jp->t_order3.load() | (jp->t_vid.load() << 1) |
-                                          (std::max(0, jp->t_nodry.load()) << 2) | (jp->t_cs.load() << 4));
+                                          (std::max(0, jp->t_nodry.load()) << 2) |
+                                          (std::max(0, jp->t_lanes.load()) << 3) | (jp->t_cs.load() << 4));
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;
@@ -2285,6 +2330,12 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
         vid = sm_gpc_order_device(dev, true);
     unsigned sched = jp->t_order3.load() >= 0 ? unsigned(jp->t_order3.load()) : (jp->order == 3 ? 1u : 0u);
     if (jp->t_nodry.load() > 0) sched |= 4u;
+    static const int lanes_env = [] {
+        const char *e = std::getenv("SKC_JIT_LANES");  // 0/1: force the lane table (testing)
+        return e ? std::atoi(e) : -1;
+    }();
+    const int lanes = lanes_env >= 0 ? lanes_env : jp->t_lanes.load();
+    if (lanes > 0 && !jp->lanemap_c.empty()) sched |= 8u;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
                      vid ? "on" : "off");
@@ -2328,6 +2379,8 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
     int bo = 0, bv = 1, bc = 2, bd = 0;
     // the dry-run prefetch was never worth dropping (r01_jit_tune.txt): only tried on request
     const int nd_max = (jp->dry && std::getenv("SKC_TUNE_DRY")) ? 2 : 1;
+    int bl = 0;
+    for (int ln = 0; ln < (jp->lanemap_c.empty() ? 1 : 2); ++ln)
     for (int nd = 0; nd < nd_max; ++nd)
     for (int o3 = 0; o3 < 2; ++o3)
         for (int v = 1; v >= 0; --v)
@@ -2336,6 +2389,7 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 jp->t_vid = v;
                 jp->t_cs = c;
                 jp->t_nodry = nd;
+                jp->t_lanes = ln;
                 double tot = 0;
                 for (int rep = 0; rep < 6; ++rep) {
                     cudaMemsetAsync(d_flush, rep, flush_bytes, st);
@@ -2353,13 +2407,14 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 }
                 if (best < 0 || tot < best) {
                     best = tot;
-                    bo = o3; bv = v; bc = c; bd = nd;
+                    bo = o3; bv = v; bc = c; bd = nd; bl = ln;
                 }
             }
     jp->t_order3 = bo;
     jp->t_vid = bv;
     jp->t_cs = bc;
     jp->t_nodry = bd;
+    jp->t_lanes = bl;
     if (best_ms) *best_ms = best / 5;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit tune: order3 %d vid %d cluster %d: %.4f ms\n", bo, bv, bc, best / 5);

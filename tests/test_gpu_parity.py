@@ -569,7 +569,8 @@ def test_jit_bitwise_equals_direct_full_batch(cfg_id):
     {"SKC_JIT_XPF": "1", "SKC_JIT_NS": "2", "SKC_JIT_STAGE_KB": "12", "SKC_JIT_GRID": "1"},
     {"SKC_JIT_PMAJOR": "0"}, {"SKC_JIT_VID": "0"}, {"SKC_JIT_RAW": "1"},
     {"SKC_JIT_RAW": "1", "SKC_JIT_NS": "3", "SKC_JIT_STAGE_KB": "20"}, {"SKC_JIT_DEAL": "0"},
-    {"SKC_JIT_DEAL": "1", "SKC_JIT_DYN": "1", "SKC_JIT_SPLIT": "2"},
+    {"SKC_JIT_DEAL": "1", "SKC_JIT_DYN": "1", "SKC_JIT_SPLIT": "2"}, {"SKC_JIT_LANES": "1"},
+    {"SKC_JIT_LANES": "1", "SKC_JIT_DYN": "2"},
 ])
 def test_jit_tuning_knobs_bitwise(knobs, monkeypatch):
     """Every JIT tuning knob (work order, dry-run prefetch, L2 policy, cluster size, layout,
