@@ -105,7 +105,8 @@ typedef struct {
     int jit_sched;                 /* JIT launch schedule from skc_plan_tune: -1 untuned,
                                       else bit 0 first round block-major, bit 1 GPC-major
                                       item numbers, bit 2 no dry-run code prefetch, bit 3
-                                      contiguous lane table, bits 4-7 cluster size        */
+                                      contiguous lane table, bits 4-7 cluster size, bit 9
+                                      dry run by every CTA                                */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).
@@ -231,7 +232,8 @@ skc_status skc_plan_compile(skc_plan *plan);
 /* JIT kernel only: measure the launch-schedule variants of the plan's kernel on this device and
  * keep the fastest (first round of work items spread over the channel blocks or block-major;
  * work items numbered GPC-major or by cluster rank; clusters of 2 CTAs or none; lane table
- * dealt by shared-memory bank residue or contiguously -- DESIGN.md
+ * dealt by shared-memory bank residue or contiguously; dry-run code prefetch by the first
+ * CTAs or by every CTA -- DESIGN.md
  * Sec. 7.4).  Times each variant 5x on zero-filled scratch buffers of N images that it
  * allocates and frees (input in the plan's layout + output + a 256 MiB L2 flush buffer, which
  * is written before every timed launch); synchronous on `stream`.  Every variant computes

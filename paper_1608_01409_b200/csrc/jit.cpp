@@ -88,7 +88,7 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 19;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 20;  // bump when the generated code changes (cache key)
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -167,7 +167,7 @@ struct JitPlan {
                                    // ~0 = none), stage offset (((y+pad)*Wp + x+pad)*2 + img)
     // launch schedule chosen by jit_tune (-1: default): first round block-major (order 3),
     // GPC-major item numbers, cluster size
-    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1}, t_nodry{-1}, t_lanes{-1};
+    std::atomic<int> t_order3{-1}, t_vid{-1}, t_cs{-1}, t_nodry{-1}, t_lanes{-1}, t_dryall{-1};
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
@@ -951,6 +951,7 @@ std::string emit_entry(const JitPlan &jp) {
     // take neighbouring items -- the same channel block -- and share the GPC's instruction
     // cache.  p_vid = 0: item t = cluster-major CTA rank.
     o("ld.param.u32 %%r63, [p_sched];");
+    o("mov.u32 %%r61, %%r63;");                    // (the whole sched word, for the dry run)
     {
         // sched bit 3: read the contiguous lane table (after counters and staging tables)
         const long long lc_off = (long long)jp.lanemap.size() * 4 + 16 + (long long)jp.stab.size() * 4;
@@ -1004,6 +1005,11 @@ std::string emit_entry(const JitPlan &jp) {
         o("add.u64 %%rd14, %%rd14, %%rd19;");
         o("ld.global.nc.u32 %%r50, [%%rd14];");     // a valid lane base (band 0)
         o("mov.u32 %%r51, %%r4;");
+        // sched bit 9: every CTA dry-runs segment t mod (blocks x chunks), so each segment is
+        // run by several CTAs spread over the GPCs (their instruction caches warm too)
+        o("and.b32 %%r62, %%r61, 512;");
+        o("setp.ne.u32 %%p0, %%r62, 0;");
+        o("@%%p0 rem.u32 %%r51, %%r51, %d;", jp.nblocks * jp.nchunks);
         o("@%%p9 bra $DRY_DONE;");
         o("$DRY_LOOP:");
         o("setp.ge.u32 %%p0, %%r51, %d;", jp.nblocks * jp.nchunks);
@@ -2206,7 +2212,8 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
     o->sched = jp->t_order3.load() < 0 ? -1
                                        : (jp->t_order3.load() | (jp->t_vid.load() << 1) |
                                           (std::max(0, jp->t_nodry.load()) << 2) |
-                                          (std::max(0, jp->t_lanes.load()) << 3) | (jp->t_cs.load() << 4));
+                                          (std::max(0, jp->t_lanes.load()) << 3) | (jp->t_cs.load() << 4) |
+                                          (std::max(0, jp->t_dryall.load()) << 9));
     o->smem = jp->smem; o->cubin_bytes = jp->cubin.size(); o->cost = jp->cost;
     o->conflict = jp->conflict; o->compile_s = jp->compile_s; o->cache_hit = jp->cache_hit;
     o->pair = jp->pair;
@@ -2336,6 +2343,7 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
     }();
     const int lanes = lanes_env >= 0 ? lanes_env : jp->t_lanes.load();
     if (lanes > 0 && !jp->lanemap_c.empty()) sched |= 8u;
+    if (jp->t_dryall.load() > 0) sched |= 512u;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
                      vid ? "on" : "off");
@@ -2379,7 +2387,8 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
     int bo = 0, bv = 1, bc = 2, bd = 0;
     // the dry-run prefetch was never worth dropping (r01_jit_tune.txt): only tried on request
     const int nd_max = (jp->dry && std::getenv("SKC_TUNE_DRY")) ? 2 : 1;
-    int bl = 0;
+    int bl = 0, ba = 0;
+    for (int da = 0; da < (jp->dry ? 2 : 1); ++da)
     for (int ln = 0; ln < (jp->lanemap_c.empty() ? 1 : 2); ++ln)
     for (int nd = 0; nd < nd_max; ++nd)
     for (int o3 = 0; o3 < 2; ++o3)
@@ -2390,6 +2399,7 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 jp->t_cs = c;
                 jp->t_nodry = nd;
                 jp->t_lanes = ln;
+                jp->t_dryall = da;
                 double tot = 0;
                 for (int rep = 0; rep < 6; ++rep) {
                     cudaMemsetAsync(d_flush, rep, flush_bytes, st);
@@ -2407,7 +2417,7 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 }
                 if (best < 0 || tot < best) {
                     best = tot;
-                    bo = o3; bv = v; bc = c; bd = nd; bl = ln;
+                    bo = o3; bv = v; bc = c; bd = nd; bl = ln; ba = da;
                 }
             }
     jp->t_order3 = bo;
@@ -2415,6 +2425,7 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
     jp->t_cs = bc;
     jp->t_nodry = bd;
     jp->t_lanes = bl;
+    jp->t_dryall = ba;
     if (best_ms) *best_ms = best / 5;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit tune: order3 %d vid %d cluster %d: %.4f ms\n", bo, bv, bc, best / 5);
