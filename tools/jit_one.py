@@ -12,6 +12,8 @@ L = cfg.layers[li]
 w = wl.gen_weights(2, li, L)
 x = torch.from_numpy(wl.gen_input(2, li, L, 0, N)).cuda()
 j = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kern)
+if os.environ.get("SKC_ONE_TUNE", "0") == "1":  # the launch schedule bench.py would use
+    print("tuned", j.tune(N), j.plan.info()["jit_sched"])
 xp = torch.empty(j.padded_shape(N), device="cuda")
 skc.skc_pad_input(j.plan, x, xp, N)
 y = j.forward_padded(xp)
