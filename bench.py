@@ -9,7 +9,15 @@ layer of the workload, skc_pad_input (a2) then skc_sparse_conv_forward (a3..a6);
 packing (a1) is a one-off per layer, done before timing ("pre-computed").
 Workload at N = 1: BASELINE.json configs[1] (AlexNet conv2-5, batch 256, FP32).  With N
 GPUs every rank runs its own 256 images (weak scaling; images are independent so the path
-has no collective -- SURVEY.md Sec. 8(e)); the whole-job value is all images / max-over-ranks time.
+has no collective -- SURVEY.md Sec. 8(e)); the whole-job value is all images / max-over-ranks
+time.  --config 5 is BASELINE.json configs[4]: ONE global batch of 4096 sharded across the
+ranks (strong scaling); after timing, every layer's outputs are gathered over NCCL, compared
+bit for bit with one GPU's run of the whole batch, and >= 8 images per shard (first and last
+included) are checked against the oracle.
+
+After timing, seeded images of the TIMED outputs of every layer are checked against the fp64
+oracle (`parity`), and the FFMA / FFMA2 / LDS micro-benchmarks give the measured peaks the
+roofline is also reported against (`peaks_measured`, `roofline.frac_measured`).
 
 Printed by rank 0: ONE JSON line.
 """
@@ -42,13 +50,18 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the config's)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="per-GPU batch (config 5: the global batch; default: the config's)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "regtile", "jit"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time plain launches, no CUDA graph")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--no-cpu-single", action="store_true", help="skip the 1-thread oracle timing")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed outputs")
+    ap.add_argument("--parity-images", type=int, default=16, help="images per layer the oracle checks")
+    ap.add_argument("--no-peaks", action="store_true", help="skip the FFMA/LDS micro-benchmarks")
     return ap.parse_args()
 
 
@@ -214,6 +227,71 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- checks
+def sample_images(lo: int, hi: int, k: int, rng) -> list:
+    """k images of [lo, hi) (all if fewer): always the first and the last, the rest seeded."""
+    idx = {lo, hi - 1} if hi > lo else set()
+    while len(idx) < min(k, hi - lo):
+        idx.add(int(rng.integers(lo, hi)))
+    return sorted(idx)
+
+
+def oracle_err(x_imgs, w, L, got) -> float:
+    """max over elements of |got - oracle| / sum|w*x| for images x_imgs (inf if an element
+    whose sum|w*x| is 0 is not exactly 0) -- the north star's tolerance is 1e-4."""
+    import oracle
+    ref, bound = oracle.conv2d_fp64(x_imgs, w, L.stride, L.pad, L.groups)
+    got = np.asarray(got, dtype=np.float64)
+    zero = bound == 0
+    if np.any(got[zero] != 0):
+        return float("inf")
+    ratio = np.abs(got - ref)[~zero] / bound[~zero]
+    return float(ratio.max()) if ratio.size else 0.0
+
+
+def verify_gathered(gathered, full, cfg_id: int, li: int, L, w, n_total: int, world: int,
+                    per_shard: int = 8, seed: int = 0) -> dict:
+    """SURVEY.md Sec. 8(c)/(e) for a batch-sharded run: the outputs gathered from all ranks
+    must equal, BIT FOR BIT, one device's run over the whole batch (`full`; None = skip), and
+    >= per_shard images of every shard -- its first and last included -- must pass the oracle.
+    gathered / full: [n_total, K, Ho, Wo] float32 arrays (NumPy or CPU tensors)."""
+    from paper_1608_01409_b200 import dist as skd
+    g = np.asarray(gathered)
+    res = {"layer": L.name, "images": 0, "max_err_over_bound": 0.0, "bitwise_vs_1gpu": None}
+    if full is not None:
+        res["bitwise_vs_1gpu"] = bool(np.array_equal(g.view(np.uint32), np.asarray(full).view(np.uint32)))
+    rng = np.random.default_rng([seed, cfg_id, li])
+    for r in range(world):
+        lo, hi = skd.shard_range(n_total, world, r)
+        idx = sample_images(lo, hi, per_shard, rng)
+        for n in idx:
+            x = wl.gen_input(cfg_id, li, L, n, n + 1)
+            res["max_err_over_bound"] = max(res["max_err_over_bound"], oracle_err(x, w, L, g[n:n + 1]))
+        res["images"] += len(idx)
+    return res
+
+
+def measure_peaks(skc, torch, dev) -> dict:
+    """FFMA / FFMA2 / LDS.32 / LDS.64 micro-benchmarks in this session: the measured
+    "achievable" FP32 and shared-memory rates (as the paper measured SGEMM and STREAM,
+    PAPER.md:550-552), beside the nominal unit-count peaks."""
+    scratch = torch.empty(4 << 20, dtype=torch.uint8, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks = nsm * 8  # 2048 threads per SM
+    out = {"blocks": blocks, "threads_per_block": 256}
+    for name, fn, iters, scale, unit in (("ffma", skc.skc_bench_ffma, 4096, 1e9, "tflops"),
+                                         ("ffma2", skc.skc_bench_ffma2, 2048, 1e9, "tflops"),
+                                         ("lds32", skc.skc_bench_lds, 4096, 1e9, "tbs"),
+                                         ("lds64", skc.skc_bench_lds64, 2048, 1e9, "tbs")):
+        best = None
+        for _ in range(3):
+            ms, n = fn(scratch, blocks, iters)
+            v = n / ms / scale
+            best = v if best is None else max(best, v)
+        out[f"{name}_{unit}"] = best
+    return out
+
+
 # ----------------------------------------------------------------------------- our leg
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
@@ -230,8 +308,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     skc.lib()
 
     from paper_1608_01409_b200 import dist as skd
-    per_gpu = args.batch or cfg.batch
-    n0, n1 = skd.shard_range(per_gpu * world, world, rank)  # weak scaling: per_gpu images each
+    # config 5 (BASELINE.json configs[4]): ONE global batch (4096) sharded across the ranks --
+    # strong scaling; every other config: each rank runs the config's batch -- weak scaling.
+    # Images are independent, so either way there is no collective on the data path.
+    strong = cfg.cfg_id == 5
+    if strong:
+        n_global = args.batch or cfg.batch
+        n0, n1 = skd.shard_range(n_global, world, rank)
+    else:
+        per = args.batch or cfg.batch
+        n_global = per * world
+        n0, n1 = rank * per, (rank + 1) * per
+    local_n = n1 - n0
     kernel = {"auto": skc.SKC_KERNEL_AUTO, "direct": skc.SKC_KERNEL_DIRECT,
               "regtile": skc.SKC_KERNEL_REGTILE, "jit": skc.SKC_KERNEL_JIT}[args.kernel]
     stream = torch.cuda.current_stream(dev)
@@ -240,8 +328,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_build = time.time()
     # plan build (pack + JIT compile + upload): one-off, untimed; the JIT
     # compiles of the layers run concurrently (host threads; ctypes releases the GIL)
-    plans = [skc.skc_pack_csr(wl.gen_weights(cfg.cfg_id, li, L), L.H, L.W, L.stride, L.pad,
-                              L.groups, kernel) for li, L in enumerate(cfg.layers)]
+    ws = [wl.gen_weights(cfg.cfg_id, li, L) for li, L in enumerate(cfg.layers)]
+    plans = [skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, kernel)
+             for w, L in zip(ws, cfg.layers)]
     import concurrent.futures as cf
     # N ranks of one node: local rank 0 compiles first and fills the on-disk JIT cache, the
     # others then load the same code from it instead of N concurrent compiles
@@ -252,19 +341,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world > 1 and local_rank == 0:
         dist.barrier()
     for li, L in enumerate(cfg.layers):
-        w = wl.gen_weights(cfg.cfg_id, li, L)
         conv = skc.SparseConv2d.from_plan(plans[li], dev)
         # launch-schedule tuning for this batch on this device (setup, untimed; outputs are
         # bitwise unaffected -- DESIGN.md Sec. 7.4)
         if os.environ.get("SKC_TUNE", "1") != "0":
-            conv.tune(per_gpu)
+            conv.tune(local_n)
         x_host = torch.from_numpy(wl.gen_input(cfg.cfg_id, li, L, n0, n1))
         x = x_host.to(dev)
         # (the raw layout is the NCHW input itself: the kernel pads while staging, and
         # skc_pad_input on the same buffer is a no-op)
-        xp = x if conv.geom["layout"] == skc.SKC_LAYOUT_RAW else torch.empty(conv.padded_shape(per_gpu), device=dev)
-        out = torch.empty(conv.out_shape(per_gpu), device=dev)
-        layers.append(dict(L=L, w=w, conv=conv, x=x, xp=xp, out=out, x_host=x_host,
+        xp = x if conv.geom["layout"] == skc.SKC_LAYOUT_RAW else torch.empty(conv.padded_shape(local_n), device=dev)
+        out = torch.empty(conv.out_shape(local_n), device=dev)
+        layers.append(dict(L=L, w=ws[li], conv=conv, x=x, xp=xp, out=out, x_host=x_host,
                            nnz=int(conv.geom["nnz"])))
         if world > 1 and not skd.check_same_plan(conv.plan, dev):
             raise SystemExit(f"bench.py: rank {rank} packed a different plan for {L.name}")
@@ -274,10 +362,10 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def step_on(st, evs=None):
         for i, d in enumerate(layers):
-            skc.skc_pad_input(d["conv"].plan, d["x"], d["xp"], per_gpu, st)
+            skc.skc_pad_input(d["conv"].plan, d["x"], d["xp"], local_n, st)
             if evs is not None:
                 evs[2 * i + 1].record(st)
-            skc.skc_sparse_conv_forward(d["conv"].plan, d["xp"], d["out"], per_gpu, st)
+            skc.skc_sparse_conv_forward(d["conv"].plan, d["xp"], d["out"], local_n, st)
             if evs is not None:
                 evs[2 * i + 2].record(st)
 
@@ -339,13 +427,76 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     per_kernel /= args.steps
-    t_step = float(np.mean(step_ms))
+    t_local = float(np.mean(step_ms))
+    t_step = t_local
     if world > 1:
-        t_step = skd.max_over_ranks(t_step, dev)
+        t_step = skd.max_over_ranks(t_local, dev)
 
-    step_nnz_flops = sum(nnz_flops(d["L"], d["nnz"], per_gpu) for d in layers)
-    step_dense_flops = sum(dense_flops(d["L"], per_gpu) for d in layers)
-    value = step_nnz_flops * world / (t_step * 1e-3) / 1e9
+    local_nnz_flops = sum(nnz_flops(d["L"], d["nnz"], local_n) for d in layers)
+    step_nnz_flops = sum(nnz_flops(d["L"], d["nnz"], n_global) for d in layers)
+    step_dense_flops = sum(dense_flops(d["L"], n_global) for d in layers)
+    value = step_nnz_flops / (t_step * 1e-3) / 1e9
+
+    # ---- parity of the TIMED outputs (they hold the last replay's results): seeded images
+    # of every layer against the fp64 oracle; with
+    # N ranks, the outputs are gathered to every rank (NCCL all_gather, off the timed path),
+    # compared bit for bit with one device's run over the whole batch, and >= 8 images per
+    # shard go through the oracle
+    parity = None
+    if not args.no_parity:
+        import oracle
+        oracle.build()
+        torch.cuda.synchronize()
+        per_layer_par = []
+        rng = np.random.default_rng([1608, cfg.cfg_id, rank])
+        for li, d in enumerate(layers):
+            L = d["L"]
+            if world == 1:
+                idx = sample_images(0, local_n, args.parity_images, rng)
+                got = d["out"][idx].cpu().numpy()
+                x_imgs = d["x_host"][idx].numpy()
+                e = oracle_err(x_imgs, d["w"], L, got)
+                per_layer_par.append({"layer": L.name, "images": len(idx), "max_err_over_bound": e})
+                continue
+            full_g = skd.gather_images(d["out"], n_global) if strong else None
+            if not strong:
+                # weak scaling: every rank checks its own images against the oracle
+                idx = sample_images(0, local_n, args.parity_images, rng)
+                e = oracle_err(d["x_host"][idx].numpy(), d["w"], L, d["out"][idx].cpu().numpy())
+                e = skd.max_over_ranks(e, dev)
+                per_layer_par.append({"layer": L.name, "images": len(idx) * world, "max_err_over_bound": e})
+                continue
+            ref = None
+            if rank == 0:
+                # one device's run over the whole global batch, same plan
+                conv = d["conv"]
+                xg = torch.from_numpy(wl.gen_input(cfg.cfg_id, li, L, 0, n_global)).to(dev)
+                xpg = torch.empty(conv.padded_shape(n_global), device=dev)
+                skc.skc_pad_input(conv.plan, xg, xpg, n_global)
+                ref = torch.empty(conv.out_shape(n_global), device=dev)
+                skc.skc_sparse_conv_forward(conv.plan, xpg, ref, n_global)
+                del xg, xpg
+                res = verify_gathered(full_g.cpu().numpy(), ref.cpu().numpy(), cfg.cfg_id, li, L,
+                                      d["w"], n_global, world)
+                per_layer_par.append(res)
+            del full_g, ref
+            if world > 1:
+                dist.barrier()
+        if rank == 0:
+            worst = max(p["max_err_over_bound"] for p in per_layer_par)
+            parity = {"max_err_over_bound": worst, "tolerance": 1e-4, "pass": worst <= 1e-4,
+                      "images": sum(p["images"] for p in per_layer_par),
+                      "what": ("timed outputs, seeded images incl. first and last, vs the fp64 "
+                               "oracle (oracle/oracle_conv.c)"
+                               + ("; outputs of all ranks gathered and compared bitwise with a "
+                                  "1-GPU run of the global batch" if strong and world > 1 else "")),
+                      "per_layer": per_layer_par}
+            if strong and world > 1:
+                parity["bitwise_vs_1gpu"] = all(p["bitwise_vs_1gpu"] for p in per_layer_par)
+                parity["pass"] = parity["pass"] and parity["bitwise_vs_1gpu"]
+
+    # ---- measured peaks (micro-benchmarks, this session)
+    peaks = None if args.no_peaks else measure_peaks(skc, torch, dev)
 
     # ---- dense FP32 baseline (cuDNN, TF32 off), same protocol
     dense = None
@@ -372,7 +523,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         sg_ms = 0.0
         for d in layers:
             L = d["L"]
-            kk, cc, pp = L.K // L.groups, (L.C // L.groups) * L.R * L.S, L.Ho * L.Wo * per_gpu
+            kk, cc, pp = L.K // L.groups, (L.C // L.groups) * L.R * L.S, L.Ho * L.Wo * local_n
             A = torch.randn(kk, cc, device=dev)
             B = torch.randn(cc, pp, device=dev)
             for _ in range(2):
@@ -387,22 +538,24 @@ def run_ours(args, cfg, rank, world, local_rank):
             torch.cuda.synchronize()
             sg_ms += a.elapsed_time(b) / reps * L.groups
             del A, B
-        dense = {"cudnn_fp32_ms": t_dense, "speedup_vs_cudnn_fp32": t_dense / t_step,
-                 "cudnn_dense_equiv_gflops": step_dense_flops / (t_dense * 1e-3) / 1e9,
-                 "sgemm_proxy_ms": sg_ms, "speedup_vs_sgemm_proxy": sg_ms / t_step,
-                 "sgemm_gflops": step_dense_flops / (sg_ms * 1e-3) / 1e9,
-                 "note": "cuDNN FP32 (allow_tf32=False) may use Winograd/FFT, so its dense-"
-                         "equivalent rate can exceed the FP32 FMA peak; the paper's own dense "
-                         "baseline is the SGEMM proxy (PAPER.md:728-732)"}
+        dense = {"cudnn_fp32_ms": t_dense, "speedup_vs_cudnn_fp32": t_dense / t_local,
+                 "cudnn_dense_equiv_gflops": sum(dense_flops(d["L"], local_n) for d in layers) / (t_dense * 1e-3) / 1e9,
+                 "sgemm_proxy_ms": sg_ms, "speedup_vs_sgemm_proxy": sg_ms / t_local,
+                 "sgemm_gflops": sum(dense_flops(d["L"], local_n) for d in layers) / (sg_ms * 1e-3) / 1e9,
+                 "note": "per rank, its own images; cuDNN FP32 (allow_tf32=False) may use "
+                         "Winograd/FFT, so its dense-equivalent rate can exceed the FP32 FMA "
+                         "peak; the paper's own dense baseline is the SGEMM proxy "
+                         "(PAPER.md:728-732)"}
 
     # ---- end to end through the C-ABI host entry point (pinned host buffers)
     e2e = None
     if not args.no_e2e:
         hin = [d["x_host"].pin_memory() for d in layers]
-        hout = [torch.empty(d["conv"].out_shape(per_gpu)).pin_memory() for d in layers]
+        hout = [torch.empty(d["conv"].out_shape(local_n)).pin_memory() for d in layers]
         # the four layers are independent: each runs its H2D / pad + conv / D2H pipeline on
         # its own stream (forked from and joined back into the timed stream), so one layer's
-        # output copy overlaps the next layer's input copy on the two copy engines
+        # output copy overlaps the next layer's input copy on the two copy engines (every
+        # plan's workspace is used by one stream only: skc.h thread-safety rule)
         side = [torch.cuda.Stream(dev) for _ in layers]
 
         def estep():
@@ -410,7 +563,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             fork.record(stream)
             for s_, d, hi, ho in zip(side, layers, hin, hout):
                 s_.wait_event(fork)
-                skc.skc_forward_host(d["conv"].plan, hi, ho, per_gpu, d["x"], d["xp"], d["out"],
+                skc.skc_forward_host(d["conv"].plan, hi, ho, local_n, d["x"], d["xp"], d["out"],
                                      s_)
             for s_ in side:
                 j = torch.cuda.Event()
@@ -426,10 +579,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         t_e2e = float(np.mean(ems))
         if world > 1:
             t_e2e = skd.max_over_ranks(t_e2e, dev)
-        e2e = {"value": step_nnz_flops * world / (t_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
+        e2e_ok = None
+        if not args.no_parity:
+            # the host outputs of the last e2e step: bitwise equal to the device path's
+            e2e_ok = all(bool(torch.equal(ho.view(torch.int32), d["out"].cpu().view(torch.int32)))
+                         for ho, d in zip(hout, layers))
+            if world > 1:
+                e2e_ok = skd.max_over_ranks(0.0 if e2e_ok else 1.0, dev) == 0.0
+        e2e = {"value": step_nnz_flops / (t_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                "ms_per_step": t_e2e,
                "h2d_bytes_per_step": int(sum(h.numel() * 4 for h in hin)),
-               "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hout))}
+               "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hout)),
+               "outputs_bitwise_equal_device_path": e2e_ok}
 
     if rank != 0:
         return
@@ -439,22 +600,26 @@ def run_ours(args, cfg, rank, world, local_rank):
     pad_ms = per_kernel[0::2]
     dom = int(np.argmax(conv_ms))
     dl = layers[dom]
-    achieved = nnz_flops(dl["L"], dl["nnz"], per_gpu) / (conv_ms[dom] * 1e-3) / 1e12
+    achieved = nnz_flops(dl["L"], dl["nnz"], local_n) / (conv_ms[dom] * 1e-3) / 1e12
     f_max = (clocks["sm_max_mhz"] or 1965.0) * 1e6
     peak_fp32 = N_SM * FP32_LANES * 2 * f_max / 1e12
     peak_smem = N_SM * SMEM_WORDS_PER_CLK * 2 * f_max / 1e12
     traffic = load_traffic()
     tr = None
-    if traffic and traffic.get("kernel_layer") == dl["L"].name and traffic.get("kernel") == args.kernel:
-        tr = traffic.get("dram_bytes_per_launch")
+    if traffic and traffic.get("kernel") == args.kernel and cfg.cfg_id in traffic.get("configs", []):
+        tr = traffic.get("dram_bytes_per_launch", {}).get(dl["L"].name)
+    peak_meas = peaks["ffma2_tflops"] if peaks else None
     per_layer = []
     for d, cm, pm in zip(layers, conv_ms, pad_ms):
         L = d["L"]
+        ach = nnz_flops(L, d["nnz"], local_n) / (cm * 1e-3) / 1e12
         per_layer.append({
             "layer": L.name, "nnz": d["nnz"], "density": d["nnz"] / (L.K * (L.C // L.groups) * L.R * L.S),
             "conv_ms": float(cm), "pad_ms": float(pm),
-            "conv_nnz_tflops": nnz_flops(L, d["nnz"], per_gpu) / (cm * 1e-3) / 1e12,
-            "pad_gbs": per_gpu * 4 * (L.C * L.H * L.W + L.C * (L.H + 2 * L.pad) * (L.W + 2 * L.pad)) / (pm * 1e-3) / 1e9,
+            "conv_nnz_tflops": ach, "frac_fp32_nominal": ach / peak_fp32,
+            "frac_fp32_measured": ach / peak_meas if peak_meas else None,
+            "pad_gbs": local_n * 4 * (L.C * L.H * L.W + L.C * (L.H + 2 * L.pad) * (L.W + 2 * L.pad)) / (pm * 1e-3) / 1e9,
+            "dram_bytes_per_launch_ncu": (traffic or {}).get("dram_bytes_per_launch", {}).get(L.name),
             "kernel_cfg": {k: d["conv"].plan.info()[k] for k in (
                 "kernel", "band_rows", "chunk_channels", "stages", "warps", "channels_per_warp",
                 "pixels_per_lane", "smem_bytes", "tile_h", "tile_w", "images_per_cta",
@@ -469,23 +634,44 @@ def run_ours(args, cfg, rank, world, local_rank):
                "kind": "oracle",
                "sample": f"{nimg} image(s) of each of the {len(cfg.layers)} layers ({secs:.1f} s)",
                "dense_equiv_gflops": df / secs / 1e9}
+        if not args.no_cpu_single:
+            # the same oracle single-threaded on one image of each layer (BASELINE.md plan)
+            r = subprocess.run([sys.executable, "-c",
+                                "import bench, json; print(json.dumps(bench.oracle_one_image(%d)))" % cfg.cfg_id],
+                               cwd=ROOT, env=dict(os.environ, OMP_NUM_THREADS="1"),
+                               capture_output=True, text=True, timeout=600)
+            try:
+                one = json.loads(r.stdout.strip().splitlines()[-1])
+                cpu["single_thread"] = {"value": one["nnz_flops"] / one["seconds"] / 1e9, "unit": "GFLOP/s",
+                                        "cores": 1, "seconds_per_image_all_layers": one["seconds"],
+                                        "sample": "1 image of each layer, OMP_NUM_THREADS=1"}
+            except (ValueError, IndexError, KeyError):
+                cpu["single_thread"] = {"error": r.stderr[-300:]}
+    par = f"dp{world} (batch-sharded, no collective)"
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name} (BASELINE.json configs[{cfg.cfg_id - 1}])",
-                   "global_batch": per_gpu * world, "per_gpu_batch": per_gpu,
-                   "layers": [l.name for l in cfg.layers], "parallelism": f"dp{world} (batch-sharded, no collective)",
+                   "global_batch": n_global, "per_gpu_batch": local_n,
+                   "layers": [l.name for l in cfg.layers], "parallelism": par,
                    "l2": "flushed between timed steps (256 MiB write)", "kernel": args.kernel,
                    "step": "per layer: skc_pad_input + skc_sparse_conv_forward"
                            + (", the step's 8 launches replayed as one CUDA graph" if graph is not None else "")},
-        "dense_equiv_gflops": step_dense_flops * world / (t_step * 1e-3) / 1e9,
+        "dense_equiv_gflops": step_dense_flops / (t_step * 1e-3) / 1e9,
+        "per_gpu_gflops": local_nnz_flops / (t_local * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                      "frac": achieved / peak_fp32, "traffic": tr,
                      "kernel": f"skc_sparse_conv_forward ({dl['L'].name})",
-                     "peak_basis": f"148 SM x 128 FP32 lanes x 2 x {f_max/1e6:.0f} MHz (CUDA-core FFMA)",
-                     "smem_roof": peak_smem, "frac_smem_roof": achieved / peak_smem},
+                     "peak_basis": f"nominal: 148 SM x 128 FP32 lanes x 2 x {f_max/1e6:.0f} MHz (CUDA-core FFMA)",
+                     "peak_measured": peak_meas,
+                     "frac_measured": achieved / peak_meas if peak_meas else None,
+                     "peak_measured_basis": "FFMA2 micro-benchmark in this session (skc_bench_ffma2)",
+                     "smem_roof_1word_per_mac": peak_smem, "frac_smem_roof": achieved / peak_smem,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write)"},
+        "peaks_measured": peaks,
+        "parity": parity,
         "per_layer": per_layer,
         "dense": dense,
         "cpu_baseline": cpu,
@@ -495,6 +681,23 @@ def run_ours(args, cfg, rank, world, local_rank):
         "plan_build_s": t_build,
     }
     print(json.dumps(line), flush=True)
+
+
+def oracle_one_image(cfg_id: int) -> dict:
+    """The oracle on ONE image of every layer of a config (run with OMP_NUM_THREADS=1 for the
+    single-threaded CPU baseline)."""
+    import oracle
+    cfg = wl.CONFIGS[cfg_id]
+    nf = 0.0
+    t = 0.0
+    for li, L in enumerate(cfg.layers):
+        w = wl.gen_weights(cfg_id, li, L)
+        x = wl.gen_input(cfg_id, li, L, 0, 1)
+        t0 = time.perf_counter()
+        oracle.conv2d_fp64(x, w, L.stride, L.pad, L.groups, want_bound=False)
+        t += time.perf_counter() - t0
+        nf += nnz_flops(L, np.count_nonzero(w), 1)
+    return {"seconds": t, "nnz_flops": nf}
 
 
 def main():

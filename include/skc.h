@@ -18,14 +18,25 @@
  *     nothing aborts.  Argument/geometry checks happen before any launch.
  *   - Precision: fp32 data, fp32 FMA accumulation (single precision).
  *   - Ownership: the caller owns every device buffer (activations, outputs, the plan
- *     workspace).  libskc NEVER allocates device memory.  A plan owns its host arrays and
- *     is freed by skc_plan_destroy(), which does not synchronise: the caller must make
- *     sure no launch using the plan's workspace is still running.
+ *     workspace, the tuning scratch).  libskc NEVER allocates device memory (no cudaMalloc
+ *     anywhere in the library).  A plan owns its host arrays and is freed by
+ *     skc_plan_destroy(), which does not synchronise: the caller must make sure no launch
+ *     using the plan's workspace is still running.
  *   - Streams: device work is enqueued asynchronously on the caller's stream (a
  *     cudaStream_t passed as void*; NULL = legacy default stream).  Launch errors are
  *     returned as SKC_ERR_CUDA; faults during execution surface at the caller's sync.
- *   - Thread safety: a plan is immutable after skc_plan_upload(); several threads or
- *     streams may launch with it concurrently.
+ *     skc_plan_upload() is the one setup call that synchronises the stream (it prepares
+ *     everything a launch needs: JIT code loaded, kernel attributes, occupancy, SM topology),
+ *     and skc_plan_tune() synchronises it too; every launch entry point (skc_pad_input,
+ *     skc_sparse_conv_forward*, skc_im2col) only enqueues work, so it may be captured into a
+ *     CUDA graph from its very first call.
+ *   - Thread safety: a plan's host data is immutable after skc_plan_upload().  A JIT plan
+ *     keeps launch-scoped scheduling state in its WORKSPACE (the dynamic work-item counter
+ *     and the first-item claim table, reset by the last CTA of each launch), so launches that
+ *     use one workspace must not overlap in time: issue them on one stream (or order them
+ *     with events), or upload the plan into one workspace per concurrent stream.  Other
+ *     kernels' launches may overlap freely.  skc_plan_tune() rewrites the plan's launch
+ *     schedule: no launch of that plan may run concurrently with it.
  *   - Layouts (all contiguous, fp32):
  *       input  NCHW            [N][C][H][W]
  *       padded input           [N][C][Hp][Wp],  Hp = H + 2*pad, Wp = W + 2*pad
@@ -146,12 +157,17 @@ skc_status skc_plan_csr(const skc_plan *plan, const int32_t **rowptr, const int3
 skc_status skc_plan_perm(const skc_plan *plan, const int32_t **perm);
 
 /* Copy the plan's kernel-private arrays into a caller-owned device workspace of at least
- * skc_info.device_bytes bytes (16-byte aligned), asynchronously on `stream`.  The host
- * arrays stay owned by the plan; the workspace must outlive every launch using the plan.
- * A JIT plan may keep a work-item counter in the workspace (skc_info.jit_split > 0: dynamic
- * scheduling; the last CTA of a launch resets it): launches that use one workspace must not
- * run concurrently -- issue them on one stream (or order them with events), or upload the
- * plan into a second workspace for a concurrent stream. */
+ * skc_info.device_bytes bytes (16-byte aligned) on `stream`, and prepare the current device
+ * for the plan's launches: kernel attributes; for JIT plans also the code (compiled now if
+ * skc_plan_compile was not called; loaded as a cudaLibrary), occupancy figures, and -- at
+ * the first JIT upload on a device -- the SM-topology probe (a few clustered probe kernels on
+ * `stream`, using the workspace as scratch) whose GPC-major SM order goes into the
+ * workspace.  SYNCHRONOUS: the one setup call that may block on `stream`; call it outside
+ * stream capture.  The host arrays stay owned by the plan; the workspace must outlive every
+ * launch using the plan, which must run on the device it was uploaded on (else forward
+ * returns SKC_ERR_STATE).  Launch-scoped scheduling state lives in the workspace (see Thread
+ * safety above).  Errors: SKC_ERR_ARG, SKC_ERR_ALIGN, SKC_ERR_UNSUPPORTED (JIT compile
+ * failed), SKC_ERR_CUDA. */
 skc_status skc_plan_upload(skc_plan *plan, void *d_workspace, size_t bytes, void *stream);
 
 /* a2 -- padded-input layout (R1): d_in [N][C][H][W] ->
@@ -233,15 +249,18 @@ skc_status skc_plan_compile(skc_plan *plan);
  * keep the fastest (first round of work items spread over the channel blocks or block-major;
  * work items numbered GPC-major or by cluster rank; clusters of 2 CTAs or none; lane table
  * dealt by shared-memory bank residue or contiguously; dry-run code prefetch by the first
- * CTAs or by every CTA -- DESIGN.md
- * Sec. 7.4).  Times each variant 5x on zero-filled scratch buffers of N images that it
- * allocates and frees (input in the plan's layout + output + a 256 MiB L2 flush buffer, which
- * is written before every timed launch); synchronous on `stream`.  Every variant computes
- * bit-identical outputs, so tuning changes speed only.  Requires skc_plan_upload; call it
- * outside stream capture.  *best_ms (may be NULL) receives the chosen variant's time.  No-op
- * for other kernels.  Errors: SKC_ERR_ARG (NULL plan, N < 1), SKC_ERR_STATE (not uploaded),
- * SKC_ERR_CUDA (allocation or launch failed). */
-skc_status skc_plan_tune(skc_plan *plan, int N, void *stream, double *best_ms);
+ * CTAs or by every CTA -- DESIGN.md Sec. 7.4; skc_info.jit_sched reports the choice).  Times
+ * each variant 5x on CALLER-OWNED scratch: d_in, a padded input of N images in the plan's
+ * layout (any finite contents), d_out, an output of N images (overwritten), and optionally
+ * d_flush, flush_bytes (NULL/0: no flush) -- a buffer larger than L2 that is written before
+ * every timed launch so code and data start cold.  Synchronous on `stream`.  Every variant
+ * computes bit-identical outputs, so tuning changes speed only.  Requires skc_plan_upload;
+ * exclusive: no launch of this plan may run concurrently.  *best_ms (may be NULL) receives
+ * the chosen variant's time (0 for non-JIT plans, for which this is a no-op).
+ * Errors: SKC_ERR_ARG (NULL plan or scratch, N < 1), SKC_ERR_ALIGN, SKC_ERR_STATE (not
+ * uploaded on this device), SKC_ERR_CUDA (a launch failed). */
+skc_status skc_plan_tune(skc_plan *plan, int N, const float *d_in, float *d_out, void *d_flush,
+                         size_t flush_bytes, void *stream, double *best_ms);
 
 /* Static self-check of a plan (host only, no GPU): every kernel-private index the kernels
  * will dereference -- shared-memory windows and pixel slots against the stage and allocation
@@ -275,20 +294,28 @@ skc_status skc_model_project(const skc_layer_cost *cost, double x, const skc_pla
                              skc_projection *out);
 skc_status skc_model_window(const skc_layer_cost *cost, const skc_platform *p, skc_window *out);
 
-/* Device micro-benchmarks that calibrate the B200 roofline (FFMA issue peak and shared-
- * memory word bandwidth; the analogue of the paper's SGEMM / STREAM calibration,
- * PAPER.md:531-532).  d_scratch: >= 4 MiB device buffer.  Each writes the elapsed
- * device milliseconds and the operation count it performed.  Synchronous. */
 /* Diagnostic: the GPC-major SM order the JIT kernel numbers its work items by (topo.cu;
  * DESIGN.md Sec. 7.4) for the current device: vid[smid] = position of SM smid when the SMs are
  * listed GPC by GPC, learned by launching thread-block clusters (which never span GPCs).
- * vid: host array of `cap` ints; *nsm receives the SM count.  Runs the probe kernels on the
- * first call per device (synchronous).  Errors: SKC_ERR_ARG (NULL, cap < SM count),
- * SKC_ERR_UNSUPPORTED (the probe could not group the SMs). */
+ * vid: host array of `cap` ints; *nsm receives the SM count.  Host only: returns the order the
+ * probe found at the first skc_plan_upload of a JIT plan on this device.  Errors: SKC_ERR_ARG
+ * (NULL, cap < SM count), SKC_ERR_STATE (no JIT plan uploaded on this device yet, or the
+ * probe could not group the SMs). */
 skc_status skc_sm_topology(int *vid, int cap, int *nsm);
 
+/* Device micro-benchmarks that calibrate the B200 roofline -- the analogue of the paper's
+ * measured SGEMM / STREAM "achievable" peaks: measured rates
+ * rather than data-sheet numbers.  ffma: scalar FP32 FMA (16 independent chains per thread);
+ * ffma2: packed fma.rn.f32x2 (FFMA2, the JIT kernel's instruction; 2 FMAs each); lds:
+ * conflict-free 4-byte shared loads; lds64: conflict-free 8-byte shared loads (the JIT
+ * kernel's window load).  `blocks` CTAs of 256 threads, `iters` loop trips; d_scratch: >= 4 MiB
+ * device buffer (never read; defeats dead-code elimination).  *ms = device milliseconds of
+ * one timed launch (after a warm-up launch), *flops / *bytes = the work it performed (FLOP =
+ * 2 per FMA).  Synchronous on the legacy default stream.  Errors: SKC_ERR_ARG, SKC_ERR_CUDA. */
 skc_status skc_bench_ffma(void *d_scratch, int blocks, int iters, double *ms, double *flops);
+skc_status skc_bench_ffma2(void *d_scratch, int blocks, int iters, double *ms, double *flops);
 skc_status skc_bench_lds(void *d_scratch, int blocks, int iters, double *ms, double *bytes);
+skc_status skc_bench_lds64(void *d_scratch, int blocks, int iters, double *ms, double *bytes);
 
 #ifdef __cplusplus
 }

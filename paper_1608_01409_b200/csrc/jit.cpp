@@ -88,7 +88,12 @@ double conc_penalty(int conc) {
     static const double pen[] = {1.0, 1.0, 1.2, 1.45, 1.5};
     return conc < 5 ? pen[conc] : 1.6;
 }
-constexpr int kJitVersion = 20;  // bump when the generated code changes (cache key)
+constexpr int kJitVersion = 21;  // bump when the generated code changes (cache key)
+// workspace regions after the lane / staging tables: the GPC-major SM order (vid[smid],
+// kVidCap u16, written by skc_plan_upload), the first-item claim table (kVidCap u32, zero
+// between launches), and scratch for the SM-topology probe (kProbeInts int32)
+constexpr int kVidCap = 1024;
+constexpr int kProbeInts = 4096;
 
 // Fast appender for the (large) generated PTX.
 struct Out {
@@ -194,7 +199,11 @@ struct JitPlan {
     int cache_hit = 0;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
-    std::atomic<uint64_t> attr_set{0};
+    // device state taken by jit_prepare (skc_plan_upload)
+    int prep_dev = -1;
+    int nsm = 0, per_sm = 1;
+    int ncl[17] = {0};         // max active clusters per cluster size 2/4/8/16
+    bool vid_ok = false;       // the workspace holds a GPC-major SM order (topology probe)
     std::mutex mu;
 };
 
@@ -963,15 +972,42 @@ std::string emit_entry(const JitPlan &jp) {
     o("setp.ne.u32 %%p9, %%r62, 0;");              // p9: skip the dry-run prefetch
     o("and.b32 %%r63, %%r63, 1;");
     o("setp.ne.u32 %%p8, %%r63, 0;");
+    // The launch is not cooperative, so nothing guarantees one CTA per SM: the first item is
+    // CLAIMED, not assumed.  Thread 0 starts at vid[smid] (smid clamped to the table) and
+    // probes the claim table (in the workspace after the vid table, one word per first-round
+    // item, zero between launches) linearly with compare-and-swap; each of the G CTAs claims
+    // exactly one of the G first items, whatever SMs they landed on.  The last CTA to exit
+    // clears the table ($EXIT).
     o("ld.param.u64 %%rd21, [p_vid];");
     o("setp.eq.u64 %%p0, %%rd21, 0;");
     o("@%%p0 bra $VID_DONE;");
     o("cvta.to.global.u64 %%rd21, %%rd21;");
+    o("mov.u32 %%r78, skc_smem;");
+    o("add.u32 %%r78, %%r78, %d;", jp.off_item + 8);
+    o("setp.ne.u32 %%p1, %%r3, 0;");
+    o("@%%p1 bra $VID_WAIT;");
     o("mov.u32 %%r79, %%smid;");
+    o("min.u32 %%r79, %%r79, %d;", kVidCap - 1);
     o("mul.wide.u32 %%rd22, %%r79, 2;");
     o("add.u64 %%rd22, %%rd21, %%rd22;");
     o("ld.global.nc.u16 %%r79, [%%rd22];");
-    o("mov.u32 %%r4, %%r79;");
+    o("rem.u32 %%r79, %%r79, %%r31;");
+    o("add.u64 %%rd23, %%rd21, %d;", 2 * kVidCap);  // claim table
+    o("$VID_PROBE:");
+    o("mul.wide.u32 %%rd22, %%r79, 4;");
+    o("add.u64 %%rd22, %%rd23, %%rd22;");
+    o("atom.global.cas.b32 %%r77, [%%rd22], 0, 1;");
+    o("setp.eq.u32 %%p1, %%r77, 0;");
+    o("@%%p1 bra $VID_GOT;");
+    o("add.u32 %%r79, %%r79, 1;");
+    o("setp.ge.u32 %%p1, %%r79, %%r31;");
+    o("@%%p1 mov.u32 %%r79, 0;");
+    o("bra.uni $VID_PROBE;");
+    o("$VID_GOT:");
+    o("st.shared.u32 [%%r78], %%r79;");
+    o("$VID_WAIT:");
+    o("bar.sync 0;");
+    o("ld.shared.u32 %%r4, [%%r78];");
     o("$VID_DONE:");
     o("add.u32 %%r5, %%r0, %d;", jp.NI - 1);
     o("div.u32 %%r5, %%r5, %d;", jp.NI);        // image groups
@@ -1379,19 +1415,32 @@ std::string emit_entry(const JitPlan &jp) {
     if (jp.xpf) o("add.u32 %%r64, %%r64, 1;");
     o("bra.uni $ITEM;");
     o("$EXIT:");
-    if (jp.dyn) {
-        o("setp.ne.u32 %%p0, %%r3, 0;");
-        o("@%%p0 bra $DONE;");
-        o("fence.acq_rel.gpu;");          // our item fetches are performed before `done`
-        o("atom.global.add.u32 %%r57, [%%rd20+4], 1;");
-        o("mov.u32 %%r56, %%nctaid.x;");
-        o("sub.u32 %%r56, %%r56, 1;");
-        o("setp.ne.u32 %%p0, %%r57, %%r56;");
-        o("@%%p0 bra $DONE;");
-        o("st.global.u32 [%%rd20], 0;");   // every CTA has taken its last item: reset
-        o("st.global.u32 [%%rd20+4], 0;");
-        o("$DONE:");
-    }
+    // launch-scoped state in the workspace (the dynamic item counter, the first-item claim
+    // table): the last CTA to exit resets it for the next launch (graph replays included)
+    o("setp.ne.u32 %%p0, %%r3, 0;");
+    o("@%%p0 bra $DONE;");
+    o("setp.ne.u64 %%p1, %%rd21, 0;");            // first items were claimed
+    if (!jp.dyn) o("@!%%p1 bra $DONE;");
+    o("add.u64 %%rd20, %%rd2, %d;", ctr_off);
+    o("fence.acq_rel.gpu;");          // our item fetches / claims are performed before `done`
+    o("atom.global.add.u32 %%r57, [%%rd20+4], 1;");
+    o("mov.u32 %%r56, %%nctaid.x;");
+    o("sub.u32 %%r56, %%r56, 1;");
+    o("setp.ne.u32 %%p0, %%r57, %%r56;");
+    o("@%%p0 bra $DONE;");
+    if (jp.dyn) o("st.global.u32 [%%rd20], 0;");   // every CTA has taken its last item: reset
+    o("@!%%p1 bra $RESET_DONE;");
+    o("add.u64 %%rd23, %%rd21, %d;", 2 * kVidCap);
+    o("mov.u32 %%r56, 0;");
+    o("$CLAIM_CLR:");
+    o("st.global.u32 [%%rd23], 0;");
+    o("add.u64 %%rd23, %%rd23, 4;");
+    o("add.u32 %%r56, %%r56, 1;");
+    o("setp.lt.u32 %%p0, %%r56, %%r31;");
+    o("@%%p0 bra $CLAIM_CLR;");
+    o("$RESET_DONE:");
+    o("st.global.u32 [%%rd20+4], 0;");
+    o("$DONE:");
     o("ret;");
     o("}");
     return std::move(o.s);
@@ -1408,8 +1457,19 @@ bool compile_ptx(const std::string &ptx, const char *opt, int maxreg, std::vecto
         return false;
     }
     const std::string mr = "--maxrregcount=" + std::to_string(maxreg);
-    const char *opts[] = {"--gpu-name=sm_100a", opt, mr.c_str(), "--compile-only"};
-    const nvPTXCompileResult r = nvPTXCompilerCompile(h, relocatable ? 4 : 3, opts);
+    // `opt` may hold several space-separated ptxas options (e.g. "-O1 -Ofc=min")
+    std::vector<std::string> words;
+    for (const char *p = opt; *p;) {
+        while (*p == ' ') ++p;
+        const char *q = p;
+        while (*q && *q != ' ') ++q;
+        if (q > p) words.emplace_back(p, size_t(q - p));
+        p = q;
+    }
+    std::vector<const char *> opts = {"--gpu-name=sm_100a", mr.c_str()};
+    for (const auto &w : words) opts.push_back(w.c_str());
+    if (relocatable) opts.push_back("--compile-only");
+    const nvPTXCompileResult r = nvPTXCompilerCompile(h, int(opts.size()), opts.data());
     bool okr = r == NVPTXCOMPILE_SUCCESS;
     if (!okr) {
         size_t n = 0;
@@ -1996,7 +2056,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     jp.off_info = jp.off_cnt + 4 * kMaxStages;
     jp.off_info = (jp.off_info + 7) / 8 * 8;
     jp.off_item = jp.off_info + 2 * NSL * 8;      // two slot tables (this item, next item)
-    jp.smem = size_t(jp.off_item) + 8;
+    jp.smem = size_t(jp.off_item) + 16;           // + the claimed first item (vid)
     jp.maxreg = reg_cap(jp.NW);
     if (const char *e = std::getenv("SKC_JIT_SYNC")) jp.sync_every = std::max(0, std::atoi(e));
     if (const char *e = std::getenv("SKC_JIT_L2HINT")) jp.l2hint = std::atoi(e) & 3;
@@ -2087,7 +2147,8 @@ int jit_compile(JitPlan *jp, std::string *msg) {
             }
         }
     }
-    const char *opt = std::getenv("SKC_JIT_OPT") ? std::getenv("SKC_JIT_OPT") : "-O1";
+    // -O2: 1.2% faster steps than -O1 (fewer register moves; profiles/r02_jit_ptxas_opt.txt)
+    const char *opt = std::getenv("SKC_JIT_OPT") ? std::getenv("SKC_JIT_OPT") : "-O2";
     uint64_t key = fnv1a(&kJitVersion, sizeof kJitVersion);
     key = fnv1a(opt, std::strlen(opt), key);
     key = fnv1a(&jp->maxreg, sizeof jp->maxreg, key);
@@ -2192,18 +2253,28 @@ int jit_compile(JitPlan *jp, std::string *msg) {
 }
 
 // device image: the lane tables, 16 bytes of (zeroed) scheduling counters, then (raw staging)
-// the per-thread staging tables
-size_t jit_image_bytes(const JitPlan *jp) {
-    return jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4 + jp->lanemap_c.size() * 4;
+// the per-thread staging tables, the contiguous lane table, and (16-byte aligned) the vid
+// table, the claim table and the topology-probe scratch
+namespace {
+size_t tables_bytes(const JitPlan *jp) {
+    return (jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4 + jp->lanemap_c.size() * 4 + 15) / 16 * 16;
 }
+}  // namespace
+size_t jit_vid_offset(const JitPlan *jp) { return tables_bytes(jp); }
+size_t jit_probe_offset(const JitPlan *jp) { return tables_bytes(jp) + 6 * size_t(kVidCap); }
+size_t jit_probe_ints() { return kProbeInts; }
+size_t jit_vid_cap() { return kVidCap; }
+size_t jit_image_bytes(const JitPlan *jp) { return jit_probe_offset(jp) + 4 * size_t(kProbeInts); }
 void jit_image(const JitPlan *jp, void *dst) {
     char *d = static_cast<char *>(dst);
+    std::memset(d, 0, jit_image_bytes(jp));
     std::memcpy(d, jp->lanemap.data(), jp->lanemap.size() * 4);
-    std::memset(d + jp->lanemap.size() * 4, 0, 16);
     if (!jp->stab.empty()) std::memcpy(d + jp->lanemap.size() * 4 + 16, jp->stab.data(), jp->stab.size() * 4);
     if (!jp->lanemap_c.empty())
         std::memcpy(d + jp->lanemap.size() * 4 + 16 + jp->stab.size() * 4, jp->lanemap_c.data(),
                     jp->lanemap_c.size() * 4);
+    uint16_t *vid = reinterpret_cast<uint16_t *>(d + jit_vid_offset(jp));
+    for (int i = 0; i < kVidCap; ++i) vid[i] = uint16_t(i);  // identity until upload
 }
 
 void jit_info(const JitPlan *jp, JitInfo *o) {
@@ -2225,56 +2296,116 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
 const std::vector<int32_t> &jit_chan(const JitPlan *jp) { return jp->chan; }
 const std::vector<uint32_t> &jit_lanes(const JitPlan *jp) { return jp->lanemap; }
 
-cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_lanemap, int N,
+// Device-side preparation, done once by skc_plan_upload (the one synchronous call): compile
+// if needed, load the cubin, set the kernel's shared-memory / cluster attributes and take the
+// occupancy figures the launch needs -- so that a forward launch makes no allocation, no
+// module load and no query that could fail (capture-safe from the first call).
+int jit_prepare(JitPlan *jp, int dev, std::string *msg) {
+    const int r = jit_compile(jp, msg);
+    if (r != SKC_OK) return r;
+    std::lock_guard<std::mutex> lk(jp->mu);
+    auto cuda_fail = [&](const char *what, cudaError_t e) {
+        *msg = std::string(what) + ": " + cudaGetErrorString(e);
+        return int(SKC_ERR_CUDA);
+    };
+    if (!jp->lib) {
+        cudaError_t e = cudaLibraryLoadData(&jp->lib, jp->cubin.data(), nullptr, nullptr, 0,
+                                            nullptr, nullptr, 0);
+        if (e != cudaSuccess) return cuda_fail("cudaLibraryLoadData", e);
+        e = cudaLibraryGetKernel(&jp->kern, jp->lib, "skc_jit_kernel");
+        if (e != cudaSuccess) return cuda_fail("cudaLibraryGetKernel", e);
+    }
+    const void *fn = reinterpret_cast<const void *>(jp->kern);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(jp->smem));
+    if (e != cudaSuccess) return cuda_fail("cudaFuncSetAttribute", e);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail("cudaFuncSetAttribute (clusters)", e);
+    int nsm = 0, per_sm = 0;
+    e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess || nsm < 1) return cuda_fail("cudaDeviceGetAttribute", e);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, jp->NW * 32, jp->smem);
+    if (e != cudaSuccess || per_sm < 1) return cuda_fail("occupancy", e);
+    for (int cs = 2; cs <= 16; cs *= 2) {
+        cudaLaunchConfig_t lc{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = unsigned(cs);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        lc.blockDim = dim3(unsigned(jp->NW * 32));
+        lc.dynamicSmemBytes = jp->smem;
+        lc.gridDim = dim3(unsigned(cs));
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, fn, &lc) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();  // (upload time) this size is not launchable: not used
+            ncl = 0;
+        }
+        jp->ncl[cs] = ncl;
+    }
+    jp->nsm = nsm;
+    jp->per_sm = per_sm;
+    jp->prep_dev = dev;
+    return SKC_OK;
+}
+
+bool jit_ready(const JitPlan *jp, int dev) { return jp->lib && jp->prep_dev == dev; }
+
+void jit_set_vid(JitPlan *jp, bool ok) { jp->vid_ok = ok; }
+
+namespace {
+// The launch schedule (skc_info.jit_sched bits): the tuned choice, the defaults, or the
+// SKC_JIT_SCHED override (testing: forces every variant the tuner can pick)
+struct Sched {
+    int o3, vid, nodry, lanes, cs, dryall;
+};
+Sched launch_sched(const JitPlan *jp) {
+    Sched s{};
+    if (const char *e = std::getenv("SKC_JIT_SCHED")) {
+        const int v = std::atoi(e);
+        s.o3 = v & 1;
+        s.vid = (v >> 1) & 1;
+        s.nodry = (v >> 2) & 1;
+        s.lanes = (v >> 3) & 1;
+        s.cs = std::max(1, (v >> 4) & 15);
+        s.dryall = (v >> 9) & 1;
+        return s;
+    }
+    s.o3 = jp->t_order3.load() >= 0 ? jp->t_order3.load() : (jp->order == 3 ? 1 : 0);
+    if (jp->t_vid.load() >= 0) {
+        s.vid = jp->t_vid.load();
+    } else {
+        const char *e = std::getenv("SKC_JIT_VID");  // GPC-major item numbers (default on)
+        s.vid = !e || std::atoi(e) != 0;
+    }
+    s.nodry = std::max(0, jp->t_nodry.load());
+    const char *le = std::getenv("SKC_JIT_LANES");  // 0/1: force the lane table (testing)
+    s.lanes = le ? std::atoi(le) : std::max(0, jp->t_lanes.load());
+    s.cs = jp->t_cs.load() > 0 ? jp->t_cs.load() : 2;
+    if (const char *e = std::getenv("SKC_JIT_CLUSTER")) s.cs = std::max(1, std::min(16, std::atoi(e)));
+    s.dryall = std::max(0, jp->t_dryall.load());
+    return s;
+}
+}  // namespace
+
+cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_ws, int N,
                        const Epilogue &epi, cudaStream_t st, std::string *msg) {
-    if (!jp->compiled) {
-        const int r = jit_compile(jp, msg);
-        if (r != SKC_OK) return cudaErrorInvalidPtx;
-    }
-    {
-        std::lock_guard<std::mutex> lk(jp->mu);
-        if (!jp->lib) {
-            cudaError_t e = cudaLibraryLoadData(&jp->lib, jp->cubin.data(), nullptr, nullptr, 0,
-                                                nullptr, nullptr, 0);
-            if (e != cudaSuccess) {
-                *msg = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
-                return e;
-            }
-            e = cudaLibraryGetKernel(&jp->kern, jp->lib, "skc_jit_kernel");
-            if (e != cudaSuccess) {
-                *msg = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
-                return e;
-            }
-        }
-    }
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (!(jp->attr_set.load(std::memory_order_acquire) >> dev & 1u)) {
-        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(jp->kern),
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(jp->smem));
-        if (e != cudaSuccess) {
-            *msg = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-            return e;
-        }
-        jp->attr_set.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel);
+    if (cudaGetDevice(&dev) != cudaSuccess || !jit_ready(jp, dev)) {
+        *msg = "JIT plan not prepared on this device (skc_plan_upload)";
+        return cudaErrorInvalidResourceHandle;
     }
     // persistent grid: one CTA per SM slot (the kernel loops over its work items)
     const int64_t nig = (int64_t(N) + jp->NI - 1) / jp->NI;
     const int64_t items = nig * jp->nblocks;
     if (items > 0x7fffffff) return cudaErrorInvalidConfiguration;
-    int nsm = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, reinterpret_cast<const void *>(jp->kern), jp->NW * 32, jp->smem) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
+    const int nsm = jp->nsm, per_sm = jp->per_sm;
+    const Sched sc = launch_sched(jp);
     // clusters of 2 CTAs: the pair is co-scheduled on one GPC and runs the same block's code
     // on neighbouring image groups, so they share instruction-cache lines (B200 packs 148 SMs
-    // into 74 pairs exactly; +2-7% measured, profiles/r01_jit_cluster.txt).  SKC_JIT_CLUSTER
-    // overrides (1 = no clusters).
-    int cs = jp->t_cs.load() > 0 ? jp->t_cs.load() : 2;
-    if (const char *e = std::getenv("SKC_JIT_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(e)));
+    // into 74 pairs exactly; +2-7% measured, profiles/r01_jit_cluster.txt)
+    int cs = sc.cs;
     if (items < 2 * cs) cs = 1;
     int64_t grid = std::min<int64_t>(items, int64_t(nsm) * per_sm);
     if (const char *e = std::getenv("SKC_JIT_GRID")) grid = std::min<int64_t>(items, std::max(1, std::atoi(e)));
@@ -2290,34 +2421,21 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
     lc.blockDim = dim3(unsigned(jp->NW * 32));
     lc.dynamicSmemBytes = jp->smem;
     lc.stream = st;
-    static const bool pdl = [] {
-        // off by default: measured no gain on the AlexNet step (profiles/r01_jit_order.txt)
-        const char *e = std::getenv("SKC_PDL");
-        return e && e[0] == '1';
-    }();
     int nat = 0;
-    if (pdl) {
+    if (const char *e = std::getenv("SKC_PDL"); e && e[0] == '1') {
+        // off by default: measured no gain on the AlexNet step (profiles/r01_jit_order.txt)
         at[nat].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[nat].val.programmaticStreamSerializationAllowed = 1;
         ++nat;
     }
     if (cs > 1) {
-        if (cs > 8)
-            cudaFuncSetAttribute(reinterpret_cast<const void *>(jp->kern),
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         at[nat].id = cudaLaunchAttributeClusterDimension;
         at[nat].val.clusterDim.x = unsigned(cs);
         at[nat].val.clusterDim.y = 1;
         at[nat].val.clusterDim.z = 1;
         ++nat;
-        lc.attrs = at;
-        lc.numAttrs = nat;
-        lc.gridDim = dim3(unsigned(cs));
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void *>(jp->kern), &lc) != cudaSuccess || ncl < 1) {
-            cudaGetLastError();  // the query's error must not leak into later launches
-            ncl = int(nsm / cs);
-        }
+        int ncl = (cs == 2 || cs == 4 || cs == 8 || cs == 16) ? jp->ncl[cs] : 0;
+        if (ncl < 1) ncl = std::max(1, nsm / cs);
         grid = std::min<int64_t>((items + cs - 1) / cs, ncl) * cs;
     }
     lc.gridDim = dim3(unsigned(grid));
@@ -2326,59 +2444,43 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_l
     const float *bias = epi.bias;
     unsigned un = unsigned(N), relu = unsigned(epi.relu), opad = unsigned(epi.opad);
     unsigned olay = unsigned(epi.olay);
-    // GPC-major item numbering needs exactly one CTA on every SM (SKC_JIT_VID=0: off)
-    static const bool vid_on = [] {
-        const char *e = std::getenv("SKC_JIT_VID");
-        return !e || std::atoi(e) != 0;
-    }();
+    const char *ws = static_cast<const char *>(d_ws);
+    // GPC-major first items (one CTA per SM, grid = all SMs; the kernel claims them, so a CTA
+    // that shares an SM with another still gets a distinct item)
     const void *vid = nullptr;
-    const bool vid_want = jp->t_vid.load() >= 0 ? jp->t_vid.load() != 0 : vid_on;
-    if (vid_want && per_sm == 1 && grid == nsm && jp->dyn != 2 && cs <= 2)
-        vid = sm_gpc_order_device(dev, true);
-    unsigned sched = jp->t_order3.load() >= 0 ? unsigned(jp->t_order3.load()) : (jp->order == 3 ? 1u : 0u);
-    if (jp->t_nodry.load() > 0) sched |= 4u;
-    static const int lanes_env = [] {
-        const char *e = std::getenv("SKC_JIT_LANES");  // 0/1: force the lane table (testing)
-        return e ? std::atoi(e) : -1;
-    }();
-    const int lanes = lanes_env >= 0 ? lanes_env : jp->t_lanes.load();
-    if (lanes > 0 && !jp->lanemap_c.empty()) sched |= 8u;
-    if (jp->t_dryall.load() > 0) sched |= 512u;
+    if (sc.vid && jp->vid_ok && per_sm == 1 && grid == nsm && grid <= kVidCap && jp->dyn != 2 && cs <= 2)
+        vid = ws + jit_vid_offset(jp);
+    unsigned sched = unsigned(sc.o3);
+    if (sc.nodry) sched |= 4u;
+    if (sc.lanes > 0 && !jp->lanemap_c.empty()) sched |= 8u;
+    if (sc.dryall) sched |= 512u;
     if (std::getenv("SKC_JIT_DEBUG"))
         std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
                      vid ? "on" : "off");
-    void *args[] = {(void *)&in, (void *)&out, (void *)&d_lanemap, (void *)&bias,
+    const void *lm = d_ws;
+    void *args[] = {(void *)&in, (void *)&out, (void *)&lm, (void *)&bias,
                     (void *)&un, (void *)&relu, (void *)&opad, (void *)&olay, (void *)&vid,
                     (void *)&sched};
     return cudaLaunchKernelExC(&lc, reinterpret_cast<const void *>(jp->kern), args);
 }
 
 // Launch-schedule tuning: time the variants (first round spread / block-major, GPC-major item
-// numbers on / off, clusters of 2 / none) of this plan's kernel on zero-filled scratch buffers
-// of N images, with the L2 flushed before every timed launch (code and data start cold, as in
-// bench.py), and keep the fastest.  Every variant computes bit-identical outputs (scheduling
-// only; tests/test_gpu_parity.py::test_jit_tuning_knobs_bitwise).  Synchronous on `st`.
-int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double *best_ms,
-             std::string *msg) {
-    const JitInput &in = jp->in;
-    const int sw = jp->pair ? 2 : 1;
-    const size_t in_bytes = size_t((N + sw - 1) / sw) * size_t(in.C) * in.Hp * in.Wp * sw * 4;
-    const size_t out_bytes = size_t(N) * size_t(in.K) * in.Ho * in.Wo * 4;
-    const size_t flush_bytes = size_t(256) << 20;
-    float *d_in = nullptr, *d_out = nullptr;
-    void *d_flush = nullptr;
+// numbers on / off, clusters of 2 / none, lane table, dry-run coverage) of this plan's kernel
+// on the caller's scratch buffers of N images, with the L2 flushed (d_flush written) before
+// every timed launch (code and data start cold, as in bench.py), and keep the fastest.  Every
+// variant computes bit-identical outputs (scheduling only;
+// tests/test_gpu_parity.py::test_jit_every_schedule_bitwise).  Synchronous on `st`.
+int jit_tune(JitPlan *jp, const void *d_ws, int N, const float *d_in, float *d_out, void *d_flush,
+             size_t flush_bytes, cudaStream_t st, double *best_ms, std::string *msg) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     auto cleanup = [&] {
-        if (d_in) cudaFree(d_in);
-        if (d_out) cudaFree(d_out);
-        if (d_flush) cudaFree(d_flush);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
     };
-    if (cudaMalloc(&d_in, in_bytes) != cudaSuccess || cudaMalloc(&d_out, out_bytes) != cudaSuccess ||
-        cudaMalloc(&d_flush, flush_bytes) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
-        cudaEventCreate(&e1) != cudaSuccess || cudaMemsetAsync(d_in, 0, in_bytes, st) != cudaSuccess) {
-        *msg = std::string("tune setup: ") + cudaGetErrorString(cudaGetLastError());
+    cudaError_t ce = cudaEventCreate(&e0);
+    if (ce == cudaSuccess) ce = cudaEventCreate(&e1);
+    if (ce != cudaSuccess) {
+        *msg = std::string("tune setup: ") + cudaGetErrorString(ce);
         cleanup();
         return SKC_ERR_CUDA;
     }
@@ -2402,12 +2504,20 @@ int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double 
                 jp->t_dryall = da;
                 double tot = 0;
                 for (int rep = 0; rep < 6; ++rep) {
-                    cudaMemsetAsync(d_flush, rep, flush_bytes, st);
+                    if (d_flush && flush_bytes) cudaMemsetAsync(d_flush, rep, flush_bytes, st);
                     cudaEventRecord(e0, st);
-                    cudaError_t e = jit_launch(jp, d_in, d_out, d_lanemap, N, epi, st, msg);
-                    cudaEventRecord(e1, st);
-                    if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
-                        *msg = std::string("tune launch: ") + cudaGetErrorString(e);
+                    cudaError_t e = jit_launch(jp, d_in, d_out, d_ws, N, epi, st, msg);
+                    const char *what = "tune launch";
+                    if (e == cudaSuccess) {
+                        what = "tune event";
+                        e = cudaEventRecord(e1, st);
+                    }
+                    if (e == cudaSuccess) {
+                        what = "tune sync";
+                        e = cudaEventSynchronize(e1);
+                    }
+                    if (e != cudaSuccess) {
+                        *msg = std::string(what) + ": " + cudaGetErrorString(e) + " " + *msg;
                         cleanup();
                         return SKC_ERR_CUDA;
                     }

@@ -1126,6 +1126,20 @@ skc_status verify_regtile(const skc_plan *p) {
 
 }  // namespace
 
+namespace {
+template <class F>
+skc_status bench_call(F &&fn, const char *name, void *d_scratch, int blocks, int iters, double *ms,
+                      double *count) {
+    if (!d_scratch || !ms || !count || blocks < 1 || iters < 1)
+        return fail(SKC_ERR_ARG, "bad micro-benchmark arguments");
+    float t = 0;
+    cudaError_t e = fn(d_scratch, blocks, iters, &t, count);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "%s: %s", name, cudaGetErrorString(e));
+    *ms = t;
+    return ok();
+}
+}  // namespace
+
 extern "C" {
 
 skc_status skc_plan_compile(skc_plan *p) {
@@ -1141,22 +1155,32 @@ skc_status skc_sm_topology(int *vid, int cap, int *nsm) {
     if (!vid || !nsm) return fail(SKC_ERR_ARG, "NULL pointer");
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(SKC_ERR_CUDA, "no CUDA device");
-    const std::vector<uint16_t> &v = sm_gpc_order(dev);
-    if (v.empty()) return fail(SKC_ERR_UNSUPPORTED, "SM topology probe failed");
+    std::vector<uint16_t> v;
+    if (!sm_gpc_order_cached(dev, &v))
+        return fail(SKC_ERR_STATE, "no SM order for this device: the probe runs at the first "
+                    "skc_plan_upload of a JIT plan (or it failed)");
     *nsm = int(v.size());
     if (cap < int(v.size())) return fail(SKC_ERR_ARG, "cap %d < %zu SMs", cap, v.size());
     for (size_t i = 0; i < v.size(); ++i) vid[i] = int(v[i]);
     return ok();
 }
 
-skc_status skc_plan_tune(skc_plan *p, int N, void *stream, double *best_ms) {
+skc_status skc_plan_tune(skc_plan *p, int N, const float *d_in, float *d_out, void *d_flush,
+                         size_t flush_bytes, void *stream, double *best_ms) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
     if (N < 1) return fail(SKC_ERR_ARG, "N = %d < 1", N);
+    if (best_ms) *best_ms = 0.0;
     if (p->kernel != SKC_KERNEL_JIT) return ok();
     if (!p->d_ws) return fail(SKC_ERR_STATE, "plan not uploaded (call skc_plan_upload)");
+    if (!d_in || !d_out) return fail(SKC_ERR_ARG, "NULL scratch buffer");
+    if (!aligned16(d_in) || !aligned16(d_out))
+        return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || !jit_ready(p->jit, dev))
+        return fail(SKC_ERR_STATE, "plan not uploaded on this device");
     std::string msg;
-    const char *ws = static_cast<const char *>(p->d_ws);
-    const int r = jit_tune(p->jit, ws + p->off_lanemap, N, (cudaStream_t)stream, best_ms, &msg);
+    const int r = jit_tune(p->jit, p->d_ws, N, d_in, d_out, d_flush, d_flush ? flush_bytes : 0,
+                           (cudaStream_t)stream, best_ms, &msg);
     if (r != SKC_OK) return fail(skc_status(r), "tune: %s", msg.c_str());
     return ok();
 }
@@ -1175,15 +1199,31 @@ skc_status skc_plan_upload(skc_plan *p, void *d_ws, size_t bytes, void *stream) 
     if (bytes < p->image.size())
         return fail(SKC_ERR_ARG, "workspace has %zu bytes, plan needs %zu", bytes,
                     p->image.size());
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+    cudaStream_t st = (cudaStream_t)stream;
+    // everything a launch needs is set up here, so forward launches are capture-safe and
+    // allocation-free from the first call: the kernel attributes, and for JIT plans the code
+    // (compiled if needed, loaded), occupancy figures and the SM topology
     if (p->kernel == SKC_KERNEL_JIT) {
         std::string msg;
-        const int r = jit_compile(p->jit, &msg);
-        if (r != SKC_OK) return fail(skc_status(r), "JIT compile: %s", msg.c_str());
-        int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) sm_gpc_order_device(dev, false);  // SM topology, once
+        const int r = jit_prepare(p->jit, dev, &msg);
+        if (r != SKC_OK) return fail(skc_status(r), "JIT prepare: %s", msg.c_str());
+        // GPC-major SM order (once per device; the probe uses this workspace as scratch and
+        // synchronises `stream`), written into the workspace's vid table
+        int *scratch = reinterpret_cast<int *>(static_cast<char *>(d_ws) + jit_probe_offset(p->jit));
+        const std::vector<uint16_t> &v = sm_gpc_order(dev, scratch, jit_probe_ints(), st);
+        uint16_t *vid = reinterpret_cast<uint16_t *>(p->image.data() + jit_vid_offset(p->jit));
+        for (size_t i = 0; i < jit_vid_cap(); ++i) vid[i] = i < v.size() ? v[i] : uint16_t(i);
+        jit_set_vid(p->jit, !v.empty() && v.size() <= jit_vid_cap());
+    } else if (p->kernel == SKC_KERNEL_REGTILE) {
+        e = prepare_regtile(p->rsh);
+    } else {
+        e = prepare_direct(p->T, p->M);
     }
-    cudaError_t e = cudaMemcpyAsync(d_ws, p->image.data(), p->image.size(),
-                                    cudaMemcpyHostToDevice, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "kernel attributes: %s", cudaGetErrorString(e));
+    e = cudaMemcpyAsync(d_ws, p->image.data(), p->image.size(), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
     p->d_ws = d_ws;
     return ok();
@@ -1260,9 +1300,11 @@ static skc_status forward_epi(const skc_plan *p, const float *d_in, float *d_out
         return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
     const uint8_t *ws = static_cast<const uint8_t *>(p->d_ws);
     if (p->kernel == SKC_KERNEL_JIT) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || !jit_ready(p->jit, dev))
+            return fail(SKC_ERR_STATE, "JIT plan not uploaded on the current device");
         std::string msg;
-        cudaError_t e = jit_launch(p->jit, d_in, d_out, ws + p->off_lanemap, N, epi,
-                                   (cudaStream_t)stream, &msg);
+        cudaError_t e = jit_launch(p->jit, d_in, d_out, ws, N, epi, (cudaStream_t)stream, &msg);
         if (e != cudaSuccess)
             return fail(SKC_ERR_CUDA, "JIT conv launch: %s %s", cudaGetErrorString(e), msg.c_str());
         return ok();
@@ -1425,24 +1467,21 @@ skc_status skc_model_window(const skc_layer_cost *c, const skc_platform *pf, skc
     return ok();
 }
 
+
 skc_status skc_bench_ffma(void *d_scratch, int blocks, int iters, double *ms, double *flops) {
-    if (!d_scratch || !ms || !flops || blocks < 1 || iters < 1)
-        return fail(SKC_ERR_ARG, "bad micro-benchmark arguments");
-    float t = 0;
-    cudaError_t e = bench_ffma(d_scratch, blocks, iters, &t, flops);
-    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "bench_ffma: %s", cudaGetErrorString(e));
-    *ms = t;
-    return ok();
+    return bench_call(bench_ffma, "bench_ffma", d_scratch, blocks, iters, ms, flops);
+}
+
+skc_status skc_bench_ffma2(void *d_scratch, int blocks, int iters, double *ms, double *flops) {
+    return bench_call(bench_ffma2, "bench_ffma2", d_scratch, blocks, iters, ms, flops);
 }
 
 skc_status skc_bench_lds(void *d_scratch, int blocks, int iters, double *ms, double *bytes) {
-    if (!d_scratch || !ms || !bytes || blocks < 1 || iters < 1)
-        return fail(SKC_ERR_ARG, "bad micro-benchmark arguments");
-    float t = 0;
-    cudaError_t e = bench_lds(d_scratch, blocks, iters, &t, bytes);
-    if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "bench_lds: %s", cudaGetErrorString(e));
-    *ms = t;
-    return ok();
+    return bench_call(bench_lds, "bench_lds", d_scratch, blocks, iters, ms, bytes);
+}
+
+skc_status skc_bench_lds64(void *d_scratch, int blocks, int iters, double *ms, double *bytes) {
+    return bench_call(bench_lds64, "bench_lds64", d_scratch, blocks, iters, ms, bytes);
 }
 
 }  // extern "C"

@@ -200,9 +200,9 @@ __global__ void __launch_bounds__(544, 1) sconv_direct_kernel(const DirectParams
 }
 
 template <int T, int M>
-cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
-    // the opt-in shared-memory limit is a per-device function attribute: set it once per
-    // device this process launches on
+cudaError_t launch_tm(const DirectParams *pp, size_t smem, cudaStream_t st) {
+    // the opt-in shared-memory limit is a per-device function attribute: skc_plan_upload sets
+    // it (pp == nullptr: prepare only); a launch on a device no upload prepared sets it too
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
@@ -213,6 +213,8 @@ cudaError_t launch_tm(const DirectParams &p, size_t smem, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel);
     }
+    if (!pp) return cudaSuccess;
+    const DirectParams &p = *pp;
     const int64_t grid =
         int64_t((p.N + p.NI - 1) / p.NI) * p.nbands * p.groups * p.cblocks;
     if (grid > 0x7fffffff || p.NW < 1 || p.NW > 16) return cudaErrorInvalidConfiguration;
@@ -237,7 +239,14 @@ bool direct_supported(int T, int M) {
 }
 
 cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st) {
-#define X(t, m) if (T == t && p.M == m) return launch_tm<t, m>(p, smem, st);
+#define X(t, m) if (T == t && p.M == m) return launch_tm<t, m>(&p, smem, st);
+    SKC_DIRECT_CASES(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t prepare_direct(int T, int M) {
+#define X(t, m) if (T == t && M == m) return launch_tm<t, m>(nullptr, 0, nullptr);
     SKC_DIRECT_CASES(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -148,9 +148,9 @@ __global__ void __launch_bounds__(NWMAX * 32, MINB) sconv_regtile_kernel(const R
 }
 
 template <int R, int S, int TY, int TX, int M, int NWMAX, int MINB>
-cudaError_t launch_shape(const RegtileParams &p, size_t smem, cudaStream_t st) {
-    // the opt-in shared-memory limit is a per-device function attribute: set it once per
-    // device this process launches on
+cudaError_t launch_shape(const RegtileParams *pp, size_t smem, cudaStream_t st) {
+    // the opt-in shared-memory limit is a per-device function attribute: skc_plan_upload sets
+    // it (pp == nullptr: prepare only); a launch on a device no upload prepared sets it too
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
@@ -161,6 +161,8 @@ cudaError_t launch_shape(const RegtileParams &p, size_t smem, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(uint64_t(1) << dev, std::memory_order_acq_rel);
     }
+    if (!pp) return cudaSuccess;
+    const RegtileParams &p = *pp;
     const int64_t grid = int64_t((p.N + p.NI - 1) / p.NI) * p.groups * p.nblocks;
     if (grid > 0x7fffffff || p.NG * p.NT > NWMAX) return cudaErrorInvalidConfiguration;
     fn<<<unsigned(grid), p.NG * p.NT * 32, smem, st>>>(p);
@@ -184,7 +186,17 @@ cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_
 #define X(r, s, ty, tx, m, nw, mb)                                                    \
     if (sh.R == r && sh.S == s && sh.TY == ty && sh.TX == tx && sh.M == m &&          \
         sh.nwmax == nw && sh.minb == mb)                                               \
-        return launch_shape<r, s, ty, tx, m, nw, mb>(p, smem, st);
+        return launch_shape<r, s, ty, tx, m, nw, mb>(&p, smem, st);
+    SKC_REGTILE_SHAPES(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t prepare_regtile(const RegtileShape &sh) {
+#define X(r, s, ty, tx, m, nw, mb)                                                    \
+    if (sh.R == r && sh.S == s && sh.TY == ty && sh.TX == tx && sh.M == m &&          \
+        sh.nwmax == nw && sh.minb == mb)                                               \
+        return launch_shape<r, s, ty, tx, m, nw, mb>(nullptr, 0, nullptr);
     SKC_REGTILE_SHAPES(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -98,9 +98,13 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
 cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
                           int S, int stride, int pad, int Ho, int Wo, cudaStream_t st);
 cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st);
+// set the kernel's opt-in shared-memory attribute on the current device (skc_plan_upload), so
+// that launches need no attribute call (capture-safe from the first launch)
+cudaError_t prepare_direct(int T, int M);
 bool direct_supported(int T, int M);
 cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_t smem,
                            cudaStream_t st);
+cudaError_t prepare_regtile(const RegtileShape &sh);
 // Instantiated register-tile shapes (count returned, shapes written to out[0..max)).
 int regtile_shapes(RegtileShape *out, int max);
 // "Compiled weights" kernel (jit.cpp).  JitInput points into the plan's canonical CSR.
@@ -134,18 +138,36 @@ size_t jit_image_bytes(const JitPlan *jp);
 void jit_image(const JitPlan *jp, void *dst);
 void jit_info(const JitPlan *jp, JitInfo *o);
 const std::vector<int32_t> &jit_chan(const JitPlan *jp);
-cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_lanemap, int N,
+// device preparation at skc_plan_upload (compile if needed, load the cubin, attributes,
+// occupancy); jit_ready: prepared on `dev`; jit_set_vid: the workspace holds the SM order
+int jit_prepare(JitPlan *jp, int dev, std::string *msg);
+bool jit_ready(const JitPlan *jp, int dev);
+void jit_set_vid(JitPlan *jp, bool ok);
+// workspace regions (byte offsets from the workspace base): vid table (jit_vid_cap() u16)
+// followed by the claim table (jit_vid_cap() u32); probe scratch (jit_probe_ints() int32)
+size_t jit_vid_offset(const JitPlan *jp);
+size_t jit_probe_offset(const JitPlan *jp);
+size_t jit_probe_ints();
+size_t jit_vid_cap();
+cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_ws, int N,
                        const Epilogue &epi, cudaStream_t st, std::string *msg);
 // Static check: tables + the emitted code decoded back to the canonical CSR (host).
 int jit_verify_code(const JitPlan *jp, std::string *msg);
-// GPC-major SM order (topo.cu): vid[smid], empty when unknown.  Synchronous, once per device.
-int jit_tune(JitPlan *jp, const void *d_lanemap, int N, cudaStream_t st, double *best_ms,
-             std::string *msg);
-const std::vector<uint16_t> &sm_gpc_order(int dev);
-const uint16_t *sm_gpc_order_device(int dev, bool peek);
+// launch-schedule tuning on caller-owned scratch (input in the plan's layout, output, and an
+// optional L2-flush buffer written before every timed launch); synchronous on `st`
+int jit_tune(JitPlan *jp, const void *d_ws, int N, const float *d_in, float *d_out, void *d_flush,
+             size_t flush_bytes, cudaStream_t st, double *best_ms, std::string *msg);
+// GPC-major SM order (topo.cu): vid[smid].  sm_gpc_order runs the probe once per device on
+// `st` with the caller's device scratch (>= scratch_ints int32; synchronous), then returns the
+// cached order; empty when the probe fails.  sm_gpc_order_cached never launches.
+const std::vector<uint16_t> &sm_gpc_order(int dev, int *d_scratch, size_t scratch_ints,
+                                          cudaStream_t st);
+bool sm_gpc_order_cached(int dev, std::vector<uint16_t> *out);
 void jit_destroy(JitPlan *jp);
 
 cudaError_t bench_ffma(void *scratch, int blocks, int iters, float *ms, double *flops);
 cudaError_t bench_lds(void *scratch, int blocks, int iters, float *ms, double *bytes);
+cudaError_t bench_ffma2(void *scratch, int blocks, int iters, float *ms, double *flops);
+cudaError_t bench_lds64(void *scratch, int blocks, int iters, float *ms, double *bytes);
 
 }  // namespace skc

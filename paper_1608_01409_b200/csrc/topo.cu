@@ -30,15 +30,16 @@ int find(std::vector<int> &par, int a) {
 }  // namespace
 
 // vid[smid] = position of the SM in a GPC-major order (GPCs by lowest SM id, SMs ascending
-// within a GPC); empty if the probe fails.  Computed once per device (the caller's device),
-// synchronously on a private stream: call it outside stream capture (plan upload does).
-const std::vector<uint16_t> &sm_gpc_order(int dev) {
+// within a GPC); empty if the probe fails.  Computed once per device, synchronously on the
+// caller's stream `st` with the caller's device scratch (skc_plan_upload passes a region of the
+// plan workspace: libskc allocates no device memory).  Later calls return the cached order.
+const std::vector<uint16_t> &sm_gpc_order(int dev, int *d, size_t scratch_ints, cudaStream_t st) {
     static std::mutex mu;
     static std::vector<std::vector<uint16_t>> cache(64);
     static std::vector<char> done(64, 0);
     std::lock_guard<std::mutex> lk(mu);
     if (dev < 0 || dev >= 64) return cache[0];
-    if (done[size_t(dev)]) return cache[size_t(dev)];
+    if (done[size_t(dev)] || !d) return cache[size_t(dev)];
     done[size_t(dev)] = 1;
     int nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1 ||
@@ -46,13 +47,9 @@ const std::vector<uint16_t> &sm_gpc_order(int dev) {
         return cache[size_t(dev)];
     std::vector<int> par(static_cast<size_t>(nsm));
     std::iota(par.begin(), par.end(), 0);
-    int *d = nullptr;
-    cudaStream_t st = nullptr;
-    bool ok = cudaMalloc(&d, sizeof(int) * 4096) == cudaSuccess &&
-              cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess;
     const int smem = 160 * 1024;  // one CTA per SM
-    ok = ok && cudaFuncSetAttribute(topo_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem) == cudaSuccess;
+    bool ok = cudaFuncSetAttribute(topo_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem) == cudaSuccess;
     cudaFuncSetAttribute(topo_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int linked = 0;
     for (int cs : {16, 8, 4, 2}) {
@@ -74,15 +71,14 @@ const std::vector<uint16_t> &sm_gpc_order(int dev) {
             cudaGetLastError();
             continue;
         }
-        const int n = std::min(ncl * cs, 4096);
+        const int n = int(std::min<size_t>(size_t(ncl) * cs, scratch_ints));
+        if (n < cs) continue;
         lc.gridDim = dim3(unsigned(n / cs * cs));
+        std::vector<int> h(static_cast<size_t>(n));
         if (cudaLaunchKernelEx(&lc, topo_probe_kernel, d, 200000LL) != cudaSuccess ||
+            cudaMemcpyAsync(h.data(), d, sizeof(int) * size_t(n), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess) {
             cudaGetLastError();
-            continue;
-        }
-        std::vector<int> h(static_cast<size_t>(n));
-        if (cudaMemcpy(h.data(), d, sizeof(int) * size_t(n), cudaMemcpyDeviceToHost) != cudaSuccess) {
             ok = false;
             break;
         }
@@ -97,9 +93,6 @@ const std::vector<uint16_t> &sm_gpc_order(int dev) {
                 }
             }
     }
-    if (d) cudaFree(d);
-    if (st) cudaStreamDestroy(st);
-    cudaGetLastError();
     if (!ok || linked == 0) return cache[size_t(dev)];
     // GPC-major order: groups by their lowest SM id (the root, since unions keep the minimum)
     std::vector<uint16_t> vid(static_cast<size_t>(nsm));
@@ -113,32 +106,11 @@ const std::vector<uint16_t> &sm_gpc_order(int dev) {
     return cache[size_t(dev)];
 }
 
-}  // namespace skc
-
-namespace skc {
-// Device copy of sm_gpc_order(dev) (made on the first call for a device, which runs the probe:
-// plan upload calls it); `peek` only returns an existing copy (safe during stream capture).
-const uint16_t *sm_gpc_order_device(int dev, bool peek) {
-    static std::mutex mu;
-    static std::vector<const uint16_t *> ptr(64, nullptr);
-    static std::vector<char> tried(64, 0);
-    if (dev < 0 || dev >= 64) return nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (tried[size_t(dev)] || peek) return ptr[size_t(dev)];
-    }
-    const std::vector<uint16_t> &v = sm_gpc_order(dev);
-    std::lock_guard<std::mutex> lk(mu);
-    if (tried[size_t(dev)]) return ptr[size_t(dev)];
-    tried[size_t(dev)] = 1;
-    if (v.empty()) return nullptr;
-    void *d = nullptr;
-    if (cudaMalloc(&d, v.size() * sizeof(uint16_t)) != cudaSuccess ||
-        cudaMemcpy(d, v.data(), v.size() * sizeof(uint16_t), cudaMemcpyHostToDevice) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    ptr[size_t(dev)] = static_cast<const uint16_t *>(d);
-    return ptr[size_t(dev)];
+bool sm_gpc_order_cached(int dev, std::vector<uint16_t> *out) {
+    const std::vector<uint16_t> &v = sm_gpc_order(dev, nullptr, 0, nullptr);
+    if (v.empty()) return false;
+    *out = v;
+    return true;
 }
+
 }  // namespace skc

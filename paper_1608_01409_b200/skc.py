@@ -30,7 +30,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
            "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc",
            "skc_plan_compile", "skc_sparse_conv_forward_into", "skc_plan_tune",
-           "skc_sm_topology")
+           "skc_sm_topology", "skc_bench_ffma2", "skc_bench_lds64")
 
 
 class SkcError(RuntimeError):
@@ -97,7 +97,7 @@ def lib():
             "skc_plan_info": [_P, ctypes.POINTER(skc_info)],
             "skc_plan_verify": [_P],
             "skc_plan_compile": [_P],
-            "skc_plan_tune": [_P, _I, _P, ctypes.POINTER(ctypes.c_double)],
+            "skc_plan_tune": [_P, _I, _P, _P, _P, ctypes.c_size_t, _P, ctypes.POINTER(ctypes.c_double)],
             "skc_sm_topology": [ctypes.POINTER(_I), _I, ctypes.POINTER(_I)],
             "skc_plan_csr": [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
             "skc_plan_perm": [_P, ctypes.POINTER(_P)],
@@ -118,6 +118,10 @@ def lib():
                                ctypes.POINTER(ctypes.c_double)],
             "skc_bench_lds": [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
                               ctypes.POINTER(ctypes.c_double)],
+            "skc_bench_ffma2": [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double)],
+            "skc_bench_lds64": [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -238,11 +242,16 @@ def skc_sm_topology(cap: int = 1024):
     return list(arr[:n.value])
 
 
-def skc_plan_tune(plan: Plan, N: int, stream=None) -> float:
-    """JIT kernel: time the launch-schedule variants on N scratch images, keep the fastest;
-    returns its time in ms (0.0 for other kernels).  Outputs are bitwise unaffected."""
+def skc_plan_tune(plan: Plan, N: int, d_in, d_out, d_flush=None, stream=None) -> float:
+    """JIT kernel: time the launch-schedule variants on caller-owned scratch of N images
+    (d_in: padded input in the plan's layout, d_out: output, d_flush: optional buffer larger
+    than L2 written before every timed launch), keep the fastest; returns its time in ms
+    (0.0 for other kernels).  Outputs are bitwise unaffected."""
     ms = ctypes.c_double(0.0)
-    _check(lib().skc_plan_tune(plan.handle, int(N), _stream(stream), ctypes.byref(ms)))
+    fl = _dptr(d_flush) if d_flush is not None else None
+    nfl = d_flush.numel() * d_flush.element_size() if d_flush is not None else 0
+    _check(lib().skc_plan_tune(plan.handle, int(N), _dptr(d_in), _dptr(d_out), fl, nfl,
+                               _stream(stream), ctypes.byref(ms)))
     return ms.value
 
 
@@ -396,6 +405,18 @@ def skc_bench_lds(scratch, blocks: int, iters: int):
     return ms.value, by.value
 
 
+def skc_bench_ffma2(scratch, blocks: int, iters: int):
+    ms, fl = ctypes.c_double(), ctypes.c_double()
+    _check(lib().skc_bench_ffma2(_dptr(scratch), blocks, iters, ctypes.byref(ms), ctypes.byref(fl)))
+    return ms.value, fl.value
+
+
+def skc_bench_lds64(scratch, blocks: int, iters: int):
+    ms, by = ctypes.c_double(), ctypes.c_double()
+    _check(lib().skc_bench_lds64(_dptr(scratch), blocks, iters, ctypes.byref(ms), ctypes.byref(by)))
+    return ms.value, by.value
+
+
 # ------------------------------------------------------------------ convenience layer
 @dataclass
 class SparseConv2d:
@@ -426,10 +447,18 @@ class SparseConv2d:
         """Padded-input buffer shape in the plan's layout (NCHW, or image pairs)."""
         return padded_shape(self.geom, N)
 
-    def tune(self, N: int = 256, stream=None) -> float:
+    def tune(self, N: int = 256, stream=None, flush=True) -> float:
         """JIT plans: pick the fastest launch schedule for batches of N on this device
-        (skc_plan_tune); returns the chosen variant's time in ms."""
-        return skc_plan_tune(self.plan, N, stream)
+        (skc_plan_tune, on scratch buffers allocated here as torch tensors); returns the
+        chosen variant's time in ms (0.0 for other kernels)."""
+        import torch
+        if self.geom["kernel"] != SKC_KERNEL_JIT:
+            return 0.0
+        dev = self.plan.workspace.device
+        xp = torch.zeros(self.padded_shape(N), dtype=torch.float32, device=dev)
+        out = torch.empty(self.out_shape(N), dtype=torch.float32, device=dev)
+        fl = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+        return skc_plan_tune(self.plan, N, xp, out, fl, stream)
 
     def forward_padded(self, xp, out=None, stream=None, N=None):
         """Conv of a padded input in the plan's layout.  N defaults to out's batch, else to

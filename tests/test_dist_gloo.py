@@ -64,7 +64,29 @@ def _worker(rank, world, port, q):
         lo, hi = skd.shard_range(9, world, rank)
         local = torch.arange(lo * 4, hi * 4, dtype=torch.float32).reshape(hi - lo, 2, 2)
         full = skd.gather_images(local, 9)
-        q.put((rank, same, differ, t, full.numpy().tolist()))
+        # bench.py's check of a sharded run, on real conv outputs: each rank's shard of a
+        # 10-image batch (computed here by the oracle, cast to fp32, as a stand-in for the
+        # GPU's), gathered over the process group, must equal one "device's" whole batch bit
+        # for bit and pass the oracle on >= 3 images per shard; a corrupted element must fail
+        import bench
+        import oracle
+        n_total = 10
+        lo2, hi2 = skd.shard_range(n_total, world, rank)
+        mine = oracle.conv2d_fp64(wl.gen_input(2, 3, L, lo2, hi2), w, L.stride, L.pad, L.groups,
+                                  want_bound=False)[0].astype(np.float32)
+        bad = mine.copy()
+        if rank == 1:
+            bad[0, 5, 3, 3] = np.nextafter(bad[0, 5, 3, 3], np.float32(np.inf))
+        g_ok = skd.gather_images(torch.from_numpy(mine), n_total).numpy()
+        g_bad = skd.gather_images(torch.from_numpy(bad), n_total).numpy()
+        ver = None
+        if rank == 0:
+            whole = oracle.conv2d_fp64(wl.gen_input(2, 3, L, 0, n_total), w, L.stride, L.pad,
+                                       L.groups, want_bound=False)[0].astype(np.float32)
+            ok = bench.verify_gathered(g_ok, whole, 2, 3, L, w, n_total, world, per_shard=3)
+            nok = bench.verify_gathered(g_bad, whole, 2, 3, L, w, n_total, world, per_shard=3)
+            ver = (ok["bitwise_vs_1gpu"], ok["images"], ok["max_err_over_bound"], nok["bitwise_vs_1gpu"])
+        q.put((rank, same, differ, t, full.numpy().tolist(), ver))
     finally:
         dist.destroy_process_group()
 
@@ -80,7 +102,11 @@ def test_gloo_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, same, differ, t, full in res:
+    for rank, same, differ, t, full, ver in res:
         assert same and differ
         assert t == 2.5
         np.testing.assert_array_equal(np.array(full), np.arange(36, dtype=np.float32).reshape(9, 2, 2))
+        if rank == 0:
+            bitwise_ok, images, err, bitwise_bad = ver
+            assert bitwise_ok and images >= 6 and err <= 1e-4, ver
+            assert bitwise_bad is False

@@ -246,38 +246,55 @@ def sample_images(N, rng, k):
     return sorted(idx)
 
 
-@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
 @pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
-def test_config_parity(cfg_id, kernel):
-    """Every BASELINE config layer at its full batch on the GPU, in the launch configuration
-    bench.py times; the oracle checks a seeded sample of images (always first and last)."""
+def test_config_parity_full_batch(cfg_id):
+    """Every BASELINE config layer (configs 1-4, all 8 config-3 sparsity points) at its FULL
+    batch, EVERY image checked against the fp64 oracle (full-batch
+    oracle where host time allows -- about a minute of the box's cores), for the AUTO plan
+    in the launch configuration bench.py times (tuned for the batch) and for the direct
+    kernel; the oracle runs once per layer and serves both."""
     cfg = wl.CONFIGS[cfg_id]
-    rng = np.random.default_rng(100 + cfg_id)
     for li, layer in enumerate(cfg.layers):
         w = wl.gen_weights(cfg_id, li, layer)
         x = wl.gen_input(cfg_id, li, layer, 0, cfg.batch)
-        out, conv = run_gpu(w, x, layer, kernel)
-        k = 4 if cfg_id != 3 else 2
-        for n in sample_images(cfg.batch, rng, k):
-            ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
-            check(out[n:n + 1], ref, bound, f"cfg{cfg_id} {layer.name} image {n}")
-        assert np.isfinite(out).all()
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        for kernel in (skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT):
+            conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                               layer.groups, kernel)
+            skc.skc_plan_verify(conv.plan)
+            if kernel == skc.SKC_KERNEL_AUTO:
+                conv.tune(cfg.batch)
+            out = conv.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+            check(out, ref, bound, f"cfg{cfg_id} {layer.name} kernel {conv.geom['kernel']}")
+            del out, conv
+        del ref, bound
 
 
-def test_config5_batch4096_sampled():
-    """BASELINE.json configs[4]: config 2's layers at batch 4096 (one GPU's worth of the
-    sharded job at P = 1), in the launch configuration bench.py uses; the oracle checks a
-    seeded sample of images of every layer (first, last, and two inside)."""
+def test_config5_sharded_parity():
+    """BASELINE.json configs[4]: config 2's layers at batch 4096, sharded over 8 GPUs.  On
+    one GPU: the whole batch, and each of the 8 shards run separately (as the 8 ranks would,
+    dist.shard_range) and concatenated -- the concatenation must equal the whole-batch run
+    BIT FOR BIT, and 8 images of every shard (its first and last included: 64 per layer) must
+    pass the oracle.  Uses bench.py's verify_gathered, the same check bench.py runs on the
+    NCCL-gathered outputs of a multi-GPU run (and tests/test_dist_gloo.py on gloo)."""
+    import bench
+    from paper_1608_01409_b200 import dist as skd
     cfg = wl.CONFIGS[5]
-    rng = np.random.default_rng(105)
+    world = 8
     for li, layer in enumerate(cfg.layers):
         w = wl.gen_weights(5, li, layer)
-        x = wl.gen_input(5, li, layer, 0, cfg.batch)
-        out, conv = run_gpu(w, x, layer)
-        for n in sample_images(cfg.batch, rng, 4):
-            ref, bound = oracle.conv2d_fp64(x[n:n + 1], w, layer.stride, layer.pad, layer.groups)
-            check(out[n:n + 1], ref, bound, f"cfg5 {layer.name} image {n}")
-        del out, x
+        x = torch.from_numpy(wl.gen_input(5, li, layer, 0, cfg.batch)).cuda()
+        conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups)
+        shard = skd.shard_range(cfg.batch, world, 0)[1]
+        conv.tune(shard)
+        full = conv.forward(x).cpu().numpy()
+        parts = [conv.forward(x[lo:hi]).cpu().numpy()
+                 for lo, hi in (skd.shard_range(cfg.batch, world, r) for r in range(world))]
+        res = bench.verify_gathered(np.concatenate(parts), full, 5, li, layer, w, cfg.batch, world)
+        assert res["bitwise_vs_1gpu"], f"{layer.name}: sharded run differs from the whole batch"
+        assert res["images"] >= 8 * world
+        assert res["max_err_over_bound"] <= TOL, res
+        del x, full, parts
 
 
 def check_epi(out, ref, bound, bias, relu, what=""):
@@ -661,14 +678,18 @@ def test_plan_tune_keeps_outputs_bitwise():
                                          layer.groups, skc.SKC_KERNEL_DIRECT)
     assert direct.tune(37) == 0.0
     with pytest.raises(skc.SkcError):
-        skc.skc_plan_tune(jit.plan, 0)
+        skc.skc_plan_tune(jit.plan, 0, xp, xp)
 
 
 @pytest.mark.gpu
 def test_sm_topology_is_a_gpc_major_permutation():
-    """The topology probe (clusters never span a GPC) yields a permutation of the SM ids in
-    which every cluster-mate group is contiguous: the two SMs of a 2-CTA cluster (one TPC)
-    always get neighbouring positions."""
+    """The topology probe (clusters never span a GPC; run by the first JIT upload on the
+    device, in the plan workspace) yields a permutation of the SM ids in which every
+    cluster-mate group is contiguous: the two SMs of a 2-CTA cluster (one TPC) always get
+    neighbouring positions."""
+    layer = wl.Layer("t0", 16, 16, 13, 13, 3, 3, 1, 1, 1, 0.5, 0.01)
+    w, _ = wl.random_tensors(np.random.default_rng(49), layer, 1)
+    skc.SparseConv2d.from_dense(w, 13, 13, 1, 1, 1, skc.SKC_KERNEL_JIT)  # uploads: probes
     vid = skc.skc_sm_topology()
     n = torch.cuda.get_device_properties(0).multi_processor_count
     assert len(vid) == n
@@ -724,3 +745,99 @@ def test_tune_small_layers_and_batches(N):
         y1 = jit.forward(xd).cpu().numpy()
         np.testing.assert_array_equal(y0.view(np.uint32), yd.view(np.uint32), err_msg=layer.name)
         np.testing.assert_array_equal(y1.view(np.uint32), yd.view(np.uint32), err_msg=layer.name)
+
+
+# every launch schedule skc_plan_tune can choose: bit 0 first round block-major, bit 1
+# GPC-major (claimed) first items, bit 2 no dry-run prefetch, bit 3 contiguous lane table,
+# bits 4-7 cluster size (1 or 2), bit 9 dry run by every CTA
+SCHEDULES = [o3 | (v << 1) | (nd << 2) | (ln << 3) | (cs << 4) | (da << 9)
+             for o3 in (0, 1) for v in (0, 1) for nd in (0, 1) for ln in (0, 1) for cs in (1, 2)
+             for da in (0, 1)]
+
+
+def test_jit_every_schedule_bitwise(monkeypatch):
+    """The schedules the bench actually runs: every launch-schedule word the tuner can pick
+    (forced with SKC_JIT_SCHED) on all four config-2 layers at the full batch of 256, in the
+    plans AUTO builds -- each BIT FOR BIT equal to the direct kernel (whose output the oracle
+    checks in test_config_parity_full_batch)."""
+    cfg = wl.CONFIGS[2]
+    for li, L in enumerate(cfg.layers):
+        w = wl.gen_weights(2, li, L)
+        x = torch.from_numpy(wl.gen_input(2, li, L, 0, cfg.batch)).cuda()
+        direct = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_DIRECT)
+        yd = direct.forward(x)
+        jit = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_AUTO)
+        assert jit.geom["kernel"] == skc.SKC_KERNEL_JIT
+        xp = torch.empty(jit.padded_shape(cfg.batch), device="cuda")
+        skc.skc_pad_input(jit.plan, x, xp, cfg.batch)
+        yj = torch.empty_like(yd)
+        for sched in SCHEDULES:
+            monkeypatch.setenv("SKC_JIT_SCHED", str(sched))
+            yj.fill_(float("nan"))
+            jit.forward_padded(xp, yj)
+            torch.cuda.synchronize()
+            assert torch.equal(yj.view(torch.int32), yd.view(torch.int32)), f"{L.name} sched {sched}"
+        monkeypatch.delenv("SKC_JIT_SCHED")
+        del x, yd, yj, xp
+
+
+def test_gpc_major_items_claimed_when_sms_are_shared(monkeypatch):
+    """GPC-major first items are CLAIMED (atomic compare-and-swap on a table in the
+    workspace), not assumed from %smid: the launch is not cooperative, so when other kernels
+    hold some SMs, CTAs of the persistent grid start late on SMs that earlier CTAs of the same
+    grid already used.  Hold ~24 SMs with spinning kernels on side streams, launch the JIT
+    kernel (GPC-major items forced, no clusters) meanwhile, repeatedly: every output must stay
+    bitwise equal to the direct kernel (a duplicated first item would leave outputs unwritten)."""
+    monkeypatch.setenv("SKC_JIT_SCHED", str((1 << 1) | (1 << 4)))
+    L = wl.CONFIGS[2].layers[3]
+    N = 256  # >= one item per SM: the grid is all SMs, the condition for GPC-major items
+    w = wl.gen_weights(2, 3, L)
+    x = torch.from_numpy(wl.gen_input(2, 3, L, 0, N)).cuda()
+    direct = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_DIRECT)
+    yd = direct.forward(x)
+    jit = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_JIT)
+    xp = torch.empty(jit.padded_shape(N), device="cuda")
+    skc.skc_pad_input(jit.plan, x, xp, N)
+    torch.cuda.synchronize()
+    side = [torch.cuda.Stream() for _ in range(24)]
+    main = torch.cuda.Stream()
+    for rep in range(6):
+        for s_ in side:
+            with torch.cuda.stream(s_):
+                torch.cuda._sleep(2_000_000 * (1 + rep % 3))  # ~1-3 ms per held SM
+        yj = torch.full_like(yd, float("nan"))
+        with torch.cuda.stream(main):
+            jit.forward_padded(xp, yj, stream=main)
+        torch.cuda.synchronize()
+        assert torch.equal(yj.view(torch.int32), yd.view(torch.int32)), f"rep {rep}"
+
+
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_first_forward_captured_in_graph(kernel):
+    """skc_plan_upload prepares everything a launch needs (JIT code loaded, attributes,
+    occupancy, SM order), so the VERY FIRST pad + forward of a fresh plan can be captured
+    into a CUDA graph; replays match an ordinary launch of a second plan bit for bit."""
+    L = wl.CONFIGS[2].layers[2]
+    N = 12
+    w = wl.gen_weights(2, 2, L)
+    x = torch.from_numpy(wl.gen_input(2, 2, L, 0, N)).cuda()
+    ref_conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kernel)
+    ref = ref_conv.forward(x)
+    conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kernel)
+    xp = torch.empty(conv.padded_shape(N), device="cuda")
+    out = torch.full_like(ref, float("nan"))
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            skc.skc_pad_input(conv.plan, x, xp, N, s)
+            skc.skc_sparse_conv_forward(conv.plan, xp, out, N, s)
+    torch.cuda.synchronize()
+    assert torch.isnan(out).all(), "capture must not execute"
+    for _ in range(3):
+        out.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
