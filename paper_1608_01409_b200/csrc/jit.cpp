@@ -159,6 +159,7 @@ struct JitPlan {
     int order = 2;
     int dry = 1;               // 1: instruction prefetch by dry-running code segments at start
     int pmajor = 1;            // 1: position-major FMA order within a channel (pair layout)
+    int lookahead = 0;         // position-major: window loads issued this many positions ahead
     // 1: an item's last chunks stage the next item's first chunks (rotated stages, barriers
     // live across items).  Measured -1..-2% on conv3/4 (profiles/r01_jit_xpf.txt): the item
     // start was not waiting on its first stage; off by default
@@ -611,7 +612,45 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         o("@!%%p4 bra $W%d;", i);
         o("$B%d:", i);
         const int cn = chunk_channels(jp, i);
-        for (int cl = 0; cl < cn; ++cl) {
+        bool cn_done = false;
+        if (pm && jp.pmajor && jp.lookahead > 0 && jp.sync_every == 0) {
+            // position-major with software-pipelined window loads: the chunk's (channel,
+            // position) sequence is flattened and position j + D is loaded before the FMAs of
+            // position j, into a rotating pool of D + 1 window registers (each warp keeps D + 1
+            // loads in flight).  Per accumulator the FMA order is unchanged (bitwise equal).
+            struct Pos { int c, u; };
+            std::vector<Pos> seq;
+            for (int cl = 0; cl < cn; ++cl) {
+                const int c = i * jp.CB + cl;
+                const auto &nz = per_c[size_t(c)];
+                if (nz.empty()) continue;
+                window_need(nz, TY, TX, PX, st, WRw, WCw, pm, nd);
+                for (int u : nd.pairs) seq.push_back(Pos{cl, u});
+            }
+            const int D = std::min(jp.lookahead, NWIN - 1);
+            auto off_of = [&](const Pos &p) {
+                return (p.c * jp.plane + (p.u / WCw) * in.Wp + (p.u % WCw)) * 4 * sw;
+            };
+            for (int j = 0; j < std::min(D, int(seq.size())); ++j)
+                o("ld.volatile.shared.b64 %%wp%d, [%%rb%d+%d];", j % (D + 1), s, off_of(seq[size_t(j)]));
+            for (int j = 0; j < int(seq.size()); ++j) {
+                if (j + D < int(seq.size()))
+                    o("ld.volatile.shared.b64 %%wp%d, [%%rb%d+%d];", (j + D) % (D + 1), s,
+                      off_of(seq[size_t(j + D)]));
+                const Pos &p = seq[size_t(j)];
+                for (const JNz &z : per_c[size_t(i * jp.CB + p.c)])
+                    for (int ty = 0; ty < TY; ++ty)
+                        for (int tx = 0; tx < TX; ++tx) {
+                            if ((ty * st + z.r) * WCw + tx * st + z.s != p.u) continue;
+                            const uint32_t wb = fbits(z.w);
+                            const int a = z.m * NPT + ty * TX + tx;
+                            o("mov.b64 %%wt, 0x%08X%08X;", wb, wb);
+                            o("fma.rn.f32x2 %%a%d, %%wt, %%wp%d, %%a%d;", a, j % (D + 1), a);
+                        }
+            }
+            cn_done = true;
+        }
+        for (int cl = 0; cl < cn && !cn_done; ++cl) {
             const int c = i * jp.CB + cl;
             const auto &nz = per_c[size_t(c)];
             if (nz.empty()) continue;
@@ -2063,6 +2102,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_ORDER")) jp.order = std::atoi(e);
     if (const char *e = std::getenv("SKC_JIT_DRY")) jp.dry = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_PMAJOR")) jp.pmajor = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_LOOKAHEAD")) jp.lookahead = std::max(0, std::min(8, std::atoi(e)));
     if (const char *e = std::getenv("SKC_JIT_XPF")) jp.xpf = std::atoi(e) ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_DYN")) jp.dyn = std::max(0, std::min(2, std::atoi(e)));
     // whole-program compile (one serial ptxas run, ~10-20 s per 100k instructions) when the
