@@ -18,13 +18,16 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include"),
-          "-I", CSRC]
+          "-I", CSRC, "-I", BUILD]
 SOURCES = ["plan.cpp", "jit.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu", "topo.cu"]
 # the JIT kernel compiles and links its generated code in-process (no ptxas on PATH needed)
 CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+# static PTX compiler + nvJitLink (a shared libnvJitLink clashes with the older copy torch
+# loads into the same process: versioned symbols); ~135 MB of the .so
 JIT_LIBS = [os.path.join(CUDA_LIB, "libnvJitLink_static.a"),
             os.path.join(CUDA_LIB, "libnvptxcompiler_static.a"), "-lpthread", "-ldl", "-lrt"]
-HEADERS = ["skc_internal.h", "ptx.cuh", "regtile_gen.inc"]
+HEADERS = ["skc_internal.h", "ptx.cuh"]
+GENERATED = os.path.join(BUILD, "regtile_gen.inc")  # gen_regtile.py output (not committed)
 
 
 def _newer(target: str, deps) -> bool:
@@ -37,7 +40,7 @@ def _newer(target: str, deps) -> bool:
 def _compile(src: str, force: bool) -> str:
     path = os.path.join(CSRC, src)
     obj = os.path.join(BUILD, src + ".o")
-    deps = [path, os.path.join(ROOT, "include", "skc.h")] + [os.path.join(CSRC, h) for h in HEADERS]
+    deps = [path, os.path.join(ROOT, "include", "skc.h"), GENERATED] + [os.path.join(CSRC, h) for h in HEADERS]
     if force or _newer(obj, deps):
         cmd = [NVCC] + ARCH + COMMON + ["-c", path, "-o", obj]
         if src.endswith(".cu"):
@@ -54,6 +57,8 @@ def _compile(src: str, force: bool) -> str:
 
 def build(force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    from paper_1608_01409_b200 import gen_regtile
+    gen_regtile.generate(GENERATED)
     with cf.ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
     if force or _newer(LIB, objs):

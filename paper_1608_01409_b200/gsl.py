@@ -69,20 +69,31 @@ class GslConfig:
 
 
 class GslController:
-    def __init__(self, layers: dict, platform: Platform, config: GslConfig = GslConfig()):
-        """layers: name -> geometry dict (K, C, R, S, H, W, stride, pad, groups)."""
+    def __init__(self, layers: dict, platform: Platform, config: GslConfig = GslConfig(),
+                 layer_platforms: dict = None):
+        """layers: name -> geometry dict (K, C, R, S, H, W, stride, pad, groups).
+        layer_platforms: optional name -> Platform measured for that layer (its own F and
+        alpha: on B200 the dense rate and the sparse kernel's efficiency differ per layer
+        shape); layers without one use `platform`."""
         if not layers:
             raise ValueError("GSL needs at least one layer")
         self.platform, self.config = platform, config
+        self.layer_platforms = dict(layer_platforms or {})
+        unknown = set(self.layer_platforms) - set(layers)
+        if unknown:
+            raise KeyError(f"platforms for unknown layers {sorted(unknown)}")
         self.layers = {}
-        p = platform
         for name, g in layers.items():
+            p = self.platform_of(name)
             cost = skc.skc_model_layer_cost(g["K"], g["C"], g["R"], g["S"], g["H"], g["W"],
                                             g.get("stride", 1), g.get("pad", 0),
                                             g.get("groups", 1), batch=1)
             win = skc.skc_model_window(cost, p.F, p.B, p.alpha, p.beta)
             ok = win["has_speedup_potential"] and name not in config.exclude
             self.layers[name] = LayerState(name, dict(g), cost, win, ACTIVE if ok else EXCLUDED)
+
+    def platform_of(self, name: str) -> Platform:
+        return self.layer_platforms.get(name, self.platform)
 
     def step(self, iteration: int, densities: dict) -> dict:
         """One periodic check; densities: name -> current density x of ACTIVE layers.
@@ -115,9 +126,9 @@ class GslController:
     def report(self) -> dict:
         """Per-layer status, final density, window and projected speedup; whole-net speedup =
         sum of dense times / sum of projected times (dense layers at dense time)."""
-        p = self.platform
         rows, t_dense, t_net = [], 0.0, 0.0
         for name, L in self.layers.items():
+            p = self.platform_of(name)
             x = self.final_density(name)
             pr = skc.skc_model_project(L.cost, x, p.F, p.B, p.alpha, p.beta)
             sparse = L.status in (ACTIVE, STOPPED_SATURATED)
@@ -125,9 +136,9 @@ class GslController:
             t_dense += pr["t_dense"]
             t_net += t
             rows.append(dict(layer=name, status=L.status, final_density=x,
-                             x_lo=L.window["x_lo"], x_hi=L.window["x_hi"],
+                             x_lo=L.window["x_lo"], x_hi=L.window["x_hi"], alpha=p.alpha,
                              projected_speedup=pr["t_dense"] / t))
-        return dict(platform=p.name, alpha=p.alpha, layers=rows,
+        return dict(platform=self.platform.name, alpha=self.platform.alpha, layers=rows,
                     net_speedup=t_dense / t_net if t_net else 1.0)
 
 

@@ -841,3 +841,33 @@ def test_first_forward_captured_in_graph(kernel):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+
+
+def test_bench_multirank_config5_gloo():
+    """bench.py's multi-rank path run for real: 2 ranks (torchrun, gloo collectives) sharing
+    this GPU on config 5 (BASELINE.json configs[4]) at a global batch of 96 -- strong scaling
+    over shard_range, timed steps, then every layer's outputs gathered from both ranks,
+    compared BIT FOR BIT with rank 0's one-device run of the whole batch, and 8 images per
+    shard (first and last included) through the oracle.  The ranks' kernels never wait on
+    each other (no collective on the data path), so sharing one GPU is only slower."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
+           "--config", "5", "--batch", "96", "--steps", "3", "--warmup", "3", "--backend", "gloo",
+           "--no-e2e", "--no-dense", "--no-cpu", "--no-peaks"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["global_batch"] == 96 and line["config"]["per_gpu_batch"] == 48
+    par = line["parity"]
+    assert par["bitwise_vs_1gpu"] is True and par["pass"] is True, par
+    assert all(p["images"] >= 16 for p in par["per_layer"]), par

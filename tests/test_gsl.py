@@ -119,3 +119,20 @@ def test_b200_profile_alpha():
     assert p.alpha == pytest.approx(62.0 / 14.9)
     c = gsl.GslController(ALEX, p)
     assert c.layers["conv3"].window["x_hi"] == pytest.approx(14.9 / 62.0)
+
+
+def test_per_layer_platforms():
+    """B200 windows are per layer (each layer's own measured F and alpha,
+    tools/layer_windows.py): a layer with its own platform gets its own window and projected
+    speedup; the others keep the default platform; unknown names are rejected."""
+    own = gsl.Platform("B200-conv3", 60e12, 6.5e12, 1.8)
+    c = gsl.GslController(ALEX, gsl.BDW, layer_platforms={"conv3": own})
+    assert c.layers["conv3"].window["x_hi"] == pytest.approx(1 / 1.8)
+    assert c.layers["conv4"].window["x_hi"] == pytest.approx(1 / gsl.BDW.alpha)
+    rep = gsl.replay(c, [(it, n, 0.2) for it in range(4) for n in ALEX])
+    row = {r["layer"]: r for r in rep["layers"]}
+    pr = skc.skc_model_project(c.layers["conv3"].cost, 0.2, own.F, own.B, own.alpha)
+    assert row["conv3"]["projected_speedup"] == pytest.approx(pr["speedup"])
+    assert row["conv3"]["alpha"] == pytest.approx(1.8)
+    with pytest.raises(KeyError):
+        gsl.GslController(ALEX, gsl.BDW, layer_platforms={"nope": own})

@@ -1,9 +1,15 @@
 #!/usr/bin/env python
-"""Row f4: replay synthetic pruning trajectories through the GSL controller with the B200
-profile MEASURED in round 1 (profiles/r01_sparsity_sweep_cfg3.jsonl: F = FP32 SGEMM rate,
-alpha = F / actual sparse rate at x >= 0.4, B = measured HBM copy bandwidth) next to the
-paper's Xeon profile.  Trajectories: each layer's density decays geometrically from 1 to a
-per-layer floor (the layer's 'achievable' density, e.g. conv1 stalls at 0.7)."""
+"""Row f4: replay synthetic pruning trajectories through the GSL controller with B200 profiles
+MEASURED on the shipped (JIT) kernel, next to the paper's Xeon profile:
+  * per layer where measured (profiles/r02_layer_windows.jsonl, tools/layer_windows.py):
+    F = the layer's FP32 SGEMM-proxy rate, alpha = F / the layer's sparse rate at x = 0.5;
+  * the other layers: the config-3 sweep of the final kernel
+    (profiles/r01_sparsity_sweep_cfg3_final.jsonl: alpha = 1.20);
+  B = the measured HBM copy bandwidth.  Trajectories: each layer's density decays
+geometrically from 1 to a per-layer floor (the layer's 'achievable' density, e.g. conv1
+stalls at 0.7).
+
+    python tools/gsl_replay.py > profiles/r02_gsl_replay.json"""
 import json
 import os
 import sys
@@ -27,18 +33,39 @@ FLOOR = {"conv1": 0.7, "conv2": 0.15, "conv3": 0.07, "conv4": 0.09, "conv5": 0.1
 
 
 def b200_from_profiles():
-    path = os.path.join(ROOT, "profiles", "r01_sparsity_sweep_cfg3.jsonl")
+    path = os.path.join(ROOT, "profiles", "r01_sparsity_sweep_cfg3_final.jsonl")
     summ = json.loads(open(path).read().strip().splitlines()[-1])["summary"]
     return gsl.b200_platform(summ["F_sgemm_tflops"] * 1e12, summ["B_gbs"] * 1e9,
                              summ["actual_sparse_tflops_x_ge_0.4"] * 1e12)
 
 
+def b200_per_layer():
+    """name -> Platform from the per-layer windows of the shipped kernel."""
+    path = os.path.join(ROOT, "profiles", "r02_layer_windows.jsonl")
+    out = {}
+    if not os.path.exists(path):
+        return out
+    alias = {"res128_28x28": "res128_3x3"}
+    for line in open(path):
+        d = json.loads(line)
+        name = alias.get(d["layer"], d["layer"])
+        if name in LAYERS:
+            out[name] = gsl.Platform(f"B200 ({d['layer']})", d["F_sgemm_tflops"] * 1e12,
+                                     d["B_gbs"] * 1e9, d["sgemm"]["alpha"])
+    return out
+
+
 def main():
     traj = [(it, n, max(FLOOR[n], 0.85 ** it)) for it in range(60) for n in LAYERS]
     out = {}
-    for plat in (b200_from_profiles(), gsl.BDW):
-        c = gsl.GslController(LAYERS, plat, gsl.GslConfig(window=3, eps=0.01))
+    b200 = b200_from_profiles()
+    per = b200_per_layer()
+    for plat, lp in ((b200, per), (gsl.BDW, None)):
+        c = gsl.GslController(LAYERS, plat, gsl.GslConfig(window=3, eps=0.01), layer_platforms=lp)
         out[plat.name] = gsl.replay(c, traj)
+        if lp:
+            out[plat.name]["per_layer_platforms"] = {n: {"F_tflops": p.F / 1e12, "alpha": p.alpha}
+                                                     for n, p in lp.items()}
     print(json.dumps(out, indent=1))
 
 

@@ -2,7 +2,10 @@
 """Row f4 stress test: AlexNet conv2-5 at batch 256 with per-output-channel densities skewed
 log-normally around the layer's density (workloads.gen_weights_skewed), with and without the
 nnz-sorted channel order the plan uses for load balance (SKC_NO_NNZ_SORT=1), against the
-uniform masks of config 2."""
+uniform masks of config 2.  AUTO plans (the JIT kernel), tuned for the batch as bench.py
+does; L2 flushed before every timed launch.
+
+    python tools/skew_bench.py > profiles/r02_skewed_masks_loadbalance.jsonl"""
 import json
 import os
 import sys
@@ -32,6 +35,7 @@ def main():
                 else:
                     os.environ["SKC_NO_NNZ_SORT"] = "1"
                 conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups)
+                conv.tune(N)
                 xp = torch.empty(conv.padded_shape(N), device="cuda")
                 skc.skc_pad_input(conv.plan, x, xp, N)
                 out = torch.empty(conv.out_shape(N), device="cuda")
@@ -39,6 +43,8 @@ def main():
                 nnz = conv.geom["nnz"]
                 print(json.dumps({"layer": L.name, "mask": mask, "nnz_sorted": sort,
                                   "kernel": conv.geom["kernel"], "nnz": nnz,
+                                  "jit_blocks": conv.geom["jit_blocks"], "jit_split": conv.geom["jit_split"],
+                                  "max_channel_nnz_over_mean": float(nnz_k.max() / nnz_k.mean()),
                                   "nnz_per_channel_cv": float(nnz_k.std() / nnz_k.mean()),
                                   "ms": ms,
                                   "nnz_tflops": 2 * nnz * L.Ho * L.Wo * N / (ms * 1e-3) / 1e12}),
