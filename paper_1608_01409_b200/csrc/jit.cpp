@@ -177,6 +177,10 @@ struct JitPlan {
     int dyn = 1;               // dynamic item scheduling (global counter in the workspace):
                                // 1 per CTA, 2 per cluster; 0: static (t += grid)
     int whole = 0;             // 1: whole-program compile (no ABI saves at block calls)
+    // 1: non-persistent kernel (one work item per CTA, block functions .noreturn and compiled
+    // as separate modules in parallel -- no ABI saves either, seconds to build) plus a
+    // separate dry-run prefetch kernel (skc_jit_dry)
+    int np = 0;
     double code_instr = 0;     // modelled instructions of all blocks' code
     int nbg = 0, nblocks = 0;  // blocks per group (even partition), total blocks
     // block b: conv group, first index into the group's nnz-sorted channels, channel count.
@@ -185,6 +189,7 @@ struct JitPlan {
     std::vector<int> bgrp;
     std::vector<std::vector<int>> bidx;  // positions in the group's nnz-sorted channel list
     int split = 0;             // even blocks (per group) split into halves
+    int deal = 0;              // 1: channels dealt to blocks in snake order (skewed masks)
     double cost = 0;           // modelled warp-instructions per image
     int conflict = 0;          // extra wavefronts per warp-wide window load, summed over warps
     std::vector<int32_t> chan; // [nblocks][M] original output channel or -1
@@ -200,6 +205,7 @@ struct JitPlan {
     int cache_hit = 0;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
+    cudaKernel_t kern_dry = nullptr;  // np mode: the dry-run prefetch kernel
     // device state taken by jit_prepare (skc_plan_upload)
     int prep_dev = -1;
     int nsm = 0, per_sm = 1;
@@ -502,7 +508,9 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     Out o;
     o.s.reserve(1 << 20);
     o("%s", kHdr);
-    o(".visible .func skc_b%d%s", b, kBlkParams);
+    // np (non-persistent per-block modules): the function never returns -- it ends the thread
+    // (`exit`), so a separately compiled block saves no callee-saved registers
+    o(".visible .func skc_b%d%s%s", b, kBlkParams, jp.np ? " .noreturn" : "");
     o("{");
     o(".reg .pred %%p<10>;");
     o(".reg .b32 %%r<32>;");
@@ -906,9 +914,9 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         }
     }
     if (fast_epi) o("$EPI_END:");
-    o("ret;");
+    o(jp.np ? "exit;" : "ret;");
     o("$DRYRET:");
-    o("ret;");
+    o(jp.np ? "exit;" : "ret;");
     o("}");
     return std::move(o.s);
 }
@@ -958,16 +966,71 @@ void emit_decode(Out &o, const JitPlan &jp, const char *tr, const char *rb, cons
     }
 }
 
+const char *kEntryParams =
+    ".param .u64 p_in, .param .u64 p_out, .param .u64 p_lm, .param .u64 p_bias, .param .u32 p_N, "
+    ".param .u32 p_relu, .param .u32 p_opad, .param .u32 p_olay, .param .u64 p_vid, "
+    ".param .u32 p_sched, .param .u32 p_G";
+
+// np mode: the instruction prefetch as its own kernel (launched just before the items): CTA j
+// executes chunk segment j mod (blocks x chunks) of the blocks' code once, with no waits and no
+// stores, so the layer's cold code is pulled into L2 by many fetch streams at once (the
+// persistent kernel does this before its first item, see emit_entry)
+void emit_dry_entry(Out &o, const JitPlan &jp) {
+    o(".visible .entry skc_jit_dry(%s)", kEntryParams);
+    o("{");
+    o(".reg .pred %%p<4>;");
+    o(".reg .b32 %%r<16>;");
+    o(".reg .b64 %%rd<8>;");
+    o("ld.param.u64 %%rd2, [p_lm];");
+    o("cvta.to.global.u64 %%rd2, %%rd2;");
+    o("mov.u32 %%r3, %%tid.x;");
+    o("mul.wide.u32 %%rd4, %%r3, 16;");
+    o("add.u64 %%rd4, %%rd2, %%rd4;");
+    o("ld.global.nc.u32 %%r10, [%%rd4];");        // a valid lane base (band 0)
+    o("mov.u32 %%r11, skc_smem;");
+    o("mov.u32 %%r4, %%ctaid.x;");
+    o("rem.u32 %%r4, %%r4, %d;", jp.nblocks * jp.nchunks);
+    o("div.u32 %%r5, %%r4, %d;", jp.nchunks);      // block
+    o("rem.u32 %%r6, %%r4, %d;", jp.nchunks);
+    o("add.u32 %%r6, %%r6, 1;");                    // chunk + 1
+    for (int b = 0; b < jp.nblocks; ++b) {
+        o("setp.eq.u32 %%p0, %%r5, %d;", b);
+        o("@%%p0 bra $DC%d;", b);
+    }
+    o("ret;");
+    for (int b = 0; b < jp.nblocks; ++b) {
+        o("$DC%d:", b);
+        o("{");
+        o(".param .b32 t0;\n.param .b32 t1;\n.param .b64 t2;\n.param .b32 t3;\n.param .b32 t4;");
+        o(".param .b64 t5;\n.param .b32 t6;\n.param .b32 t7;\n.param .b64 t8;\n.param .b32 t9;");
+        o(".param .b64 t10;\n.param .b32 t11;\n.param .b32 t12;\n.param .b32 t13;");
+        o(".param .b32 t14;\n.param .b32 t15;");
+        o("st.param.b32 [t0], %%r10;\nst.param.b32 [t1], %%r11;\nst.param.b64 [t2], 0;");
+        o("st.param.b32 [t3], 0;\nst.param.b32 [t4], 0;\nst.param.b64 [t5], 0;");
+        o("st.param.b32 [t6], 0;\nst.param.b32 [t7], 0;\nst.param.b64 [t8], 0;");
+        o("st.param.b32 [t9], 0;\nst.param.b64 [t10], 0;\nst.param.b32 [t11], %%r6;");
+        o("st.param.b32 [t12], 0;\nst.param.b32 [t13], %d;", jp.off_info);
+        o("st.param.b32 [t14], %d;\nst.param.b32 [t15], 0;", jp.off_info);
+        o(".param .b64 t16;\n.param .b32 t17;\n.param .b64 t18;");
+        o("st.param.b64 [t16], 0;\nst.param.b32 [t17], 0;\nst.param.b64 [t18], 0;");
+        o("call.uni skc_b%d, (t0, t1, t2, t3, t4, t5, t6, t7, t8, t9, t10, t11, t12, t13, "
+          "t14, t15, t16, t17, t18);", b);
+        o("}");
+    }
+    o("ret;");
+    o("}");
+}
+
 std::string emit_entry(const JitPlan &jp) {
     const JitInput &in = jp.in;
     const int sw = jp.pair ? 2 : 1;
     Out o;
     o("%s", kHdr);
-    for (int b = 0; b < jp.nblocks; ++b) o(".extern .func skc_b%d%s;", b, kBlkParams);
+    for (int b = 0; b < jp.nblocks; ++b)
+        o(".extern .func skc_b%d%s%s;", b, kBlkParams, jp.np ? " .noreturn" : "");
     o(".extern .shared .align 128 .b8 skc_smem[];");
-    o(".visible .entry skc_jit_kernel(.param .u64 p_in, .param .u64 p_out, .param .u64 p_lm, "
-      ".param .u64 p_bias, .param .u32 p_N, .param .u32 p_relu, .param .u32 p_opad, "
-      ".param .u32 p_olay, .param .u64 p_vid, .param .u32 p_sched)");
+    if (jp.np) emit_dry_entry(o, jp);
+    o(".visible .entry skc_jit_kernel(%s)", kEntryParams);
     o("{");
     o(".reg .pred %%p<10>;");
     o(".reg .b32 %%r<80>;");
@@ -993,7 +1056,13 @@ std::string emit_entry(const JitPlan &jp) {
     o("mov.u32 %%r37, %%clusterid.x;");
     o("mov.u32 %%r38, %%nclusterid.x;");
     o("mad.lo.u32 %%r4, %%r37, %%r36, %%r35;");  // item t
-    o("mul.lo.u32 %%r31, %%r38, %%r36;");        // stride G
+    if (jp.np) {
+        // one work item per CTA (the grid is all items); G = the CTAs resident at once, which
+        // the first-round order and the GPC-major first items refer to
+        o("ld.param.u32 %%r31, [p_G];");
+    } else {
+        o("mul.lo.u32 %%r31, %%r38, %%r36;");    // stride G
+    }
     // GPC-major item numbering (one CTA per SM, grid = all SMs): the first item of the CTA on
     // SM s is vid[s], the SM's position in a GPC-major order (topo.cu), so the CTAs of one GPC
     // take neighbouring items -- the same channel block -- and share the GPC's instruction
@@ -1019,6 +1088,7 @@ std::string emit_entry(const JitPlan &jp) {
     // clears the table ($EXIT).
     o("ld.param.u64 %%rd21, [p_vid];");
     o("setp.eq.u64 %%p0, %%rd21, 0;");
+    if (jp.np) o("setp.ge.or.u32 %%p0, %%r4, %%r31, %%p0;");  // np: only the first G items
     o("@%%p0 bra $VID_DONE;");
     o("cvta.to.global.u64 %%rd21, %%rd21;");
     o("mov.u32 %%r78, skc_smem;");
@@ -1044,6 +1114,25 @@ std::string emit_entry(const JitPlan &jp) {
     o("bra.uni $VID_PROBE;");
     o("$VID_GOT:");
     o("st.shared.u32 [%%r78], %%r79;");
+    if (jp.np) {
+        // np: the G-th CTA to claim clears the table (every claim is made by then; CTAs of
+        // items >= G never touch it)
+        o("add.u64 %%rd22, %%rd2, %d;", jp.NB * jp.NW * 32 * 16 + 4);
+        o("fence.acq_rel.gpu;");
+        o("atom.global.add.u32 %%r77, [%%rd22], 1;");
+        o("sub.u32 %%r76, %%r31, 1;");
+        o("setp.ne.u32 %%p1, %%r77, %%r76;");
+        o("@%%p1 bra $VID_WAIT;");
+        o("mov.u32 %%r76, 0;");
+        o("$VID_CLR:");
+        o("mul.wide.u32 %%rd20, %%r76, 4;");
+        o("add.u64 %%rd20, %%rd23, %%rd20;");
+        o("st.global.u32 [%%rd20], 0;");
+        o("add.u32 %%r76, %%r76, 1;");
+        o("setp.lt.u32 %%p1, %%r76, %%r31;");
+        o("@%%p1 bra $VID_CLR;");
+        o("st.global.u32 [%%rd22], 0;");
+    }
     o("$VID_WAIT:");
     o("bar.sync 0;");
     o("ld.shared.u32 %%r4, [%%r78];");
@@ -1070,7 +1159,7 @@ std::string emit_entry(const JitPlan &jp) {
     // PDL: the next grid may be scheduled as our CTAs retire; the dry run below needs no data,
     // so it overlaps the previous grid's tail; wait for the previous grid before the first item
     o("griddepcontrol.launch_dependents;");
-    if (jp.dry) {
+    if (jp.dry && !jp.np) {  // (np: the dry run is its own kernel, skc_jit_dry)
         // Instruction prefetch: the code of a layer is cold in DRAM at launch and fetching it
         // is latency-bound per code stream.  Before the first item every CTA dry-runs a few
         // (block, chunk) code segments -- pairs ctaid, ctaid + G, ... of nblocks x nchunks --
@@ -1450,6 +1539,13 @@ std::string emit_entry(const JitPlan &jp) {
         o("bra.uni $NEXT;");
     }
     o("$NEXT:");
+    if (jp.np) {
+        // one item per CTA; the block function ends the thread (unreachable)
+        o("$EXIT:");
+        o("ret;");
+        o("}");
+        return std::move(o.s);
+    }
     if (!jp.dyn) o("add.u32 %%r4, %%r4, %%r31;");
     if (jp.xpf) o("add.u32 %%r64, %%r64, 1;");
     o("bra.uni $ITEM;");
@@ -1807,12 +1903,20 @@ void choose_blocks(JitPlan &jp, int n_hint) {
         block_nz(in, ks, per_c);
         return block_instr(in, per_c, jp.TY, jp.TX, jp.PX, jp.pair, jp.CB, int(idx.size()), nd);
     };
-    // channels of even block q (of nbg): contiguous ranges of the nnz-sorted list (default),
-    // or dealt in snake order (SKC_JIT_DEAL=1: every block gets heavy and light channels
-    // alike, equal item times).  Measured neutral on the step (conv2 +0.8%, conv4 -1.5%;
-    // profiles/r01_jit_deal.txt)
-    int deal = 0;
-    if (const char *e = std::getenv("SKC_JIT_DEAL")) deal = std::atoi(e) ? 1 : 0;
+    // channels of even block q (of nbg): contiguous ranges of the nnz-sorted list, or dealt in
+    // snake order (every block gets heavy and light channels alike).  With uniform masks the
+    // two measured the same (conv2 +0.8%, conv4 -1.5%; profiles/r01_jit_deal.txt); with skewed
+    // per-channel densities the contiguous ranges put the heaviest channels into one block,
+    // whose items then finish last (conv4 1.72x slower than unsorted,
+    // profiles/r02_skewed_masks_loadbalance.jsonl).  Snake dealing is taken when the
+    // contiguous blocks are imbalanced (SKC_JIT_DEAL=0/1 forces one)
+    int deal_force = -1;
+    if (const char *e = std::getenv("SKC_JIT_DEAL")) deal_force = std::atoi(e) ? 1 : 0;
+    double best_span = 0, snake_span = 0, imb0 = 1.0, imb1 = 1.0;
+    std::vector<Blk> best, snake;
+    const int smax = jp.dyn ? std::min(jp.nbg, (in.Kg + Mp - 1) / Mp) : 0;
+    for (int deal = 0; deal <= 1; ++deal) {
+    if (deal_force >= 0 && deal != deal_force) continue;
     std::vector<std::vector<int>> even(size_t(jp.nbg));
     for (int k = 0; k < in.Kg; ++k) {
         int q = k / Mp;
@@ -1822,9 +1926,6 @@ void choose_blocks(JitPlan &jp, int n_hint) {
         }
         if (q < jp.nbg) even[size_t(q)].push_back(k);
     }
-    double best_span = 0;
-    std::vector<Blk> best;
-    const int smax = jp.dyn ? std::min(jp.nbg, (in.Kg + Mp - 1) / Mp) : 0;
     for (int sp = 0; sp <= smax; ++sp) {
         if (force >= 0 && sp != std::min(force, smax)) continue;
         std::vector<Blk> full, tail;
@@ -1850,16 +1951,45 @@ void choose_blocks(JitPlan &jp, int n_hint) {
         for (const Blk &b : blks) tb.push_back(item_time(jp, b.instr));
         jp.nblocks = int(blks.size());
         const double span = simulate_makespan(jp, tb, nig, P);
+        // block imbalance: heaviest block's modelled instructions over the mean (the model
+        // charges every instruction alike, but a heavy block's code is longer than the
+        // instruction caches, so contiguous ranges of a skewed nnz-sorted list measured far
+        // slower than the makespan model says: decided by imbalance instead, below)
+        double imax = 0, isum = 0;
+        for (const Blk &b : full) {
+            imax = std::max(imax, b.instr);
+            isum += b.instr;
+        }
+        const double imb = full.empty() ? 1.0 : imax * double(full.size()) / isum;
         if (std::getenv("SKC_JIT_DEBUG"))
-            std::fprintf(stderr, "skc jit: split %d blocks %d P %lld nig %lld span %.0f ideal %.0f\n", sp,
-                         jp.nblocks, (long long)P, (long long)nig, span,
-                         [&] { double t = 0; for (double x : tb) t += x; return t * nig / P; }());
-        // a split must gain at least 1% (its halves repeat the window loads)
+            std::fprintf(stderr, "skc jit: deal %d split %d blocks %d P %lld nig %lld span %.0f ideal %.0f imbalance %.3f\n",
+                         deal, sp, jp.nblocks, (long long)P, (long long)nig, span,
+                         [&] { double t = 0; for (double x : tb) t += x; return t * nig / P; }(), imb);
+        if (sp == 0) (deal ? imb1 : imb0) = imb;
+        // a split (its halves repeat the window loads) must gain >= 1%
+        if (deal != (deal_force >= 0 ? deal_force : 0)) {
+            // snake dealing: kept aside, taken below if the contiguous blocks are imbalanced
+            if (sp == 0 && (snake.empty() || span < snake_span)) {
+                snake = blks;
+                snake_span = span;
+            }
+            continue;
+        }
         if (best.empty() || span < best_span * 0.99) {
             best_span = span;
             best = blks;
             jp.split = sp;
+            jp.deal = deal;
         }
+    }
+    }  // deal
+    // contiguous ranges of a skewed list: one block holds the heavy channels (imbalance > 1.25;
+    // uniform masks: 1.02-1.10) -- deal in snake order instead (no split)
+    if (deal_force < 0 && !snake.empty() && imb0 > 1.25 && imb1 < imb0) {
+        best = snake;
+        best_span = snake_span;
+        jp.split = 0;
+        jp.deal = 1;
     }
     // dynamic scheduling only where it splits: with equal items the static order measured
     // as fast or faster (conv3 -2.5%: it keeps the CTAs of a TPC on the same code)
@@ -2152,6 +2282,12 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     }
     jp.whole = jp.code_instr <= kWholeMaxInstr ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
+    if (const char *e = std::getenv("SKC_JIT_NP")) jp.np = std::atoi(e) ? 1 : 0;
+    if (jp.raw || jp.xpf) jp.np = 0;
+    if (jp.np) {
+        jp.whole = 0;  // separate modules, compiled in parallel
+        jp.dyn = 0;    // items in blockIdx order: the hardware hands them out as SMs free up
+    }
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
     for (int b = 0; b < jp.nblocks; ++b) {
         plan_block_channels(in, jp.bgrp[size_t(b)], jp.bidx[size_t(b)], ks);
@@ -2354,6 +2490,15 @@ int jit_prepare(JitPlan *jp, int dev, std::string *msg) {
         if (e != cudaSuccess) return cuda_fail("cudaLibraryLoadData", e);
         e = cudaLibraryGetKernel(&jp->kern, jp->lib, "skc_jit_kernel");
         if (e != cudaSuccess) return cuda_fail("cudaLibraryGetKernel", e);
+        if (jp->np) {
+            e = cudaLibraryGetKernel(&jp->kern_dry, jp->lib, "skc_jit_dry");
+            if (e != cudaSuccess) return cuda_fail("cudaLibraryGetKernel (dry)", e);
+        }
+    }
+    if (jp->kern_dry) {
+        cudaError_t ed = cudaFuncSetAttribute(reinterpret_cast<const void *>(jp->kern_dry),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(jp->smem));
+        if (ed != cudaSuccess) return cuda_fail("cudaFuncSetAttribute (dry)", ed);
     }
     const void *fn = reinterpret_cast<const void *>(jp->kern);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(jp->smem));
@@ -2468,6 +2613,7 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
         at[nat].val.programmaticStreamSerializationAllowed = 1;
         ++nat;
     }
+    int64_t conc = grid;  // CTAs resident at once (np: the first-round width G)
     if (cs > 1) {
         at[nat].id = cudaLaunchAttributeClusterDimension;
         at[nat].val.clusterDim.x = unsigned(cs);
@@ -2477,6 +2623,12 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
         int ncl = (cs == 2 || cs == 4 || cs == 8 || cs == 16) ? jp->ncl[cs] : 0;
         if (ncl < 1) ncl = std::max(1, nsm / cs);
         grid = std::min<int64_t>((items + cs - 1) / cs, ncl) * cs;
+        conc = grid;
+    }
+    if (jp->np) {
+        // one CTA per work item (a multiple of the cluster size; CTAs past the last item exit)
+        grid = (items + cs - 1) / cs * cs;
+        if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
     }
     lc.gridDim = dim3(unsigned(grid));
     lc.attrs = at;
@@ -2488,7 +2640,8 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
     // GPC-major first items (one CTA per SM, grid = all SMs; the kernel claims them, so a CTA
     // that shares an SM with another still gets a distinct item)
     const void *vid = nullptr;
-    if (sc.vid && jp->vid_ok && per_sm == 1 && grid == nsm && grid <= kVidCap && jp->dyn != 2 && cs <= 2)
+    if (sc.vid && jp->vid_ok && per_sm == 1 && conc == nsm && grid >= conc && conc <= kVidCap &&
+        jp->dyn != 2 && cs <= 2)
         vid = ws + jit_vid_offset(jp);
     unsigned sched = unsigned(sc.o3);
     if (sc.nodry) sched |= 4u;
@@ -2498,9 +2651,22 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
         std::fprintf(stderr, "skc jit: grid %lld cs %d gpc-major items %s\n", (long long)grid, cs,
                      vid ? "on" : "off");
     const void *lm = d_ws;
+    unsigned uG = unsigned(conc);
     void *args[] = {(void *)&in, (void *)&out, (void *)&lm, (void *)&bias,
                     (void *)&un, (void *)&relu, (void *)&opad, (void *)&olay, (void *)&vid,
-                    (void *)&sched};
+                    (void *)&sched, (void *)&uG};
+    if (jp->np && jp->dry && !sc.nodry) {
+        // the dry-run prefetch kernel: one chunk segment per CTA (all segments; with sched
+        // bit 9 at least one per resident CTA, each segment then run by several CTAs)
+        const int64_t segs = int64_t(jp->nblocks) * jp->nchunks;
+        cudaLaunchConfig_t ld{};
+        ld.blockDim = lc.blockDim;
+        ld.dynamicSmemBytes = jp->smem;
+        ld.stream = st;
+        ld.gridDim = dim3(unsigned(sc.dryall ? std::max<int64_t>(segs, conc) : segs));
+        cudaError_t e = cudaLaunchKernelExC(&ld, reinterpret_cast<const void *>(jp->kern_dry), args);
+        if (e != cudaSuccess) return e;
+    }
     return cudaLaunchKernelExC(&lc, reinterpret_cast<const void *>(jp->kern), args);
 }
 

@@ -153,6 +153,57 @@ __global__ void __launch_bounds__(256) pad_pairs_kernel(const float *__restrict_
     }
 }
 
+// Flat variant: one grid-stride loop over every (pair, element) of the batch with a grid of
+// whole waves (SMs x 8 CTAs), so the pass has no partly filled last wave per image and no
+// per-image grid dimension; otherwise as pad_pairs_kernel.  i < 2^31 (checked by the launcher).
+__global__ void __launch_bounds__(256) pad_pairs_flat_kernel(const float *__restrict__ in,
+                                                             float *__restrict__ out, int C, int H,
+                                                             int W, int pad, int Wp, uint32_t per_img,
+                                                             uint32_t total, int64_t N,
+                                                             FastDiv div_img, FastDiv div_plane,
+                                                             FastDiv div_wp) {
+    pdl_wait_and_trigger();
+    const int64_t img = int64_t(C) * H * W;
+    const uint32_t span = gridDim.x * blockDim.x * 2;
+    for (uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) * 2; base < total;
+         base += span * kPadUnroll) {
+        float v[kPadUnroll][4];
+#pragma unroll
+        for (int u = 0; u < kPadUnroll; ++u) {
+            const uint32_t i0 = base + u * span;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t i = i0 + k;
+                v[u][2 * k] = v[u][2 * k + 1] = 0.0f;
+                if (i < total) {
+                    const uint32_t p = fdiv(i, div_img);
+                    const uint32_t r0 = i - p * per_img;
+                    const uint32_t plane = fdiv(r0, div_plane);
+                    const uint32_t rem = r0 - plane * div_plane.d;
+                    const uint32_t yy = fdiv(rem, div_wp);
+                    const int y = int(yy) - pad;
+                    const int x = int(rem - yy * uint32_t(Wp)) - pad;
+                    if (y >= 0 && y < H && x >= 0 && x < W) {
+                        const float *a = in + 2 * int64_t(p) * img + (int64_t(plane) * H + y) * W + x;
+                        v[u][2 * k] = __ldg(a);
+                        if (2 * int64_t(p) + 1 < N) v[u][2 * k + 1] = __ldg(a + img);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPadUnroll; ++u) {
+            const uint32_t i0 = base + u * span;
+            if (i0 + 1 < total) {
+                *reinterpret_cast<float4 *>(out + 2 * size_t(i0)) =
+                    make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+            } else if (i0 < total) {
+                *reinterpret_cast<float2 *>(out + 2 * size_t(i0)) = make_float2(v[u][0], v[u][1]);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
@@ -222,9 +273,30 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
     const int Hp = H + 2 * pad, Wp = W + 2 * pad;
     const uint32_t per_img = uint32_t(int64_t(C) * Hp * Wp);
     const int threads = 256;
+    const int64_t P = (N + 1) / 2;
+    const char *flat_env = std::getenv("SKC_PAD_FLAT");
+    const bool flat = !flat_env || flat_env[0] != '0';
+    if (flat && P * int64_t(per_img) < (int64_t(1) << 31)) {
+        static int nsm = 0;
+        if (!nsm) {
+            int dev = 0, v = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess &&
+                cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+                nsm = v;
+            else
+                nsm = 148;
+        }
+        const uint32_t total = uint32_t(P * int64_t(per_img));
+        const int64_t need = (int64_t(total) + threads * 2 * kPadUnroll - 1) / (threads * 2 * kPadUnroll);
+        const int64_t grid = need < int64_t(nsm) * 8 ? need : int64_t(nsm) * 8;
+        cudaError_t e = pdl_launch(pad_pairs_flat_kernel, dim3(unsigned(grid)), dim3(threads), st, in, out,
+                                   C, H, W, pad, Wp, per_img, total, N, make_fastdiv(per_img),
+                                   make_fastdiv(uint32_t(Hp * Wp)), make_fastdiv(uint32_t(Wp)));
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+    }
     int64_t bx = (int64_t(per_img) + threads * 8 - 1) / (threads * 8);
     bx = bx > 4096 ? 4096 : bx;
-    const int64_t P = (N + 1) / 2;
     for (int64_t p0 = 0; p0 < P; p0 += 65535) {
         const int64_t np = (P - p0) < 65535 ? (P - p0) : 65535;
         // the last pair of an odd batch has no second image (has_b = 0 for that launch's

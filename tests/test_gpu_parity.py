@@ -51,14 +51,17 @@ def check(out, ref, bound, what=""):
     return worst
 
 
-@pytest.mark.parametrize("layout", ["nchw", "pairs"])
+@pytest.mark.parametrize("layout", ["nchw", "pairs", "pairs_per_image_grid"])
 def test_pad_bitwise_numpy(layout, monkeypatch):
     """a2 vs the library routine numpy.pad, ragged sizes and pads; for the
     image-pair layout of JIT plans, de-interleaving must give numpy.pad bit for bit and an
     odd batch's missing second image must be zeros.  (The JIT configuration may pick either
-    layout for a tiny layer; the pair case forces the pair layout.)"""
-    if layout == "pairs":
+    layout for a tiny layer; the pair cases force the pair layout; both pair-pad kernels --
+    the flat whole-wave one (default) and the per-image grid one -- are checked.)"""
+    if layout.startswith("pairs"):
         monkeypatch.setenv("SKC_JIT_PAIR", "1")
+        monkeypatch.setenv("SKC_PAD_FLAT", "0" if layout == "pairs_per_image_grid" else "1")
+        layout = "pairs"
     rng = np.random.default_rng(0)
     kern = skc.SKC_KERNEL_DIRECT if layout == "nchw" else skc.SKC_KERNEL_JIT
     for (N, C, H, W, p) in [(1, 4, 1, 1, 1), (3, 8, 7, 9, 2), (2, 96, 27, 27, 2), (4, 256, 13, 13, 1),
@@ -587,7 +590,10 @@ def test_jit_bitwise_equals_direct_full_batch(cfg_id):
     {"SKC_JIT_PMAJOR": "0"}, {"SKC_JIT_VID": "0"}, {"SKC_JIT_RAW": "1"},
     {"SKC_JIT_RAW": "1", "SKC_JIT_NS": "3", "SKC_JIT_STAGE_KB": "20"}, {"SKC_JIT_DEAL": "0"},
     {"SKC_JIT_DEAL": "1", "SKC_JIT_DYN": "1", "SKC_JIT_SPLIT": "2"}, {"SKC_JIT_LANES": "1"},
-    {"SKC_JIT_LANES": "1", "SKC_JIT_DYN": "2"},
+    {"SKC_JIT_LANES": "1", "SKC_JIT_DYN": "2"}, {"SKC_JIT_NP": "1"},
+    {"SKC_JIT_NP": "1", "SKC_JIT_SCHED": "546"}, {"SKC_JIT_NP": "1", "SKC_JIT_SCHED": "17"},
+    {"SKC_JIT_NP": "1", "SKC_JIT_GRID": "5", "SKC_JIT_CLUSTER": "1"}, {"SKC_JIT_LOOKAHEAD": "2"},
+    {"SKC_JIT_DEAL": "1", "SKC_JIT_NP": "1"}, {"SKC_JIT_OPT": "-O1"},
 ])
 def test_jit_tuning_knobs_bitwise(knobs, monkeypatch):
     """Every JIT tuning knob (work order, dry-run prefetch, L2 policy, cluster size, layout,
@@ -755,11 +761,14 @@ SCHEDULES = [o3 | (v << 1) | (nd << 2) | (ln << 3) | (cs << 4) | (da << 9)
              for da in (0, 1)]
 
 
-def test_jit_every_schedule_bitwise(monkeypatch):
+@pytest.mark.parametrize("np_mode", ["0", "1"])
+def test_jit_every_schedule_bitwise(np_mode, monkeypatch):
     """The schedules the bench actually runs: every launch-schedule word the tuner can pick
     (forced with SKC_JIT_SCHED) on all four config-2 layers at the full batch of 256, in the
-    plans AUTO builds -- each BIT FOR BIT equal to the direct kernel (whose output the oracle
-    checks in test_config_parity_full_batch)."""
+    plans AUTO builds (persistent whole-program kernel, and the non-persistent per-block-module
+    kernel, SKC_JIT_NP=1) -- each BIT FOR BIT equal to the direct kernel (whose output the
+    oracle checks in test_config_parity_full_batch)."""
+    monkeypatch.setenv("SKC_JIT_NP", np_mode)
     cfg = wl.CONFIGS[2]
     for li, L in enumerate(cfg.layers):
         w = wl.gen_weights(2, li, L)
