@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed outputs")
     ap.add_argument("--parity-images", type=int, default=16, help="images per layer the oracle checks")
     ap.add_argument("--no-peaks", action="store_true", help="skip the FFMA/LDS micro-benchmarks")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: host-side collectives; lets "
+                         "several ranks share one GPU for a functional run of the multi-rank path)")
     return ap.parse_args()
 
 
@@ -300,8 +303,10 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: CUDA device required (there is no CPU fallback)")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    # collectives (off the timed path) on the GPU with NCCL, on host tensors with gloo
+    cdev = dev if args.backend == "nccl" else torch.device("cpu")
     torch.backends.cudnn.allow_tf32 = False
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.benchmark = True
@@ -354,7 +359,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         out = torch.empty(conv.out_shape(local_n), device=dev)
         layers.append(dict(L=L, w=ws[li], conv=conv, x=x, xp=xp, out=out, x_host=x_host,
                            nnz=int(conv.geom["nnz"])))
-        if world > 1 and not skd.check_same_plan(conv.plan, dev):
+        if world > 1 and not skd.check_same_plan(conv.plan, cdev):
             raise SystemExit(f"bench.py: rank {rank} packed a different plan for {L.name}")
 
     t_build = time.time() - t_build
@@ -372,7 +377,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     def step(evs=None):
         step_on(stream, evs)
 
-    clk = ClockSampler(local_rank).start()
+    clk = ClockSampler(dev.index).start()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -430,7 +435,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_local = float(np.mean(step_ms))
     t_step = t_local
     if world > 1:
-        t_step = skd.max_over_ranks(t_local, dev)
+        t_step = skd.max_over_ranks(t_local, cdev)
 
     local_nnz_flops = sum(nnz_flops(d["L"], d["nnz"], local_n) for d in layers)
     step_nnz_flops = sum(nnz_flops(d["L"], d["nnz"], n_global) for d in layers)
@@ -458,12 +463,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                 e = oracle_err(x_imgs, d["w"], L, got)
                 per_layer_par.append({"layer": L.name, "images": len(idx), "max_err_over_bound": e})
                 continue
-            full_g = skd.gather_images(d["out"], n_global) if strong else None
+            full_g = skd.gather_images(d["out"] if cdev.type == "cuda" else d["out"].cpu(),
+                                       n_global) if strong else None
             if not strong:
                 # weak scaling: every rank checks its own images against the oracle
                 idx = sample_images(0, local_n, args.parity_images, rng)
                 e = oracle_err(d["x_host"][idx].numpy(), d["w"], L, d["out"][idx].cpu().numpy())
-                e = skd.max_over_ranks(e, dev)
+                e = skd.max_over_ranks(e, cdev)
                 per_layer_par.append({"layer": L.name, "images": len(idx) * world, "max_err_over_bound": e})
                 continue
             ref = None
@@ -578,14 +584,14 @@ def run_ours(args, cfg, rank, world, local_rank):
             ems.append(a.elapsed_time(b))
         t_e2e = float(np.mean(ems))
         if world > 1:
-            t_e2e = skd.max_over_ranks(t_e2e, dev)
+            t_e2e = skd.max_over_ranks(t_e2e, cdev)
         e2e_ok = None
         if not args.no_parity:
             # the host outputs of the last e2e step: bitwise equal to the device path's
             e2e_ok = all(bool(torch.equal(ho.view(torch.int32), d["out"].cpu().view(torch.int32)))
                          for ho, d in zip(hout, layers))
             if world > 1:
-                e2e_ok = skd.max_over_ranks(0.0 if e2e_ok else 1.0, dev) == 0.0
+                e2e_ok = skd.max_over_ranks(0.0 if e2e_ok else 1.0, cdev) == 0.0
         e2e = {"value": step_nnz_flops / (t_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                "ms_per_step": t_e2e,
                "h2d_bytes_per_step": int(sum(h.numel() * 4 for h in hin)),
@@ -708,8 +714,11 @@ def main():
         import torch
         import torch.distributed as dist
         if args.impl == "ours":
-            torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if args.backend == "nccl":
+                torch.cuda.set_device(local_rank)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            else:
+                dist.init_process_group("gloo")
     try:
         if args.impl == "reference":
             run_reference(args, cfg, rank, world)

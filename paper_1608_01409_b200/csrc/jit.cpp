@@ -181,6 +181,7 @@ struct JitPlan {
     // as separate modules in parallel -- no ABI saves either, seconds to build) plus a
     // separate dry-run prefetch kernel (skc_jit_dry)
     int np = 0;
+    int np_ret = 0;            // debug (SKC_JIT_NP_RET=1): np, but block functions return
     double code_instr = 0;     // modelled instructions of all blocks' code
     int nbg = 0, nblocks = 0;  // blocks per group (even partition), total blocks
     // block b: conv group, first index into the group's nnz-sorted channels, channel count.
@@ -510,7 +511,7 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
     o("%s", kHdr);
     // np (non-persistent per-block modules): the function never returns -- it ends the thread
     // (`exit`), so a separately compiled block saves no callee-saved registers
-    o(".visible .func skc_b%d%s%s", b, kBlkParams, jp.np ? " .noreturn" : "");
+    o(".visible .func skc_b%d%s%s", b, kBlkParams, jp.np && !jp.np_ret ? " .noreturn" : "");
     o("{");
     o(".reg .pred %%p<10>;");
     o(".reg .b32 %%r<32>;");
@@ -914,9 +915,9 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
         }
     }
     if (fast_epi) o("$EPI_END:");
-    o(jp.np ? "exit;" : "ret;");
+    o(jp.np && !jp.np_ret ? "exit;" : "ret;");
     o("$DRYRET:");
-    o(jp.np ? "exit;" : "ret;");
+    o(jp.np && !jp.np_ret ? "exit;" : "ret;");
     o("}");
     return std::move(o.s);
 }
@@ -1027,7 +1028,7 @@ std::string emit_entry(const JitPlan &jp) {
     Out o;
     o("%s", kHdr);
     for (int b = 0; b < jp.nblocks; ++b)
-        o(".extern .func skc_b%d%s%s;", b, kBlkParams, jp.np ? " .noreturn" : "");
+        o(".extern .func skc_b%d%s%s;", b, kBlkParams, jp.np && !jp.np_ret ? " .noreturn" : "");
     o(".extern .shared .align 128 .b8 skc_smem[];");
     if (jp.np) emit_dry_entry(o, jp);
     o(".visible .entry skc_jit_kernel(%s)", kEntryParams);
@@ -2287,6 +2288,8 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (jp.np) {
         jp.whole = 0;  // separate modules, compiled in parallel
         jp.dyn = 0;    // items in blockIdx order: the hardware hands them out as SMs free up
+        if (const char *e = std::getenv("SKC_JIT_NP_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
+        if (const char *e = std::getenv("SKC_JIT_NP_RET")) jp.np_ret = std::atoi(e) ? 1 : 0;
     }
     jp.chan.assign(size_t(jp.nblocks) * jp.M, -1);
     for (int b = 0; b < jp.nblocks; ++b) {
@@ -2582,8 +2585,9 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
         return cudaErrorInvalidResourceHandle;
     }
     // persistent grid: one CTA per SM slot (the kernel loops over its work items)
+    // work items: image groups x row bands x channel blocks (as the kernel numbers them)
     const int64_t nig = (int64_t(N) + jp->NI - 1) / jp->NI;
-    const int64_t items = nig * jp->nblocks;
+    const int64_t items = nig * jp->NB * jp->nblocks;
     if (items > 0x7fffffff) return cudaErrorInvalidConfiguration;
     const int nsm = jp->nsm, per_sm = jp->per_sm;
     const Sched sc = launch_sched(jp);

@@ -274,8 +274,11 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
     const uint32_t per_img = uint32_t(int64_t(C) * Hp * Wp);
     const int threads = 256;
     const int64_t P = (N + 1) / 2;
+    // SKC_PAD_FLAT=1: one whole-wave grid over the batch -- measured SLOWER than the per-pair
+    // grid (conv2-5 pads 0.038/0.027/0.037/0.038 vs 0.0325/0.024/0.031/0.032 ms,
+    // profiles/r02_pad_flat.txt), kept as an option
     const char *flat_env = std::getenv("SKC_PAD_FLAT");
-    const bool flat = !flat_env || flat_env[0] != '0';
+    const bool flat = flat_env && flat_env[0] == '1';
     if (flat && P * int64_t(per_img) < (int64_t(1) << 31)) {
         static int nsm = 0;
         if (!nsm) {
