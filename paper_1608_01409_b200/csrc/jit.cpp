@@ -2281,8 +2281,15 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     }
                 }
     }
+    // moderate code: one whole-program module (fastest code; compile time grows ~n^1.7 with
+    // the module, 20-70 s for an AlexNet layer).  Larger code: the non-persistent kernel over
+    // per-block .noreturn modules compiled in parallel (seconds; 3-6% faster than the
+    // persistent kernel over per-block modules, whose calls save callee-saved registers --
+    // config 4 res256 / res512 -3.6% / -5.7%, profiles/r02_jit_np.txt).  SKC_JIT_NP=1 forces
+    // the fast-build mode for any code (AlexNet: 3.4-4.8 s per layer, step +3.6%)
     jp.whole = jp.code_instr <= kWholeMaxInstr ? 1 : 0;
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
+    jp.np = jp.whole ? 0 : 1;
     if (const char *e = std::getenv("SKC_JIT_NP")) jp.np = std::atoi(e) ? 1 : 0;
     if (jp.raw || jp.xpf) jp.np = 0;
     if (jp.np) {
