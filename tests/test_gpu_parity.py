@@ -51,21 +51,23 @@ def check(out, ref, bound, what=""):
     return worst
 
 
-@pytest.mark.parametrize("layout", ["nchw", "pairs", "pairs_per_image_grid"])
+@pytest.mark.parametrize("layout", ["nchw", "pairs", "pairs_grid", "pairs_flat"])
 def test_pad_bitwise_numpy(layout, monkeypatch):
     """a2 vs the library routine numpy.pad, ragged sizes and pads; for the
     image-pair layout of JIT plans, de-interleaving must give numpy.pad bit for bit and an
     odd batch's missing second image must be zeros.  (The JIT configuration may pick either
-    layout for a tiny layer; the pair cases force the pair layout; both pair-pad kernels --
-    the flat whole-wave one (default) and the per-image grid one -- are checked.)"""
+    layout for a tiny layer; the pair cases force the pair layout; all three pair-pad kernels
+    -- per-plane (default; planes <= 2048 positions), per-pair grid, flat -- are checked.)"""
     if layout.startswith("pairs"):
         monkeypatch.setenv("SKC_JIT_PAIR", "1")
-        monkeypatch.setenv("SKC_PAD_FLAT", "0" if layout == "pairs_per_image_grid" else "1")
+        monkeypatch.setenv("SKC_PAD_PLANES", "1" if layout == "pairs" else "0")
+        monkeypatch.setenv("SKC_PAD_FLAT", "1" if layout == "pairs_flat" else "0")
         layout = "pairs"
     rng = np.random.default_rng(0)
     kern = skc.SKC_KERNEL_DIRECT if layout == "nchw" else skc.SKC_KERNEL_JIT
     for (N, C, H, W, p) in [(1, 4, 1, 1, 1), (3, 8, 7, 9, 2), (2, 96, 27, 27, 2), (4, 256, 13, 13, 1),
-                            (2, 4, 5, 4, 0), (1, 64, 56, 56, 1), (65, 4, 3, 3, 3), (5, 2, 3, 3, 1)]:
+                            (2, 4, 5, 4, 0), (1, 64, 56, 56, 1), (65, 4, 3, 3, 3), (5, 2, 3, 3, 1),
+                            (7, 12, 40, 40, 2), (3, 4, 14, 14, 1)]:
         x = rng.standard_normal((N, C, H, W), dtype=np.float32)
         x[0, 0, 0, 0] = -0.0
         try:
