@@ -51,16 +51,15 @@ def check(out, ref, bound, what=""):
     return worst
 
 
-@pytest.mark.parametrize("layout", ["nchw", "pairs", "pairs_grid", "pairs_flat"])
+@pytest.mark.parametrize("layout", ["nchw", "pairs", "pairs_flat"])
 def test_pad_bitwise_numpy(layout, monkeypatch):
     """a2 vs the library routine numpy.pad, ragged sizes and pads; for the
     image-pair layout of JIT plans, de-interleaving must give numpy.pad bit for bit and an
     odd batch's missing second image must be zeros.  (The JIT configuration may pick either
-    layout for a tiny layer; the pair cases force the pair layout; all three pair-pad kernels
-    -- per-plane (default; planes <= 2048 positions), per-pair grid, flat -- are checked.)"""
+    layout for a tiny layer; the pair cases force the pair layout; both pair-pad kernels --
+    the per-pair grid (default) and the flat one -- are checked.)"""
     if layout.startswith("pairs"):
         monkeypatch.setenv("SKC_JIT_PAIR", "1")
-        monkeypatch.setenv("SKC_PAD_PLANES", "1" if layout == "pairs" else "0")
         monkeypatch.setenv("SKC_PAD_FLAT", "1" if layout == "pairs_flat" else "0")
         layout = "pairs"
     rng = np.random.default_rng(0)
