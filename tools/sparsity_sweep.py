@@ -71,6 +71,7 @@ def main():
     for li, L in enumerate(cfg.layers):
         w = wl.gen_weights(3, li, L)
         conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups)
+        conv.tune(N)
         xp = torch.empty(conv.padded_shape(N), device="cuda")
         out = torch.empty(conv.out_shape(N), device="cuda")
         t_pad = timed(lambda: skc.skc_pad_input(conv.plan, x, xp, N), flush=flush)
@@ -78,10 +79,14 @@ def main():
         nnz = conv.geom["nnz"]
         density = nnz / (L.K * (L.C // L.groups) * L.R * L.S)
         t = t_pad + t_conv
+        # rates on both time bases, named explicitly: conv = skc_sparse_conv_forward alone,
+        # layer = skc_pad_input + skc_sparse_conv_forward (the speedups use the layer time)
         r = dict(sparsity=L.sparsity, density=density, nnz=nnz, kernel=conv.geom["kernel"],
                  t_pad_ms=t_pad, t_conv_ms=t_conv, t_layer_ms=t,
                  nnz_tflops=2 * nnz * L.Ho * L.Wo * N / (t_conv * 1e-3) / 1e12,
+                 nnz_tflops_layer=2 * nnz * L.Ho * L.Wo * N / (t * 1e-3) / 1e12,
                  dense_equiv_tflops=dense_flops / (t * 1e-3) / 1e12,
+                 dense_equiv_tflops_conv=dense_flops / (t_conv * 1e-3) / 1e12,
                  speedup_vs_sgemm_proxy=t_sgemm / t, speedup_vs_cudnn=t_cudnn / t)
         rows.append(r)
         print(json.dumps(r), flush=True)
