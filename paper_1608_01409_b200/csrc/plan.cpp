@@ -1359,7 +1359,9 @@ skc_status skc_forward_host(const skc_plan *p, const float *h_in, float *h_out, 
     const size_t pad_img = p->layout == SKC_LAYOUT_RAW ? in_img : size_t(p->C) * p->Hp * p->Wp;
     const size_t out_img = size_t(p->K) * p->Ho * p->Wo;
     // chunks: a few per call, whole images, >= 8 images each
-    int nchunk = std::max(1, std::min(8, N / 8));
+    int max_chunks = 8;  // SKC_HOST_CHUNKS: pipeline depth (tuning)
+    if (const char *e = std::getenv("SKC_HOST_CHUNKS")) max_chunks = std::max(1, std::atoi(e));
+    int nchunk = std::max(1, std::min(max_chunks, N / 8));
     int per = (N + nchunk - 1) / nchunk;
     if (p->layout == SKC_LAYOUT_PAIRS) per += per & 1;  // chunks start on an image pair
     nchunk = (N + per - 1) / per;
