@@ -629,7 +629,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             "kernel_cfg": {k: d["conv"].plan.info()[k] for k in (
                 "kernel", "band_rows", "chunk_channels", "stages", "warps", "channels_per_warp",
                 "pixels_per_lane", "smem_bytes", "tile_h", "tile_w", "images_per_cta",
-                "jit_blocks", "jit_split", "jit_sched", "code_bytes", "jit_compile_s", "jit_cache_hit")},
+                "jit_blocks", "jit_split", "jit_sched", "jit_np", "jit_deal", "code_bytes", "jit_compile_s",
+                "jit_cache_hit")},
         })
     cpu = None
     if not args.no_cpu and world >= 1:
@@ -683,10 +684,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,
-        "gpu_launches": 2 * len(layers) * args.steps,
+        # per layer: the pad pass + the conv kernel (+ the dry-run prefetch kernel of np plans)
+        "gpu_launches": sum(2 + dry_kernel(d["conv"].plan.info()) for d in layers) * args.steps,
         "plan_build_s": t_build,
     }
     print(json.dumps(line), flush=True)
+
+
+def dry_kernel(info: dict) -> int:
+    """1 if a forward of this plan also launches the np dry-run prefetch kernel."""
+    sched = int(info.get("jit_sched", -1))
+    return int(bool(info.get("jit_np")) and not (sched >= 0 and sched & 4))
 
 
 def oracle_one_image(cfg_id: int) -> dict:

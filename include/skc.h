@@ -118,6 +118,11 @@ typedef struct {
                                       item numbers, bit 2 no dry-run code prefetch, bit 3
                                       contiguous lane table, bits 4-7 cluster size, bit 9
                                       dry run by every CTA                                */
+    int jit_np;                    /* JIT: 1 = non-persistent kernel over per-block modules
+                                      (one work item per CTA); a forward then launches 2
+                                      kernels: the dry-run code prefetch and the items     */
+    int jit_deal;                  /* JIT: 1 = channels dealt to blocks in snake order
+                                      (skewed per-channel nnz), 0 = contiguous ranges     */
 } skc_info;
 
 /* a1 -- CSR/offset packer (PAPER.md:210-216 Fig. 2 caption; :251-256 mode-1 matricisation).

@@ -2476,6 +2476,8 @@ void jit_info(const JitPlan *jp, JitInfo *o) {
     o->pair = jp->pair;
     o->bands = jp->NB;
     o->whole = jp->whole;
+    o->np = jp->np;
+    o->deal = jp->deal;
     o->compiled = jp->compiled ? 1 : 0;
 }
 

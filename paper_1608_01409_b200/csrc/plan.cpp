@@ -875,6 +875,8 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.jit_whole = 0;
     i.jit_split = 0;
     i.jit_sched = -1;
+    i.jit_np = 0;
+    i.jit_deal = 0;
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -888,6 +890,8 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
         i.jit_whole = j.whole;
         i.jit_split = j.split;
         i.jit_sched = j.sched;
+        i.jit_np = j.np;
+        i.jit_deal = j.deal;
     }
     return ok();
 }

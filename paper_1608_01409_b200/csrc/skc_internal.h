@@ -126,6 +126,8 @@ struct JitInfo {
     int split; // even blocks per group split into halves
     int sched; // tuned launch schedule (skc_info.jit_sched), -1 untuned
     int raw;   // 1: reads the unpadded NCHW input (halo filled while staging)
+    int np;    // 1: non-persistent kernel (one item per CTA) + dry-run kernel
+    int deal;  // 1: channels dealt to blocks in snake order
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).

@@ -52,7 +52,8 @@ class skc_info(ctypes.Structure):
         ("jit_compiled", ctypes.c_int), ("jit_cache_hit", ctypes.c_int),
         ("jit_compile_s", ctypes.c_double), ("code_bytes", ctypes.c_size_t),
         ("model_instr_per_image", ctypes.c_double), ("layout", ctypes.c_int), ("bands", ctypes.c_int), ("jit_whole", ctypes.c_int),
-        ("jit_split", ctypes.c_int), ("jit_sched", ctypes.c_int)]
+        ("jit_split", ctypes.c_int), ("jit_sched", ctypes.c_int), ("jit_np", ctypes.c_int),
+        ("jit_deal", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

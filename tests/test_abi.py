@@ -203,3 +203,19 @@ def test_plan_verify_random(L):
             n_rt += kern == skc.SKC_KERNEL_REGTILE
             skc.skc_plan_verify(plan)
     assert n_rt >= 20
+
+
+def test_library_never_allocates_device_memory():
+    """skc.h: libskc never allocates device memory -- PyTorch owns every buffer (workspace,
+    activations, tuning scratch).  No allocation call may appear in the library's sources."""
+    import glob
+    import re
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_1608_01409_b200", "csrc")
+    bad = re.compile(r"\b(cudaMalloc\w*|cuMemAlloc\w*|cudaMallocAsync|cudaHostAlloc|cudaMallocManaged)\s*\(")
+    hits = []
+    for path in glob.glob(os.path.join(root, "*")):
+        for n, line in enumerate(open(path, errors="replace"), 1):
+            if bad.search(line):
+                hits.append(f"{os.path.basename(path)}:{n}: {line.strip()}")
+    assert not hits, hits
