@@ -229,7 +229,9 @@ skc_status skc_sparse_conv_forward_into(const skc_plan *plan, const float *d_in_
  * h_out [N][K][Ho][Wo] (host memory; pinned for asynchronous overlap).  The batch is cut
  * into image chunks; the H2D copy of a chunk, pad + conv of the previous one (on `stream`)
  * and the D2H copy of the one before run concurrently on two internal copy streams.  The
- * call returns after enqueueing; `stream` completes after the last D2H copy.  Caller-owned
+ * call returns after enqueueing; `stream` completes after the last D2H copy.  It creates (and
+ * releases) two internal non-blocking copy streams and a few events per call, so unlike the
+ * device-buffer entry points it cannot be captured into a CUDA graph.  Caller-owned
  * device scratch for the whole batch: d_in [N][C][H][W], d_in_padded (in the plan's layout),
  * d_out.  Requires
  * skc_plan_upload.  Errors: as skc_pad_input / skc_sparse_conv_forward, SKC_ERR_CUDA for

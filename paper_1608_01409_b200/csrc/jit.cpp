@@ -982,6 +982,7 @@ void emit_dry_entry(Out &o, const JitPlan &jp) {
     o(".reg .pred %%p<4>;");
     o(".reg .b32 %%r<16>;");
     o(".reg .b64 %%rd<8>;");
+    o("griddepcontrol.launch_dependents;");   // the items may start as dry CTAs retire
     o("ld.param.u64 %%rd2, [p_lm];");
     o("cvta.to.global.u64 %%rd2, %%rd2;");
     o("mov.u32 %%r3, %%tid.x;");
@@ -1212,7 +1213,13 @@ std::string emit_entry(const JitPlan &jp) {
         o("bra.uni $DRY_LOOP;");
         o("$DRY_DONE:");
     }
+    // (sched bit 10: launched programmatically right after the np dry-run kernel, which this
+    // kernel does not depend on -- its inputs were complete before that kernel started)
+    o("and.b32 %%r62, %%r61, 1024;");
+    o("setp.ne.u32 %%p0, %%r62, 0;");
+    o("@%%p0 bra $NO_PDL_WAIT;");
     o("griddepcontrol.wait;");
+    o("$NO_PDL_WAIT:");
     // dynamic scheduling: thread 0 takes the next item from a global counter in the plan
     // workspace (after the lane tables); items are numbered longest-first, so CTAs that
     // finish early take the short tail items.  The last CTA to exit resets the counters.
@@ -2615,7 +2622,7 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
                      jp->smem, per_sm);
     }
     cudaLaunchConfig_t lc{};
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     lc.blockDim = dim3(unsigned(jp->NW * 32));
     lc.dynamicSmemBytes = jp->smem;
     lc.stream = st;
@@ -2670,7 +2677,10 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
                     (void *)&sched, (void *)&uG};
     if (jp->np && jp->dry && !sc.nodry) {
         // the dry-run prefetch kernel: one chunk segment per CTA (all segments; with sched
-        // bit 9 at least one per resident CTA, each segment then run by several CTAs)
+        // bit 9 at least one per resident CTA, each segment then run by several CTAs).  A plain
+        // launch (it follows the producer of the input); the items kernel is launched
+        // programmatically after it and skips its grid-dependency wait (sched bit 10): it
+        // needs nothing from the dry run, so its CTAs take SMs as the dry CTAs retire
         const int64_t segs = int64_t(jp->nblocks) * jp->nchunks;
         cudaLaunchConfig_t ld{};
         ld.blockDim = lc.blockDim;
@@ -2679,6 +2689,18 @@ cudaError_t jit_launch(JitPlan *jp, const float *in, float *out, const void *d_w
         ld.gridDim = dim3(unsigned(sc.dryall ? std::max<int64_t>(segs, conc) : segs));
         cudaError_t e = cudaLaunchKernelExC(&ld, reinterpret_cast<const void *>(jp->kern_dry), args);
         if (e != cudaSuccess) return e;
+        if (!std::getenv("SKC_NP_NOPDL")) {
+            bool has_pdl = false;
+            for (int i = 0; i < nat; ++i)
+                has_pdl |= at[i].id == cudaLaunchAttributeProgrammaticStreamSerialization;
+            if (!has_pdl) {
+                at[nat].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[nat].val.programmaticStreamSerializationAllowed = 1;
+                ++nat;
+                lc.numAttrs = nat;
+            }
+            sched |= 1024u;
+        }
     }
     return cudaLaunchKernelExC(&lc, reinterpret_cast<const void *>(jp->kern), args);
 }
