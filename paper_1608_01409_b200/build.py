@@ -22,10 +22,9 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.
 SOURCES = ["plan.cpp", "jit.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu", "topo.cu"]
 # the JIT kernel compiles and links its generated code in-process (no ptxas on PATH needed)
 CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
-# static PTX compiler + nvJitLink (a shared libnvJitLink clashes with the older copy torch
-# loads into the same process: versioned symbols); ~135 MB of the .so
-JIT_LIBS = [os.path.join(CUDA_LIB, "libnvJitLink_static.a"),
-            os.path.join(CUDA_LIB, "libnvptxcompiler_static.a"), "-lpthread", "-ldl", "-lrt"]
+# the PTX compiler is static (it only exists as an archive); nvJitLink is dlopen'ed at run time
+# from the toolkit (jit.cpp: jitlink()), so its 130 MB archive is not linked in
+JIT_LIBS = [os.path.join(CUDA_LIB, "libnvptxcompiler_static.a"), "-lpthread", "-ldl", "-lrt"]
 HEADERS = ["skc_internal.h", "ptx.cuh"]
 GENERATED = os.path.join(BUILD, "regtile_gen.inc")  # gen_regtile.py output (not committed)
 

@@ -42,6 +42,7 @@
 #include "skc.h"
 #include "skc_internal.h"
 
+#include <dlfcn.h>
 #include <nvJitLink.h>
 #include <nvPTXCompiler.h>
 
@@ -1592,6 +1593,53 @@ std::string emit_entry(const JitPlan &jp) {
 // ---------------------------------------------------------------------------------------
 // compile + link (PTX compiler library in a thread pool, nvJitLink), with an on-disk cache
 // ---------------------------------------------------------------------------------------
+// nvJitLink (only the per-block build links modules) is loaded from the toolkit at first use,
+// privately (RTLD_LOCAL) by path: PyTorch maps its own, older libnvJitLink.so.12 into the
+// process, whose versioned symbols do not match this header's, so the library can neither
+// link the shared one at build time nor rely on the one already loaded; linking the static
+// archive instead would add ~90 MB to libskc.so.  Without it, plans compile as one whole
+// program (nvPTXCompiler alone).
+struct JitLinkApi {
+    bool ok = false;
+    nvJitLinkResult (*create)(nvJitLinkHandle *, uint32_t, const char **) = nullptr;
+    nvJitLinkResult (*destroy)(nvJitLinkHandle *) = nullptr;
+    nvJitLinkResult (*add_data)(nvJitLinkHandle, nvJitLinkInputType, const void *, size_t, const char *) = nullptr;
+    nvJitLinkResult (*complete)(nvJitLinkHandle) = nullptr;
+    nvJitLinkResult (*cubin_size)(nvJitLinkHandle, size_t *) = nullptr;
+    nvJitLinkResult (*cubin)(nvJitLinkHandle, void *) = nullptr;
+    nvJitLinkResult (*log_size)(nvJitLinkHandle, size_t *) = nullptr;
+    nvJitLinkResult (*log)(nvJitLinkHandle, char *) = nullptr;
+};
+
+const JitLinkApi &jitlink() {
+    static JitLinkApi api = [] {
+        JitLinkApi a;
+        std::vector<std::string> paths;
+        if (const char *e = std::getenv("SKC_NVJITLINK")) paths.push_back(e);
+        for (const char *h : {"CUDA_HOME", "CUDA_PATH"})
+            if (const char *e = std::getenv(h)) paths.push_back(std::string(e) + "/lib64/libnvJitLink.so.12");
+        paths.push_back("/usr/local/cuda/lib64/libnvJitLink.so.12");
+        paths.push_back("/usr/local/cuda-12.9/lib64/libnvJitLink.so.12");
+        void *h = nullptr;
+        for (const auto &p : paths)
+            if ((h = dlopen(p.c_str(), RTLD_NOW | RTLD_LOCAL))) break;
+        if (!h) return a;
+        auto sym = [&](const char *n) { return dlsym(h, n); };
+        a.create = reinterpret_cast<decltype(a.create)>(sym("__nvJitLinkCreate_12_9"));
+        a.destroy = reinterpret_cast<decltype(a.destroy)>(sym("__nvJitLinkDestroy_12_9"));
+        a.add_data = reinterpret_cast<decltype(a.add_data)>(sym("__nvJitLinkAddData_12_9"));
+        a.complete = reinterpret_cast<decltype(a.complete)>(sym("__nvJitLinkComplete_12_9"));
+        a.cubin_size = reinterpret_cast<decltype(a.cubin_size)>(sym("__nvJitLinkGetLinkedCubinSize_12_9"));
+        a.cubin = reinterpret_cast<decltype(a.cubin)>(sym("__nvJitLinkGetLinkedCubin_12_9"));
+        a.log_size = reinterpret_cast<decltype(a.log_size)>(sym("__nvJitLinkGetErrorLogSize_12_9"));
+        a.log = reinterpret_cast<decltype(a.log)>(sym("__nvJitLinkGetErrorLog_12_9"));
+        a.ok = a.create && a.destroy && a.add_data && a.complete && a.cubin_size && a.cubin &&
+               a.log_size && a.log;
+        return a;
+    }();
+    return api;
+}
+
 bool compile_ptx(const std::string &ptx, const char *opt, int maxreg, std::vector<char> &obj,
                  std::string *msg, bool relocatable = true) {
     nvPTXCompilerHandle h = nullptr;
@@ -2298,6 +2346,10 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     if (const char *e = std::getenv("SKC_JIT_WHOLE")) jp.whole = std::atoi(e) ? 1 : 0;
     jp.np = jp.whole ? 0 : 1;
     if (const char *e = std::getenv("SKC_JIT_NP")) jp.np = std::atoi(e) ? 1 : 0;
+    if (!jp.whole && !jitlink().ok) {  // no linker: one whole-program module, whatever its size
+        jp.whole = 1;
+        jp.np = 0;
+    }
     if (jp.raw || jp.xpf) jp.np = 0;
     if (jp.np) {
         jp.whole = 0;  // separate modules, compiled in parallel
@@ -2411,33 +2463,33 @@ int jit_compile(JitPlan *jp, std::string *msg) {
             return SKC_ERR_UNSUPPORTED;
         }
     // link
+    const JitLinkApi &jl = jitlink();
     nvJitLinkHandle lh = nullptr;
     const char *lopts[] = {"-arch=sm_100a"};
-    if (nvJitLinkCreate(&lh, 1, lopts) != NVJITLINK_SUCCESS) {
-        *msg = "nvJitLinkCreate failed";
+    if (!jl.ok || jl.create(&lh, 1, lopts) != NVJITLINK_SUCCESS) {
+        *msg = jl.ok ? "nvJitLinkCreate failed" : "nvJitLink not found (set SKC_NVJITLINK)";
         return SKC_ERR_UNSUPPORTED;
     }
     nvJitLinkResult lr = NVJITLINK_SUCCESS;
     for (size_t i = 0; i < objs.size() && lr == NVJITLINK_SUCCESS; ++i) {
         const std::string name = "m" + std::to_string(i);
-        lr = nvJitLinkAddData(lh, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(),
-                              name.c_str());
+        lr = jl.add_data(lh, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(), name.c_str());
     }
-    if (lr == NVJITLINK_SUCCESS) lr = nvJitLinkComplete(lh);
+    if (lr == NVJITLINK_SUCCESS) lr = jl.complete(lh);
     if (lr != NVJITLINK_SUCCESS) {
         size_t n = 0;
-        nvJitLinkGetErrorLogSize(lh, &n);
+        jl.log_size(lh, &n);
         std::string log(n, '\0');
-        if (n) nvJitLinkGetErrorLog(lh, &log[0]);
-        nvJitLinkDestroy(&lh);
+        if (n) jl.log(lh, &log[0]);
+        jl.destroy(&lh);
         *msg = "nvJitLink failed (" + std::to_string(int(lr)) + "): " + log.substr(0, 800);
         return SKC_ERR_UNSUPPORTED;
     }
     size_t n = 0;
-    nvJitLinkGetLinkedCubinSize(lh, &n);
+    jl.cubin_size(lh, &n);
     jp->cubin.resize(n);
-    nvJitLinkGetLinkedCubin(lh, jp->cubin.data());
-    nvJitLinkDestroy(&lh);
+    jl.cubin(lh, jp->cubin.data());
+    jl.destroy(&lh);
     cache_write(key, jp->cubin);
     jp->compiled = true;
     jp->compile_s =
