@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--layer", type=int, default=1)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between launches")
     a = ap.parse_args()
     cfg = wl.CONFIGS[a.config]
     L = cfg.layers[a.layer]
@@ -39,7 +40,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ts = []
     for r in range(a.reps + 3):
-        flush.fill_(1)
+        if not a.no_flush:
+            flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         skc.skc_sparse_conv_forward(conv.plan, xp, out, N)
