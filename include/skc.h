@@ -202,6 +202,15 @@ skc_status skc_sparse_conv_forward(const skc_plan *plan, const float *d_in_padde
 skc_status skc_im2col(const skc_plan *plan, const float *d_in_nchw, float *d_lowered, int N,
                       void *stream);
 
+/* skc_im2col in a chosen layout of the lowered tensor: layout SKC_LAYOUT_NCHW as above, or
+ * SKC_LAYOUT_PAIRS = the padded layout of a JIT (AUTO) 1x1 plan over it (pad 0):
+ * d_lowered[p][(c*R + r)*S + s][y][x][j] = lowered image 2p+j ([ceil(N/2)][C*R*S][Ho][Wo][2],
+ * zeros for a missing second image of an odd batch), so the compiled-weights kernel can run
+ * the lowered SpMDM without a separate re-layout pass.  Errors: as skc_im2col, SKC_ERR_ARG for
+ * another layout, SKC_ERR_ALIGN (PAIRS: pointers not 16-byte aligned). */
+skc_status skc_im2col_ex(const skc_plan *plan, const float *d_in_nchw, float *d_lowered, int N,
+                         int layout, void *stream);
+
 /* Row f1 -- the same convolution with a fused epilogue (the layout
  * function makes writing into another layout legitimate):
  *     d_out[n][k][y + out_pad][x + out_pad] = act(conv(n, k, y, x) + bias[k])

@@ -72,28 +72,58 @@ __global__ void __launch_bounds__(256) pad_kernel(const float *__restrict__ in,
 }
 
 // Row f3: lowering (im2col) for the comparison baseline.
-// L[n][(c*R + r)*S + s][y][x] = in[n][c][y*stride + r - pad][x*stride + s - pad] (0 outside):
-// one thread per lowered element, coalesced writes, per-image grid.y, 32-bit magic division.
+// L[n][(c*R + r)*S + s][y][x] = in[n][c][y*stride + r - pad][x*stride + s - pad] (0 outside).
+// HBM-bound (the R*S-fold replicated write stream).  One WARP per lowered row (unit, crs) at a
+// time, rows dealt warp-strided over a grid of whole waves: (c, r, s) and the row's source
+// base are warp-uniform, so a lane does one division per element (y = pix / Wo), each warp
+// store is a contiguous run, and a CTA does many rows (one CTA or one element per thread per
+// row made the pass CTA-launch bound: 0.43-1.2 ms for AlexNet conv2-5 at batch 256).
+// PAIRS: the image-pair interleaved layout of a JIT 1x1 plan (pad 0): out[p][crs][y][x][j] =
+// L[2p+j][crs][y][x], one float2 per element, zero for a missing second image of an odd N.
+template <bool PAIRS>
 __global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ in,
                                                      float *__restrict__ out, int C, int H,
                                                      int W, int R, int S, int stride, int pad,
-                                                     int Wo, uint32_t per_img, FastDiv div_howo,
-                                                     FastDiv div_wo, FastDiv div_rs,
-                                                     FastDiv div_s) {
-    const int64_t n = blockIdx.y;
-    const float *src = in + n * int64_t(C) * H * W;
-    float *dst = out + n * int64_t(per_img);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < per_img;
-         i += gridDim.x * blockDim.x) {
-        const uint32_t crs = fdiv(i, div_howo);
-        const uint32_t pix = i - crs * div_howo.d;
-        const uint32_t y = fdiv(pix, div_wo), x = pix - y * uint32_t(Wo);
-        const uint32_t c = fdiv(crs, div_rs), rs = crs - c * div_rs.d;
-        const uint32_t r = fdiv(rs, div_s), s = rs - r * uint32_t(S);
-        const int yi = int(y) * stride + int(r) - pad, xi = int(x) * stride + int(s) - pad;
-        float v = 0.0f;
-        if (yi >= 0 && yi < H && xi >= 0 && xi < W) v = __ldg(src + (int64_t(c) * H + yi) * W + xi);
-        dst[i] = v;
+                                                     int Wo, uint32_t howo, FastDiv div_wo,
+                                                     uint32_t CRS, uint64_t rows, int64_t N) {
+    constexpr int U = 4;  // elements per lane in flight
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const int64_t img = int64_t(C) * H * W;
+    const int RS = R * S;
+    for (uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < rows;
+         row += nwarps) {
+        const uint64_t unit = row / CRS;  // image (NCHW) or pair (PAIRS)
+        const int crs = int(row - unit * CRS);
+        const int c = crs / RS, rs = crs - c * RS;
+        const int r = rs / S, s = rs - r * S;
+        const float *src = in + int64_t(PAIRS ? 2 * unit : unit) * img + int64_t(c) * H * W;
+        const bool hb = PAIRS && int64_t(2 * unit + 1) < N;
+        const uint64_t base = row * howo;
+        for (uint32_t p0 = lane; p0 < howo; p0 += 32 * U) {
+            float2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t pix = p0 + 32 * u;
+                v[u] = make_float2(0.0f, 0.0f);
+                const uint32_t y = fdiv(pix, div_wo), x = pix - y * uint32_t(Wo);
+                const int yi = int(y) * stride + r - pad, xi = int(x) * stride + s - pad;
+                if (pix < howo && yi >= 0 && yi < H && xi >= 0 && xi < W) {
+                    const int64_t o = int64_t(yi) * W + xi;
+                    v[u].x = __ldg(src + o);
+                    if (hb) v[u].y = __ldg(src + img + o);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t pix = p0 + 32 * u;
+                if (pix >= howo) break;
+                if (PAIRS)
+                    reinterpret_cast<float2 *>(out)[base + pix] = v[u];
+                else
+                    out[base + pix] = v[u].x;
+            }
+        }
     }
 }
 
@@ -206,22 +236,41 @@ __global__ void __launch_bounds__(256) pad_pairs_flat_kernel(const float *__rest
 
 }  // namespace
 
+namespace {
+cudaError_t im2col_launch(bool pairs, const float *in, float *out, int64_t N, int C, int H, int W,
+                          int R, int S, int stride, int pad, int Ho, int Wo, cudaStream_t st) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0, v = 0;
+        nsm = (cudaGetDevice(&dev) == cudaSuccess &&
+               cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+                  ? v
+                  : 148;
+    }
+    const uint32_t howo = uint32_t(Ho) * uint32_t(Wo);
+    const uint32_t crs = uint32_t(C * R * S);
+    const uint64_t rows = uint64_t(pairs ? (N + 1) / 2 : N) * crs;
+    // whole waves: 8 CTAs of 8 warps per SM, fewer for a small pass
+    const uint64_t need = (rows + 7) / 8;
+    const unsigned grid = unsigned(need < uint64_t(nsm) * 8 ? need : uint64_t(nsm) * 8);
+    if (pairs)
+        im2col_kernel<true><<<grid, 256, 0, st>>>(in, out, C, H, W, R, S, stride, pad, Wo, howo,
+                                                  make_fastdiv(uint32_t(Wo)), crs, rows, N);
+    else
+        im2col_kernel<false><<<grid, 256, 0, st>>>(in, out, C, H, W, R, S, stride, pad, Wo, howo,
+                                                   make_fastdiv(uint32_t(Wo)), crs, rows, N);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
                           int S, int stride, int pad, int Ho, int Wo, cudaStream_t st) {
-    const uint32_t per_img = uint32_t(int64_t(C) * R * S * Ho * Wo);
-    int64_t bx = (int64_t(per_img) + 255) / 256;
-    bx = bx > 4096 ? 4096 : bx;
-    for (int64_t n0 = 0; n0 < N; n0 += 65535) {
-        const int64_t nn = (N - n0) < 65535 ? (N - n0) : 65535;
-        const dim3 grid{static_cast<unsigned>(bx), static_cast<unsigned>(nn), 1u};
-        im2col_kernel<<<grid, 256, 0, st>>>(in + n0 * int64_t(C) * H * W,
-                                            out + n0 * int64_t(per_img), C, H, W, R, S, stride,
-                                            pad, Wo, per_img, make_fastdiv(uint32_t(Ho * Wo)),
-                                            make_fastdiv(uint32_t(Wo)),
-                                            make_fastdiv(uint32_t(R * S)),
-                                            make_fastdiv(uint32_t(S)));
-    }
-    return cudaGetLastError();
+    return im2col_launch(false, in, out, N, C, H, W, R, S, stride, pad, Ho, Wo, st);
+}
+
+cudaError_t launch_im2col_pairs(const float *in, float *out, int64_t N, int C, int H, int W,
+                                int R, int S, int stride, int pad, int Ho, int Wo, cudaStream_t st) {
+    return im2col_launch(true, in, out, N, C, H, W, R, S, stride, pad, Ho, Wo, st);
 }
 
 namespace {

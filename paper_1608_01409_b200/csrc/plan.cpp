@@ -1255,18 +1255,30 @@ skc_status skc_pad_input(const skc_plan *p, const float *d_in, float *d_pad, int
     return ok();
 }
 
-skc_status skc_im2col(const skc_plan *p, const float *d_in, float *d_lowered, int N,
-                      void *stream) {
+skc_status skc_im2col_ex(const skc_plan *p, const float *d_in, float *d_lowered, int N,
+                         int layout, void *stream) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
+    if (layout != SKC_LAYOUT_NCHW && layout != SKC_LAYOUT_PAIRS)
+        return fail(SKC_ERR_ARG, "im2col layout %d: NCHW (0) or PAIRS (1)", layout);
+    if (layout == SKC_LAYOUT_PAIRS && (!aligned16(d_in) || !aligned16(d_lowered)))
+        return fail(SKC_ERR_ALIGN, "device pointers must be 16-byte aligned");
     if (N < 0) return fail(SKC_ERR_ARG, "N = %d < 0", N);
     if (N == 0) return ok();
     if (!d_in || !d_lowered) return fail(SKC_ERR_ARG, "NULL device pointer");
     if (int64_t(p->C) * p->R * p->S * p->Ho * p->Wo >= (int64_t(1) << 31))
         return fail(SKC_ERR_OVERFLOW, "lowered image does not fit int32 indexing");
-    cudaError_t e = launch_im2col(d_in, d_lowered, N, p->C, p->H, p->W, p->R, p->S, p->stride,
-                                  p->pad, p->Ho, p->Wo, (cudaStream_t)stream);
+    cudaError_t e = layout == SKC_LAYOUT_PAIRS
+                        ? launch_im2col_pairs(d_in, d_lowered, N, p->C, p->H, p->W, p->R, p->S,
+                                              p->stride, p->pad, p->Ho, p->Wo, (cudaStream_t)stream)
+                        : launch_im2col(d_in, d_lowered, N, p->C, p->H, p->W, p->R, p->S,
+                                        p->stride, p->pad, p->Ho, p->Wo, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "im2col launch: %s", cudaGetErrorString(e));
     return ok();
+}
+
+skc_status skc_im2col(const skc_plan *p, const float *d_in, float *d_lowered, int N,
+                      void *stream) {
+    return skc_im2col_ex(p, d_in, d_lowered, N, SKC_LAYOUT_NCHW, stream);
 }
 
 static skc_status forward_epi(const skc_plan *p, const float *d_in, float *d_out, int N,

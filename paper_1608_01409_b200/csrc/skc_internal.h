@@ -97,6 +97,8 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
                              int pad, cudaStream_t st);
 cudaError_t launch_im2col(const float *in, float *out, int64_t N, int C, int H, int W, int R,
                           int S, int stride, int pad, int Ho, int Wo, cudaStream_t st);
+cudaError_t launch_im2col_pairs(const float *in, float *out, int64_t N, int C, int H, int W, int R,
+                          int S, int stride, int pad, int Ho, int Wo, cudaStream_t st);
 cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_t st);
 // set the kernel's opt-in shared-memory attribute on the current device (skc_plan_upload), so
 // that launches need no attribute call (capture-safe from the first launch)

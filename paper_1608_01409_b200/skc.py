@@ -28,7 +28,7 @@ EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
-           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_pack_fc",
+           "skc_plan_verify", "skc_sparse_conv_forward_ex", "skc_im2col", "skc_im2col_ex", "skc_pack_fc",
            "skc_plan_compile", "skc_sparse_conv_forward_into", "skc_plan_tune",
            "skc_sm_topology", "skc_bench_ffma2", "skc_bench_lds64")
 
@@ -108,6 +108,7 @@ def lib():
             "skc_sparse_conv_forward_ex": [_P, _P, _P, _I, _P, _I, _I, _P],
             "skc_sparse_conv_forward_into": [_P, _P, _P, _P, _I, _P, _I, _P],
             "skc_im2col": [_P, _P, _P, _I, _P],
+            "skc_im2col_ex": [_P, _P, _P, _I, _I, _P],
             "skc_pack_fc": [_P, _I, _I, _I, _I, ctypes.POINTER(_P)],
             "skc_forward_host": [_P, _P, _P, _I, _P, _P, _P, _P],
             "skc_model_layer_cost": [_I] * 9 + [ctypes.c_int64, _I, ctypes.POINTER(skc_layer_cost)],
@@ -309,6 +310,13 @@ def skc_im2col(plan: Plan, d_in, d_lowered, N: int, stream=None):
     _check(lib().skc_im2col(plan.handle, _dptr(d_in), _dptr(d_lowered), int(N), _stream(stream)))
 
 
+def skc_im2col_ex(plan: Plan, d_in, d_lowered, N: int, layout: int, stream=None):
+    """f3: the lowered tensor in layout SKC_LAYOUT_NCHW or SKC_LAYOUT_PAIRS (the padded layout
+    of a JIT 1x1 plan over it)."""
+    _check(lib().skc_im2col_ex(plan.handle, _dptr(d_in), _dptr(d_lowered), int(N), int(layout),
+                               _stream(stream)))
+
+
 def skc_pack_fc(w: np.ndarray, batch: int, kernel: int = SKC_KERNEL_AUTO) -> Plan:
     """f2: pruned FC weights float32 [M, K] -> plan for Y[M x B] = W X[K x B] (B = batch)."""
     w = np.ascontiguousarray(w, dtype=np.float32)
@@ -337,8 +345,10 @@ class SparseLinear:
 
 
 class LoweredSparseConv2d:
-    """f3 baseline: im2col + CSR SpMDM (the direct kernel run as a 1x1 conv over the lowered
-    tensor).  Same weights, same nonzero order as SparseConv2d -> identical results."""
+    """f3 baseline: im2col + CSR SpMDM (a 1x1 conv over the lowered tensor, with the direct
+    kernel by default or the compiled-weights kernel with kernel=SKC_KERNEL_AUTO, whose
+    image-pair layout im2col then writes directly).  Same weights, same nonzero order as
+    SparseConv2d -> identical results."""
 
     def __init__(self, w: np.ndarray, H: int, W: int, stride=1, pad=0, groups=1,
                  kernel=SKC_KERNEL_DIRECT, device="cuda"):
@@ -349,7 +359,12 @@ class LoweredSparseConv2d:
         w1 = np.ascontiguousarray(w.reshape(K, Cg * R * S, 1, 1))
         self.conv = SparseConv2d.from_dense(w1, self.Ho, self.Wo, 1, 0, groups, kernel, device)
 
+    def _layout(self):
+        return SKC_LAYOUT_PAIRS if self.conv.geom["layout"] == SKC_LAYOUT_PAIRS else SKC_LAYOUT_NCHW
+
     def lowered_shape(self, N):
+        if self._layout() == SKC_LAYOUT_PAIRS:
+            return ((N + 1) // 2, self.CRS, self.Ho, self.Wo, 2)
         return (N, self.CRS, self.Ho, self.Wo)
 
     def forward(self, x, lowered=None, out=None, stream=None):
@@ -357,8 +372,8 @@ class LoweredSparseConv2d:
         N = x.shape[0]
         if lowered is None:
             lowered = torch.empty(self.lowered_shape(N), dtype=torch.float32, device=x.device)
-        skc_im2col(self.geom_plan, x, lowered, N, stream)
-        return self.conv.forward_padded(lowered, out, stream)
+        skc_im2col_ex(self.geom_plan, x, lowered, N, self._layout(), stream)
+        return self.conv.forward_padded(lowered, out, stream, N=N)
 
 
 def skc_forward_host(plan: Plan, h_in, h_out, N: int, d_in, d_pad, d_out, stream=None):

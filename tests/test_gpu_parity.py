@@ -421,6 +421,51 @@ def test_im2col_equals_unfold():
                                       ref.numpy().view(np.uint32))
 
 
+def test_im2col_pairs_equals_unfold():
+    """f3: the image-pair lowering equals torch.nn.functional.unfold interleaved by image
+    pairs, bitwise, with a zero second image for an odd batch."""
+    rng = np.random.default_rng(43)
+    for (N, C, H, W, R, st, p) in [(3, 3, 7, 9, 3, 1, 1), (2, 4, 27, 27, 5, 1, 2),
+                                   (5, 2, 11, 10, 3, 2, 0)]:
+        x = rng.standard_normal((N, C, H, W), dtype=np.float32)
+        plan = skc.skc_pack_csr(np.ones((1, C, R, R), np.float32), H, W, st, p, 1)
+        g = plan.info()
+        P = (N + 1) // 2
+        low = torch.full((P, C * R * R, g["Ho"], g["Wo"], 2), 7.0, device="cuda")
+        skc.skc_im2col_ex(plan, torch.from_numpy(x).cuda(), low, N, skc.SKC_LAYOUT_PAIRS)
+        torch.cuda.synchronize()
+        ref = torch.nn.functional.unfold(torch.from_numpy(x), R, padding=p, stride=st).numpy()
+        ref = ref.reshape(N, C * R * R, g["Ho"], g["Wo"])
+        if N % 2:
+            ref = np.concatenate([ref, np.zeros_like(ref[:1])])
+        ref = ref.reshape(P, 2, C * R * R, g["Ho"], g["Wo"]).transpose(0, 2, 3, 4, 1)
+        np.testing.assert_array_equal(low.cpu().numpy().view(np.uint32),
+                                      np.ascontiguousarray(ref).view(np.uint32))
+    with pytest.raises(skc.SkcError):
+        skc.skc_im2col_ex(plan, torch.from_numpy(x).cuda(), low, N, skc.SKC_LAYOUT_RAW)
+
+
+@pytest.mark.parametrize("N", [4, 5])
+def test_lowered_auto_equals_direct_auto(N):
+    """f3 with the compiled-weights kernel on both sides: im2col in the JIT plan's image-pair
+    layout + the 1x1 JIT SpMDM equals the direct JIT convolution bit for bit."""
+    rng = np.random.default_rng(44 + N)
+    K, C, H, W, R = 24, 12, 13, 13, 3
+    w = rng.standard_normal((K, C, R, R)).astype(np.float32)
+    w[rng.random(w.shape) < 0.8] = 0.0
+    x = rng.standard_normal((N, C, H, W), dtype=np.float32)
+    direct = skc.SparseConv2d.from_dense(w, H, W, 1, 1, 1, skc.SKC_KERNEL_AUTO)
+    low = skc.LoweredSparseConv2d(w, H, W, 1, 1, 1, kernel=skc.SKC_KERNEL_AUTO)
+    assert low.conv.geom["kernel"] == skc.SKC_KERNEL_JIT
+    xd = torch.from_numpy(x).cuda()
+    a = direct.forward(xd)
+    b = low.forward(xd)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(b.cpu().numpy().view(np.uint32), a.cpu().numpy().view(np.uint32))
+    ref, bound = oracle.conv2d_fp64(x, w, 1, 1, 1)
+    check(b.cpu().numpy(), ref, bound, "lowered auto")
+
+
 @pytest.mark.parametrize("li", [0, 1, 2, 3])
 def test_lowered_equals_direct(li):
     """f3: sparse conv WITH lowering (im2col + SpMDM) gives bit-for-bit the direct sparse
