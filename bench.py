@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "regtile", "jit"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time plain launches, no CUDA graph")
+    ap.add_argument("--pad-overlap", type=int, default=1, choices=[0, 1],
+                    help="graph step: run the pads of layers 2..L on a low-priority side stream, "
+                         "filling the previous conv's tail (the layers' inputs are independent)")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -382,17 +385,45 @@ def run_ours(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
+    def step_overlap(main, side):
+        # the conv launches stay in layer order on the high-priority main stream; the pad of
+        # layer i > 0 runs on the low-priority side stream (forked after layer 0's pad) and
+        # conv i waits for it.  Every conv kernel fills all SMs (1 CTA of 512 threads x 128
+        # registers per SM), so a pad's CTAs get SMs only as the running conv's CTAs retire:
+        # the HBM-bound pads fill the ALU-bound convs' tails instead of running between them.
+        # (layer order: the natural one measured best, profiles/r02_pad_overlap.txt)
+        seq = layers
+        skc.skc_pad_input(seq[0]["conv"].plan, seq[0]["x"], seq[0]["xp"], local_n, main)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        side.wait_event(fork)
+        ready = []
+        for d in seq[1:]:
+            skc.skc_pad_input(d["conv"].plan, d["x"], d["xp"], local_n, side)
+            e = torch.cuda.Event()
+            e.record(side)
+            ready.append(e)
+        for i, d in enumerate(seq):
+            if i > 0:
+                main.wait_event(ready[i - 1])
+            skc.skc_sparse_conv_forward(d["conv"].plan, d["xp"], d["out"], local_n, main)
+
     # the step's 8 launches captured once in a CUDA graph (replayed per timed step: no
     # host launch gaps between the kernels); per-layer times come from an uncaptured pass
     graph = None
     if not args.no_graph:
         try:
-            cap = torch.cuda.Stream(dev)
+            lo, hi = torch.cuda.Stream.priority_range()  # (lowest, greatest) priority
+            cap = torch.cuda.Stream(dev, priority=hi)
+            side = torch.cuda.Stream(dev, priority=lo)
             cap.wait_stream(stream)
             with torch.cuda.stream(cap):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=cap):
-                    step_on(cap)
+                    if args.pad_overlap and len(layers) > 1:
+                        step_overlap(cap, side)
+                    else:
+                        step_on(cap)
             torch.cuda.synchronize()
             g.replay()
             torch.cuda.synchronize()
@@ -667,7 +698,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "layers": [l.name for l in cfg.layers], "parallelism": par,
                    "l2": "flushed between timed steps (256 MiB write)", "kernel": args.kernel,
                    "step": "per layer: skc_pad_input + skc_sparse_conv_forward"
-                           + (", the step's 8 launches replayed as one CUDA graph" if graph is not None else "")},
+                           + (", the step's 8 launches replayed as one CUDA graph" if graph is not None else "")
+                           + ("; pads of layers 2..L on a low-priority side stream overlapping the previous conv"
+                              if graph is not None and args.pad_overlap and len(layers) > 1 else "")},
         "dense_equiv_gflops": step_dense_flops / (t_step * 1e-3) / 1e9,
         "per_gpu_gflops": local_nnz_flops / (t_local * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
