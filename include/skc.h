@@ -72,9 +72,14 @@ typedef enum {
     SKC_KERNEL_AUTO = 0,
     SKC_KERNEL_DIRECT = 1,   /* Fig. 2 statement per lane: one shared-memory read per MAC */
     SKC_KERNEL_REGTILE = 2,  /* register-tiled input window, per-nonzero dispatch        */
-    SKC_KERNEL_JIT = 3       /* "compiled weights": the CSR walk emitted as straight-line
+    SKC_KERNEL_JIT = 3,      /* "compiled weights": the CSR walk emitted as straight-line
                                 sm_100a code (immediate weights, register windows, packed
                                 FFMA2), compiled at plan time, see skc_plan_compile      */
+    SKC_KERNEL_SPMDM = 4     /* row f2: sparse x dense matrix product for FC layers and
+                                1x1 / stride 1 / pad 0 / one-group convs (plane % 4 == 0):
+                                X staged by TMA in chunks of rows, a lane owns 4-8 columns,
+                                the chunk's (offset, w) entries travel with it; AUTO picks it
+                                for skc_pack_fc plans                                    */
 } skc_kernel;
 
 /* Padded-input layouts (the method only needs a layout function f with
@@ -145,8 +150,12 @@ skc_status skc_pack_csr_ex(const float *w_host, int K, int C, int R, int S, int 
  * X[K x B] with W dense-pruned on the host (row-major [M][K]) and X, Y device row-major (the
  * batch is the fast axis -- SpMDM's dense operand).  This is exactly the 1x1 convolution of
  * one image with K channels of 1 x B pixels (the virtual dense matrix degenerates to X), so
- * the plan runs on the same kernels: skc_plan_upload, then
+ * the plan runs through the conv entry points: skc_plan_upload, then
  * skc_sparse_conv_forward(plan, X, Y, 1, stream) (X needs no padding; or _ex for bias+ReLU).
+ * kernel: SKC_KERNEL_AUTO picks SKC_KERNEL_SPMDM when B % 4 == 0, else the direct kernel;
+ * SKC_KERNEL_SPMDM with B % 4 != 0 is SKC_ERR_UNSUPPORTED.  SPMDM plans accept the fused
+ * epilogue (bias, ReLU, out_pad, the next plan's layout).  Every output element is
+ * accumulated by one thread in CSR order, so the SPMDM and direct kernels agree bit for bit.
  * The plan is specific to B.  Errors: as skc_pack_csr_ex. */
 skc_status skc_pack_fc(const float *w_host, int M, int K, int B, int kernel, skc_plan **out);
 

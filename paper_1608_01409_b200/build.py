@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include"),
           "-I", CSRC, "-I", BUILD]
-SOURCES = ["plan.cpp", "jit.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu", "topo.cu"]
+SOURCES = ["plan.cpp", "jit.cpp", "pad.cu", "sconv_direct.cu", "sconv_regtile.cu", "microbench.cu", "topo.cu", "spmdm.cu"]
 # the JIT kernel compiles and links its generated code in-process (no ptxas on PATH needed)
 CUDA_LIB = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
 # the PTX compiler is static (it only exists as an archive); nvJitLink is dlopen'ed at run time

@@ -83,6 +83,12 @@ struct skc_plan {
     size_t off_nz = 0, off_chunkptr = 0, off_perm = 0;
     size_t off_stream = 0, off_segoff = 0, off_chan = 0, off_lanemap = 0;
 
+    // SpMDM kernel (kernel == SKC_KERNEL_SPMDM, spmdm.cu): configuration, the params the
+    // launch fills in with workspace pointers, and the image offsets of its tables
+    SpmdmParams sp{};
+    int sp_LC = 0, sp_RWM = 0, sp_NW = 0;
+    size_t off_trow = 0, off_blk = 0, off_meta = 0;
+
     // "compiled weights" kernel (kernel == SKC_KERNEL_JIT, jit.cpp)
     JitPlan *jit = nullptr;
     // padded-input layout the plan's kernel reads (skc_pad_input writes it):
@@ -664,6 +670,142 @@ double direct_cost(const skc_plan *p) {
     return double(p->colidx.size()) * p->direct_waves / 0.80;
 }
 
+// ---- row f2: the SpMDM kernel's tables (spmdm.cu) ------------------------------------------
+constexpr int kSpmdmSMs = 148;                 // B200 SM count (grid sizing at pack time)
+constexpr int kSpmdmNW = 16;                   // warps per CTA
+constexpr size_t kSpmdmSmemMax = 227 << 10;    // opt-in shared memory per CTA
+constexpr size_t kSpmdmStageX = 64 << 10;      // X bytes per stage we aim for
+
+bool spmdm_eligible(const skc_plan *p) {
+    return p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && p->groups == 1 &&
+           (int64_t(p->Hp) * p->Wp) % 4 == 0;
+}
+
+// Tile configuration: LC columns per lane, RWM rows per warp, ntiles row tiles.  Cost model
+// in shared-memory wavefronts per CTA (the kernel's bound): per nonzero and warp, the X row
+// slice (min(BC, plane)/32 wavefronts) + 1 broadcast entry; per chunk row staged, the same
+// slice again (TMA writes into the stage); times the waves of CTAs over the SMs.  A column
+// block narrower than the plane needs one bulk copy per X row, which the producer issues
+// one at a time (~40 clk each, profiles/r02_fc_spmdm.txt): a chunk then costs at least
+// KC x 40 clk, which made LC = 4 blocks of a 256-wide batch copy-bound.
+struct SpmdmCfg {
+    int LC = 0, RWM = 0, ntiles = 0, ncb = 0;
+    double cost = 1e300;
+};
+
+SpmdmCfg spmdm_choose(const skc_plan *p) {
+    const int M = p->K, C = p->C, plane = p->Hp * p->Wp;
+    const double nnzr = double(p->colidx.size()) / M;
+    SpmdmCfg best;
+    for (int LC : {8, 4}) {
+        const int BC = 32 * LC;
+        const int ncb = (plane + BC - 1) / BC;
+        const double xw = double(std::min(BC, plane)) / 32.0;
+        for (int RWM : {4, 8}) {
+            const int min_t = (M + kSpmdmNW * RWM - 1) / (kSpmdmNW * RWM);
+            std::vector<int> cand{min_t};
+            for (int k = 1; k <= 8; ++k) cand.push_back((k * kSpmdmSMs + ncb - 1) / ncb);
+            const int KC = std::min<int>(C, int(std::max<size_t>(1, kSpmdmStageX /
+                                                 (size_t(ncb == 1 ? plane : BC) * 4))));
+            const int nch = (C + KC - 1) / KC;
+            for (int nt : cand) {
+                if (nt < min_t || nt > M) continue;
+                const int RT = (M + nt - 1) / nt;
+                const int waves = (nt * ncb + kSpmdmSMs - 1) / kSpmdmSMs;
+                const double chunk = std::max(RT * nnzr * KC / C * (xw + 1.0) + KC * xw,
+                                              ncb == 1 ? 0.0 : 40.0 * KC);
+                const double cost = waves * nch * chunk;
+                if (cost < best.cost * 0.999) best = SpmdmCfg{LC, RWM, nt, ncb, cost};
+            }
+        }
+    }
+    return best;
+}
+
+skc_status build_spmdm(skc_plan *p) {
+    const int M = p->K, C = p->C, plane = p->Hp * p->Wp;
+    const SpmdmCfg cfg = spmdm_choose(p);
+    const int LC = cfg.LC, nt = cfg.ntiles, ncb = cfg.ncb, BC = 32 * LC;
+    const uint32_t xpitch = uint32_t(ncb == 1 ? plane : BC) * 4u;
+    std::vector<int32_t> trow(size_t(nt) + 1);
+    for (int t = 0; t <= nt; ++t) trow[size_t(t)] = int32_t(int64_t(t) * M / nt);
+    int RTmax = 0;
+    for (int t = 0; t < nt; ++t) RTmax = std::max(RTmax, trow[size_t(t) + 1] - trow[size_t(t)]);
+    const uint32_t hbytes = uint32_t(align_up(size_t(RTmax + 1) * 4, 16));
+    int KC = int(std::max<size_t>(1, kSpmdmStageX / xpitch));
+    KC = std::min(KC, C);
+    for (;;) {
+        const int nch = (C + KC - 1) / KC;
+        // blocks: header (uint32 entry offsets per local row), entries (x offset, w bits)
+        std::vector<int64_t> blk(size_t(nt) * nch + 1, 0);
+        std::vector<uint8_t> meta;
+        size_t mstage = 16;
+        std::vector<int32_t> cur(static_cast<size_t>(M), 0);
+        for (int m = 0; m < M; ++m) cur[size_t(m)] = p->rowptr[size_t(m)];
+        for (int t = 0; t < nt; ++t)
+            for (int j = 0; j < nch; ++j) {
+                const size_t b0 = meta.size();
+                blk[size_t(t) * nch + j] = int64_t(b0);
+                meta.resize(b0 + hbytes, 0);
+                std::vector<uint32_t> hdr;
+                std::vector<uint32_t> ent;
+                const int kend = std::min(C, (j + 1) * KC);
+                for (int m = trow[size_t(t)]; m < trow[size_t(t) + 1]; ++m) {
+                    hdr.push_back(uint32_t(ent.size() / 2));
+                    int32_t &c = cur[size_t(m)];
+                    while (c < p->rowptr[size_t(m) + 1] && p->colidx[size_t(c)] / plane < kend) {
+                        const int k = p->colidx[size_t(c)] / plane;
+                        uint32_t wb;
+                        std::memcpy(&wb, &p->values[size_t(c)], 4);
+                        ent.push_back(uint32_t(k - j * KC) * xpitch);
+                        ent.push_back(wb);
+                        ++c;
+                    }
+                }
+                hdr.push_back(uint32_t(ent.size() / 2));
+                std::memcpy(meta.data() + b0, hdr.data(), hdr.size() * 4);
+                meta.resize(align_up(b0 + hbytes + ent.size() * 4, 16), 0);
+                if (!ent.empty()) std::memcpy(meta.data() + b0 + hbytes, ent.data(), ent.size() * 4);
+                mstage = std::max(mstage, meta.size() - b0);
+            }
+        blk[size_t(nt) * nch] = int64_t(meta.size());
+        for (int m = 0; m < M; ++m)
+            if (cur[size_t(m)] != p->rowptr[size_t(m) + 1])
+                return fail(SKC_ERR_STATE, "spmdm: row %d not fully packed", m);
+        const size_t xstage = align_up(size_t(KC) * xpitch, 128);
+        mstage = align_up(mstage, 128);
+        int NS = 0;
+        for (int ns : {3, 2})
+            if (128 + ns * (xstage + mstage) <= kSpmdmSmemMax) { NS = ns; break; }
+        if (NS == 0) {
+            if (KC == 1) return fail(SKC_ERR_UNSUPPORTED, "spmdm: a chunk does not fit shared memory");
+            KC = std::max(1, KC / 2);
+            continue;
+        }
+        // image: trow | blk | meta
+        p->off_trow = 0;
+        p->off_blk = align_up(trow.size() * 4, 16);
+        p->off_meta = align_up(p->off_blk + blk.size() * 8, 16);
+        p->image.assign(p->off_meta + meta.size(), 0);
+        std::memcpy(p->image.data() + p->off_trow, trow.data(), trow.size() * 4);
+        std::memcpy(p->image.data() + p->off_blk, blk.data(), blk.size() * 8);
+        std::memcpy(p->image.data() + p->off_meta, meta.data(), meta.size());
+        SpmdmParams &sp = p->sp;
+        sp = SpmdmParams{};
+        sp.K = M; sp.C = C; sp.H = p->H; sp.W = p->W; sp.plane = plane;
+        sp.KC = KC; sp.nch = nch; sp.NS = NS; sp.ntiles = nt; sp.ncb = ncb;
+        sp.xcontig = ncb == 1;
+        sp.xpitch = xpitch; sp.xstage = uint32_t(xstage); sp.mstage = uint32_t(mstage);
+        sp.hbytes = hbytes;
+        p->sp_LC = LC; p->sp_RWM = cfg.RWM; p->sp_NW = kSpmdmNW;
+        p->smem = 128 + NS * (xstage + mstage);
+        p->kernel = SKC_KERNEL_SPMDM;
+        p->layout = SKC_LAYOUT_NCHW;
+        (void)BC;
+        return SKC_OK;
+    }
+}
+
 bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
 }  // namespace
@@ -687,7 +829,7 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
                        int pad, int groups, int kernel, int max_ni, skc_plan **out) {
     if (!w || !out) return fail(SKC_ERR_ARG, "NULL weights or output pointer");
     *out = nullptr;
-    if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_JIT)
+    if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_SPMDM)
         return fail(SKC_ERR_ARG, "unknown kernel variant %d", kernel);
     skc_status st = check_geometry(K, C, R, S, H, W, stride, pad, groups);
     if (st != SKC_OK) return st;
@@ -749,6 +891,22 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
         });
     }
 
+    // row f2: the SpMDM kernel for FC plans (AUTO with max_ni == 1: skc_pack_fc) and on request
+    // for any eligible 1x1 plan
+    if (kernel == SKC_KERNEL_SPMDM || (kernel == SKC_KERNEL_AUTO && max_ni == 1 && spmdm_eligible(p))) {
+        if (!spmdm_eligible(p)) {
+            delete p;
+            return fail(SKC_ERR_UNSUPPORTED, "SPMDM needs a 1x1, stride-1, pad-0, one-group plan "
+                        "with H*W %% 4 == 0");
+        }
+        st = build_spmdm(p);
+        if (st != SKC_OK) {
+            delete p;
+            return st;
+        }
+        *out = p;
+        return ok();
+    }
     // kernel choice: the compiled-weights kernel when a configuration fits (AUTO; disabled
     // with SKC_NO_JIT=1); else the register-tiled kernel when an instantiated tile shape fits
     // and the cost model prefers it; the direct kernel otherwise (any stride, any R x S)
@@ -877,6 +1035,11 @@ skc_status skc_plan_info(const skc_plan *p, skc_info *info) {
     i.jit_sched = -1;
     i.jit_np = 0;
     i.jit_deal = 0;
+    if (p->kernel == SKC_KERNEL_SPMDM) {
+        i.band_rows = 0; i.chunk_channels = p->sp.KC; i.stages = p->sp.NS; i.warps = p->sp_NW;
+        i.channels_per_warp = p->sp_RWM; i.pixels_per_lane = p->sp_LC; i.lane_mapping = 0;
+        i.images_per_cta = 1;
+    }
     if (p->kernel == SKC_KERNEL_JIT) {
         JitInfo j{};
         jit_info(p->jit, &j);
@@ -947,6 +1110,61 @@ std::vector<NzKey> csr_keys(const skc_plan *p) {
 template <class T>
 const T *img_ptr(const skc_plan *p, size_t off) {
     return reinterpret_cast<const T *>(p->image.data() + off);
+}
+
+int sp_rows_max(const skc_plan *p) { return p->sp_NW * p->sp_RWM; }
+
+// SpMDM tables decoded back to the canonical CSR: tiles cover the rows once, each block's
+// header is monotone and its entries land inside the chunk's stage, and the (row, k, w) set in
+// per-row order is exactly the CSR's.
+skc_status verify_spmdm(const skc_plan *p) {
+    const SpmdmParams &sp = p->sp;
+    const int plane = sp.plane;
+    const int32_t *trow = img_ptr<int32_t>(p, p->off_trow);
+    const int64_t *blk = img_ptr<int64_t>(p, p->off_blk);
+    const uint8_t *meta = p->image.data() + p->off_meta;
+    const size_t meta_bytes = p->image.size() - p->off_meta;
+    if (trow[0] != 0 || trow[sp.ntiles] != p->K)
+        return fail(SKC_ERR_STATE, "verify: row tiles do not span [0, %d)", p->K);
+    std::vector<int32_t> nxt(p->rowptr.begin(), p->rowptr.end() - 1);  // next CSR entry per row
+    for (int t = 0; t < sp.ntiles; ++t) {
+        const int r0 = trow[t], rows = trow[t + 1] - r0;
+        if (rows < 0 || rows > sp_rows_max(p))
+            return fail(SKC_ERR_STATE, "verify: tile %d has %d rows", t, rows);
+        for (int j = 0; j < sp.nch; ++j) {
+            const int64_t b0 = blk[size_t(t) * sp.nch + j], b1 = blk[size_t(t) * sp.nch + j + 1];
+            if (b0 % 16 || b1 % 16 || b1 < b0 + sp.hbytes || size_t(b1) > meta_bytes ||
+                uint64_t(b1 - b0) > sp.mstage)
+                return fail(SKC_ERR_STATE, "verify: block (%d, %d) bounds", t, j);
+            const uint32_t *hdr = reinterpret_cast<const uint32_t *>(meta + b0);
+            const uint32_t *ent = reinterpret_cast<const uint32_t *>(meta + b0 + sp.hbytes);
+            const uint64_t nent = uint64_t(b1 - b0 - sp.hbytes) / 8;
+            const int kr = std::min(sp.KC, p->C - j * sp.KC);
+            if (hdr[0] != 0) return fail(SKC_ERR_STATE, "verify: block (%d, %d) header", t, j);
+            for (int lr = 0; lr < rows; ++lr) {
+                if (hdr[lr + 1] < hdr[lr] || hdr[lr + 1] > nent)
+                    return fail(SKC_ERR_STATE, "verify: block (%d, %d) row %d offsets", t, j, lr);
+                const int m = r0 + lr;
+                for (uint32_t i = hdr[lr]; i < hdr[lr + 1]; ++i) {
+                    const uint32_t xo = ent[2 * i], wb = ent[2 * i + 1];
+                    if (xo % sp.xpitch || xo / sp.xpitch >= uint32_t(kr))
+                        return fail(SKC_ERR_STATE, "verify: entry outside the chunk's stage");
+                    const int32_t c = nxt[size_t(m)]++;
+                    uint32_t vb;
+                    if (c >= p->rowptr[size_t(m) + 1])
+                        return fail(SKC_ERR_STATE, "verify: row %d has extra entries", m);
+                    std::memcpy(&vb, &p->values[size_t(c)], 4);
+                    if (int64_t(j) * sp.KC + xo / sp.xpitch != p->colidx[size_t(c)] / plane || wb != vb)
+                        return fail(SKC_ERR_STATE, "verify: row %d entry %d differs from the CSR", m,
+                                    int(c - p->rowptr[size_t(m)]));
+                }
+            }
+        }
+    }
+    for (int m = 0; m < p->K; ++m)
+        if (nxt[size_t(m)] != p->rowptr[size_t(m) + 1])
+            return fail(SKC_ERR_STATE, "verify: row %d misses entries", m);
+    return SKC_OK;
 }
 
 skc_status verify_direct(const skc_plan *p) {
@@ -1193,6 +1411,7 @@ skc_status skc_plan_verify(const skc_plan *p) {
     if (!p) return fail(SKC_ERR_ARG, "NULL plan");
     const skc_status st = p->kernel == SKC_KERNEL_JIT       ? verify_jit(p)
                           : p->kernel == SKC_KERNEL_REGTILE ? verify_regtile(p)
+                          : p->kernel == SKC_KERNEL_SPMDM   ? verify_spmdm(p)
                                                             : verify_direct(p);
     return st == SKC_OK ? ok() : st;
 }
@@ -1223,6 +1442,8 @@ skc_status skc_plan_upload(skc_plan *p, void *d_ws, size_t bytes, void *stream) 
         jit_set_vid(p->jit, !v.empty() && v.size() <= jit_vid_cap());
     } else if (p->kernel == SKC_KERNEL_REGTILE) {
         e = prepare_regtile(p->rsh);
+    } else if (p->kernel == SKC_KERNEL_SPMDM) {
+        e = prepare_spmdm(p->sp_LC, p->sp_RWM, p->smem);
     } else {
         e = prepare_direct(p->T, p->M);
     }
@@ -1323,6 +1544,19 @@ static skc_status forward_epi(const skc_plan *p, const float *d_in, float *d_out
         cudaError_t e = jit_launch(p->jit, d_in, d_out, ws, N, epi, (cudaStream_t)stream, &msg);
         if (e != cudaSuccess)
             return fail(SKC_ERR_CUDA, "JIT conv launch: %s %s", cudaGetErrorString(e), msg.c_str());
+        return ok();
+    }
+    if (p->kernel == SKC_KERNEL_SPMDM) {
+        if (N > 65535) return fail(SKC_ERR_ARG, "N = %d > 65535 for the SpMDM kernel", N);
+        SpmdmParams sp = p->sp;
+        sp.X = d_in;
+        sp.Y = d_out;
+        sp.meta = ws + p->off_meta;
+        sp.blk = reinterpret_cast<const int64_t *>(ws + p->off_blk);
+        sp.trow = reinterpret_cast<const int32_t *>(ws + p->off_trow);
+        sp.epi = epi;
+        cudaError_t e = launch_spmdm(sp, p->sp_LC, p->sp_RWM, p->sp_NW, N, p->smem, (cudaStream_t)stream);
+        if (e != cudaSuccess) return fail(SKC_ERR_CUDA, "spmdm launch: %s", cudaGetErrorString(e));
         return ok();
     }
     if (p->kernel == SKC_KERNEL_REGTILE) {

@@ -104,6 +104,25 @@ cudaError_t launch_direct(const DirectParams &p, int T, size_t smem, cudaStream_
 // that launches need no attribute call (capture-safe from the first launch)
 cudaError_t prepare_direct(int T, int M);
 bool direct_supported(int T, int M);
+// SpMDM kernel (spmdm.cu, row f2): 1x1 / stride 1 / pad 0 / one group, the plane's pixels as
+// the dense operand's columns.  Row tiles t own output rows [trow[t], trow[t+1]); the chunk j
+// block of tile t is meta[blk[t*nch + j] .. blk[t*nch + j + 1]): a header of per-row
+// entry offsets (uint32, hbytes, 16-aligned), then uint2 entries (x byte offset in the stage, w bits).
+struct SpmdmParams {
+    const float *X;        // [N][C][plane]
+    float *Y;              // [N][K][plane] (or the epilogue's layout)
+    const uint8_t *meta;   // workspace
+    const int64_t *blk;    // [ntiles*nch + 1] byte offsets into meta
+    const int32_t *trow;   // [ntiles + 1]
+    int K, C, H, W, plane;
+    int KC, nch, NS, ntiles, ncb;
+    int xcontig;           // 1: one column block spanning the plane (one copy per chunk)
+    uint32_t xpitch, xstage, mstage, hbytes;
+    Epilogue epi;
+};
+cudaError_t prepare_spmdm(int LC, int RWM, size_t smem);
+cudaError_t launch_spmdm(const SpmdmParams &p, int LC, int RWM, int NW, int N, size_t smem,
+                         cudaStream_t st);
 cudaError_t launch_regtile(const RegtileParams &p, const RegtileShape &sh, size_t smem,
                            cudaStream_t st);
 cudaError_t prepare_regtile(const RegtileShape &sh);

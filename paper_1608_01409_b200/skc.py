@@ -17,7 +17,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libskc.so")
 
-SKC_KERNEL_AUTO, SKC_KERNEL_DIRECT, SKC_KERNEL_REGTILE, SKC_KERNEL_JIT = 0, 1, 2, 3
+SKC_KERNEL_AUTO, SKC_KERNEL_DIRECT, SKC_KERNEL_REGTILE, SKC_KERNEL_JIT, SKC_KERNEL_SPMDM = 0, 1, 2, 3, 4
 SKC_LAYOUT_NCHW, SKC_LAYOUT_PAIRS, SKC_LAYOUT_RAW = 0, 1, 2
 STATUS = {0: "SKC_OK", -1: "SKC_ERR_ARG", -2: "SKC_ERR_GEOMETRY", -3: "SKC_ERR_NONFINITE",
           -4: "SKC_ERR_OVERFLOW", -5: "SKC_ERR_UNSUPPORTED", -6: "SKC_ERR_ALIGN",

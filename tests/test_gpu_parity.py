@@ -491,10 +491,13 @@ def test_sparse_fc_alexnet():
         w = wl.gen_fc_weights(i, L)
         x = wl.gen_fc_input(i, L, wl.FC_BATCH)
         fc = skc.SparseLinear(w, wl.FC_BATCH)
+        assert fc.plan.info()["kernel"] == skc.SKC_KERNEL_SPMDM
         skc.skc_plan_verify(fc.plan)
         y = fc.forward(torch.from_numpy(x).cuda())
         torch.cuda.synchronize()
         yo = y.cpu().numpy()
+        yd, _ = _fc_run(w, x, skc.SKC_KERNEL_DIRECT)
+        np.testing.assert_array_equal(yo.view(np.uint32), yd.view(np.uint32))
         ref = w.astype(np.float64) @ x.astype(np.float64)
         bound = np.abs(w).astype(np.float64) @ np.abs(x).astype(np.float64)
         check(yo, ref, bound, f"fc {L.name}")
@@ -510,6 +513,75 @@ def test_sparse_fc_small_vs_oracle():
         y = fc.forward(torch.from_numpy(x).cuda()).cpu().numpy()
         ref, bound = oracle.conv2d_fp64(x.reshape(1, K, 1, B), w.reshape(M, K, 1, 1))
         check(y.reshape(1, M, 1, B), ref, bound, f"fc {M}x{K}x{B}")
+
+
+def _fc_run(w, x, kernel, bias=None, relu=False, out_pad=0):
+    M, K = w.shape
+    B = x.shape[1]
+    p = skc.skc_pack_fc(w, B, kernel)
+    p.upload("cuda")
+    skc.skc_plan_verify(p)
+    shape = (M, B) if out_pad == 0 else (M, 1 + 2 * out_pad, B + 2 * out_pad)
+    y = torch.full(shape, -7.0, device="cuda")
+    b = torch.from_numpy(bias).cuda() if bias is not None else None
+    skc.skc_sparse_conv_forward_ex(p, torch.from_numpy(x).cuda(), y, 1, b, relu, out_pad)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), p.info()
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 4), (7, 13, 8), (65, 100, 132), (300, 257, 256),
+                                   (1000, 4096, 256), (33, 700, 12), (129, 2000, 260)])
+def test_spmdm_equals_direct_bitwise(shape):
+    """f2: the SpMDM kernel (several row tiles, column blocks with a ragged last one, K over
+    several chunks) gives bit for bit the direct kernel's result on the same FC plan, and
+    passes the oracle bar (numpy float64 matmul)."""
+    M, K, B = shape
+    rng = np.random.default_rng(M + K + B)
+    w = np.where(rng.random((M, K)) < 0.1, rng.standard_normal((M, K)), 0).astype(np.float32)
+    w[M // 2] = 0  # an empty row
+    x = rng.standard_normal((K, B)).astype(np.float32)
+    ys, gi = _fc_run(w, x, skc.SKC_KERNEL_SPMDM)
+    yd, gd = _fc_run(w, x, skc.SKC_KERNEL_DIRECT)
+    assert gi["kernel"] == skc.SKC_KERNEL_SPMDM and gd["kernel"] == skc.SKC_KERNEL_DIRECT
+    np.testing.assert_array_equal(ys.view(np.uint32), yd.view(np.uint32))
+    ref = w.astype(np.float64) @ x.astype(np.float64)
+    bound = np.abs(w).astype(np.float64) @ np.abs(x).astype(np.float64)
+    check(ys, ref, bound, f"spmdm {shape}")
+
+
+@pytest.mark.parametrize("out_pad", [0, 2])
+def test_spmdm_epilogue_equals_direct(out_pad):
+    """f2 + a6: bias, ReLU and a padded output (the general store path) bitwise as the
+    direct kernel's epilogue; the halo is left untouched."""
+    rng = np.random.default_rng(61 + out_pad)
+    M, K, B = 90, 300, 136
+    w = np.where(rng.random((M, K)) < 0.15, rng.standard_normal((M, K)), 0).astype(np.float32)
+    x = rng.standard_normal((K, B)).astype(np.float32)
+    bias = rng.standard_normal(M).astype(np.float32)
+    ys, _ = _fc_run(w, x, skc.SKC_KERNEL_SPMDM, bias, True, out_pad)
+    yd, _ = _fc_run(w, x, skc.SKC_KERNEL_DIRECT, bias, True, out_pad)
+    np.testing.assert_array_equal(ys.view(np.uint32), yd.view(np.uint32))
+    inner = ys if out_pad == 0 else ys[:, out_pad, out_pad:out_pad + B]
+    ref = np.maximum(w.astype(np.float64) @ x.astype(np.float64) + bias[:, None], 0)
+    assert np.allclose(inner, ref, rtol=1e-4, atol=1e-4)
+    if out_pad:
+        halo = ys.copy()
+        halo[:, out_pad, out_pad:out_pad + B] = -7.0
+        assert np.all(halo == -7.0)
+
+
+def test_spmdm_1x1_conv_images():
+    """The SpMDM kernel on a 1x1 conv plan with several images (grid z) = the direct kernel."""
+    rng = np.random.default_rng(62)
+    w = np.where(rng.random((48, 40, 1, 1)) < 0.25, rng.standard_normal((48, 40, 1, 1)), 0).astype(np.float32)
+    x = rng.standard_normal((3, 40, 14, 14)).astype(np.float32)
+    L = type("L", (), dict(H=14, W=14, stride=1, pad=0, groups=1))
+    a, ca = run_gpu(w, x, L, skc.SKC_KERNEL_SPMDM)
+    b, _ = run_gpu(w, x, L, skc.SKC_KERNEL_DIRECT)
+    assert ca.geom["kernel"] == skc.SKC_KERNEL_SPMDM
+    np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+    ref, bound = oracle.conv2d_fp64(x, w)
+    check(a, ref, bound, "spmdm 1x1 conv")
 
 
 @pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
