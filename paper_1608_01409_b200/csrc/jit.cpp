@@ -323,10 +323,7 @@ int window_regs(int TY, int TX, int PX, int R, int S, int st, bool pairmode) {
 // Register cap per thread for NW warps on one SM: warps are spread over the 4 SM
 // sub-partitions, each with a 16K-register file, so ceil(NW/4) * regs * 32 <= 16384.
 int reg_cap(int NW) {
-    int per = 16384 / (32 * ((NW + 3) / 4));
-    // SKC_JIT_REGCAP: a lower cap, leaving registers for a co-resident CTA of another kernel
-    // (the overlapped pad pass; experiment, profiles/r02_pad_coresident.txt)
-    if (const char *e = std::getenv("SKC_JIT_REGCAP")) per = std::min(per, std::max(32, std::atoi(e)));
+    const int per = 16384 / (32 * ((NW + 3) / 4));
     return per >= 256 ? 255 : (per & ~7);
 }
 

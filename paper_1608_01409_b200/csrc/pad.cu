@@ -132,8 +132,7 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float *__restrict__ i
 // f(c, y+r, x+s) = f(c, y, x) + f(0, r, s) per image): out[p][c][y][x][j] = in[2p+j][c][y-pad]
 // [x-pad], zero in the halo and for a missing second image.  grid.y = pair; each thread
 // writes two consecutive (A, B) elements as one float4.
-template <int TPB>
-__global__ void __launch_bounds__(TPB, TPB == 128 ? 16 : 1) pad_pairs_kernel(const float *__restrict__ in,
+__global__ void __launch_bounds__(256) pad_pairs_kernel(const float *__restrict__ in,
                                                         float *__restrict__ out, int C, int H,
                                                         int W, int pad, int Wp, uint32_t per_img,
                                                         FastDiv div_plane, FastDiv div_wp,
@@ -348,14 +347,7 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
-    // SKC_PAD_CTA=128: CTAs of 128 threads x <= 32 registers (4096 registers), small enough to
-    // run beside a conv kernel whose register cap leaves that much (SKC_JIT_REGCAP=120)
-    static const bool small = [] {
-        const char *e = std::getenv("SKC_PAD_CTA");
-        return e && std::atoi(e) == 128;
-    }();
-    const int tpb = small ? 128 : threads;
-    int64_t bx = (int64_t(per_img) + tpb * 8 - 1) / (tpb * 8);
+    int64_t bx = (int64_t(per_img) + threads * 8 - 1) / (threads * 8);
     bx = bx > 4096 ? 4096 : bx;
     for (int64_t p0 = 0; p0 < P; p0 += 65535) {
         const int64_t np = (P - p0) < 65535 ? (P - p0) : 65535;
@@ -363,8 +355,7 @@ cudaError_t launch_pad_pairs(const float *in, float *out, int64_t N, int C, int 
         // last pair: the kernel checks p + 1 < gridDim.y)
         const int has_b = (p0 + np < P) || (N % 2 == 0);
         const dim3 grid{static_cast<unsigned>(bx), static_cast<unsigned>(np), 1u};
-        cudaError_t e = pdl_launch(small ? pad_pairs_kernel<128> : pad_pairs_kernel<256>, grid,
-                                   dim3(small ? 128 : threads), st,
+        cudaError_t e = pdl_launch(pad_pairs_kernel, grid, dim3(threads), st,
                                    in + 2 * p0 * int64_t(C) * H * W,
                                    out + 2 * p0 * int64_t(per_img), C, H, W, pad, Wp, per_img,
                                    make_fastdiv(uint32_t(Hp * Wp)), make_fastdiv(uint32_t(Wp)),
