@@ -774,9 +774,12 @@ skc_status build_spmdm(skc_plan *p) {
                 return fail(SKC_ERR_STATE, "spmdm: row %d not fully packed", m);
         const size_t xstage = align_up(size_t(KC) * xpitch, 128);
         mstage = align_up(mstage, 128);
+        // + 512 B of slack after the last stage: a lane's second column group (LC = 8) may read
+        // up to 512 B past the last staged row when the plane is narrower than 256 columns
+        // (those values are never stored)
         int NS = 0;
         for (int ns : {3, 2})
-            if (128 + ns * (xstage + mstage) <= kSpmdmSmemMax) { NS = ns; break; }
+            if (128 + ns * (xstage + mstage) + 512 <= kSpmdmSmemMax) { NS = ns; break; }
         if (NS == 0) {
             if (KC == 1) return fail(SKC_ERR_UNSUPPORTED, "spmdm: a chunk does not fit shared memory");
             KC = std::max(1, KC / 2);
@@ -798,7 +801,7 @@ skc_status build_spmdm(skc_plan *p) {
         sp.xpitch = xpitch; sp.xstage = uint32_t(xstage); sp.mstage = uint32_t(mstage);
         sp.hbytes = hbytes;
         p->sp_LC = LC; p->sp_RWM = cfg.RWM; p->sp_NW = kSpmdmNW;
-        p->smem = 128 + NS * (xstage + mstage);
+        p->smem = 128 + NS * (xstage + mstage) + 512;
         p->kernel = SKC_KERNEL_SPMDM;
         p->layout = SKC_LAYOUT_NCHW;
         (void)BC;
