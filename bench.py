@@ -166,6 +166,16 @@ def load_traffic():
     return None
 
 
+def load_layer_roofs():
+    """Per-layer binding roof (FP32 pipe vs shared-memory crossbar incl. the TMA stage writes)
+    from the committed ncu captures (profiles/r02_layer_roofs.json, tools/layer_roofs.py)."""
+    path = os.path.join(ROOT, "profiles", "r02_layer_roofs.json")
+    try:
+        return {d["layer"]: d for d in json.load(open(path))["layers"]}
+    except (OSError, ValueError, KeyError):
+        return {}
+
+
 # ----------------------------------------------------------------------------- oracle legs
 def oracle_sample(cfg, budget_s):
     """Time the oracle (as it stands) on a bounded sample: whole images of every layer,
@@ -648,6 +658,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     if traffic and traffic.get("kernel") == args.kernel and cfg.cfg_id in traffic.get("configs", []):
         tr = traffic.get("dram_bytes_per_launch", {}).get(dl["L"].name)
     peak_meas = peaks["ffma2_tflops"] if peaks else None
+    # the binding roof of each layer's kernel, from its committed ncu capture (config 2, AUTO):
+    # roof cycles = max(FFMA2 / 2, LDS wavefronts + TMA bytes / 128) per SM, rescaled from the
+    # capture's SM clock to this run's
+    roofs = load_layer_roofs() if (cfg.cfg_id in (2, 5) and args.kernel == "auto") else {}
     per_layer = []
     for d, cm, pm in zip(layers, conv_ms, pad_ms):
         L = d["L"]
@@ -659,6 +673,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             "frac_fp32_measured": ach / peak_meas if peak_meas else None,
             "pad_gbs": local_n * 4 * (L.C * L.H * L.W + L.C * (L.H + 2 * L.pad) * (L.W + 2 * L.pad)) / (pm * 1e-3) / 1e9,
             "dram_bytes_per_launch_ncu": (traffic or {}).get("dram_bytes_per_launch", {}).get(L.name),
+            "binding_roof": (lambda r: None if r is None else {
+                "resource": r["binding"],
+                "roof_tflops": r["roof_tflops"] * (f_max / 1e9) / r["sm_clock_ghz"],
+                "frac": ach / (r["roof_tflops"] * (f_max / 1e9) / r["sm_clock_ghz"]),
+                "source": "profiles/r02_layer_roofs.json (" + r["source"] + ")"})(roofs.get(L.name)),
             "kernel_cfg": {k: d["conv"].plan.info()[k] for k in (
                 "kernel", "band_rows", "chunk_channels", "stages", "warps", "channels_per_warp",
                 "pixels_per_lane", "smem_bytes", "tile_h", "tile_w", "images_per_cta",
