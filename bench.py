@@ -347,7 +347,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     # plan build (pack + JIT compile + upload): one-off, untimed; the JIT
     # compiles of the layers run concurrently (host threads; ctypes releases the GIL)
     ws = [wl.gen_weights(cfg.cfg_id, li, L) for li, L in enumerate(cfg.layers)]
-    plans = [skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, kernel)
+    # each plan configured for the images one forward call of this rank processes
+    plans = [skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, kernel, batch_hint=local_n)
              for w, L in zip(ws, cfg.layers)]
     import concurrent.futures as cf
     # N ranks of one node: local rank 0 compiles first and fills the on-disk JIT cache, the
@@ -672,7 +673,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             "conv_nnz_tflops": ach, "frac_fp32_nominal": ach / peak_fp32,
             "frac_fp32_measured": ach / peak_meas if peak_meas else None,
             "pad_gbs": local_n * 4 * (L.C * L.H * L.W + L.C * (L.H + 2 * L.pad) * (L.W + 2 * L.pad)) / (pm * 1e-3) / 1e9,
-            "dram_bytes_per_launch_ncu": (traffic or {}).get("dram_bytes_per_launch", {}).get(L.name),
+            "dram_bytes_per_launch_ncu": (traffic or {}).get("dram_bytes_per_launch", {}).get(L.name)
+            if (traffic and traffic.get("kernel") == args.kernel and cfg.cfg_id in traffic.get("configs", [])) else None,
             "binding_roof": (lambda r: None if r is None else {
                 "resource": r["binding"],
                 "roof_tflops": r["roof_tflops"] * (f_max / 1e9) / r["sm_clock_ghz"],

@@ -2062,7 +2062,7 @@ void choose_blocks(JitPlan &jp, int n_hint) {
 }
 }  // namespace
 
-int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *msg) {
+int jit_configure(const JitInput &in, int max_ni, int batch_hint, JitPlan **out, std::string *msg) {
     *out = nullptr;
     const int plane = in.Hp * in.Wp;
     // TMA bulk copies of whole channel runs need 16-byte aligned sources and sizes: a run of
@@ -2100,8 +2100,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
     double code_cap = 3.0e6;  // warp-instructions of all blocks' code (SKC_JIT_MAX_CODE)
     if (const char *e = std::getenv("SKC_JIT_MAX_CODE")) code_cap = std::atof(e);
     std::vector<int> nw_opts = {16, 12, 20, 24, 8};  // likely winners first (pruning)
-    int n_hint = 256;  // batch the configuration is tuned for (SKC_JIT_NHINT)
-    if (const char *e = std::getenv("SKC_JIT_NHINT")) n_hint = std::max(1, std::atoi(e));
+    const int n_hint = std::max(1, batch_hint);  // batch the configuration is tuned for
     const int64_t nnz_total = in.rowptr[in.K];
     if (nw_force) nw_opts = {nw_force};
     bool any_aligned = false;
@@ -2136,7 +2135,8 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     if (band_force > 0 && NB != band_force) continue;
                     const int tpi = ((ty_n + NB - 1) / NB) * tx_n;  // tiles of the largest band
                     if (NB > 1 && ty_n * tx_n <= lanes_max) break;  // a whole slot fits already
-                    int NSL = std::min(max_ni / sw, lanes_max / tpi);  // slots per CTA item
+                    // slots per CTA item (no more images per item than the batch has)
+                    int NSL = std::min({max_ni / sw, lanes_max / tpi, (n_hint + sw - 1) / sw});
                     if (NSL < 1) continue;
                     int CB = 0, NS = 0, IS = 0, stage = 0;
                     size_t smem = 0;
@@ -2169,7 +2169,7 @@ int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *ms
                     if (xb > 0 && (in.Kg + M - 1) / M != nbg) continue;  // no real extra block
                     // distinct blocks running at once for a batch of n_hint images (an item
                     // covers NI images x 1/NB of their pixels: NIe image-equivalents)
-                    const double NIe = double(NI) / NB;
+                    const double NIe = double(std::min(NI, n_hint)) / NB;  // real images only
                     const int nig = (n_hint + NI - 1) / NI * NB;
                     const int conc = std::max(1, (kSMs + nig - 1) / nig);
                     const double share = std::max(kFetchInv, NW / kIssue) / NIe * conc_penalty(conc);
@@ -2431,60 +2431,66 @@ int jit_compile(JitPlan *jp, std::string *msg) {
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return SKC_OK;
     }
-    // compile modules in parallel
-    std::vector<std::vector<char>> objs(mods.size());
-    std::vector<std::string> errs(mods.size());
-    std::atomic<size_t> next{0};
-    std::atomic<bool> bad{false};
-    unsigned nth = std::max(1u, std::thread::hardware_concurrency());
-    if (const char *e = std::getenv("SKC_JIT_THREADS")) nth = unsigned(std::max(1, std::atoi(e)));
-    nth = std::min<unsigned>(nth, unsigned(mods.size()));
-    // biggest modules first
-    std::vector<size_t> order(mods.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
-    std::sort(order.begin(), order.end(),
-              [&](size_t a, size_t b) { return mods[a].size() > mods[b].size(); });
-    auto work = [&]() {
-        for (;;) {
-            const size_t i = next.fetch_add(1);
-            if (i >= order.size() || bad.load()) return;
-            const size_t m = order[i];
-            if (!compile_ptx(mods[m], opt, jp->maxreg, objs[m], &errs[m])) bad.store(true);
-            std::string().swap(mods[m]);  // free the text early
-        }
-    };
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work);
-    work();
-    for (auto &t : pool) t.join();
-    for (const auto &e : errs)
-        if (!e.empty()) {
-            *msg = e;
-            return SKC_ERR_UNSUPPORTED;
-        }
-    // link
+    // compile modules in parallel, then link; if the link runs out of the constant bank for
+    // optimizer-generated constants (many small blocks: configurations for small batches),
+    // compile again with ptxas --disable-optimizer-constants, as the linker asks
     const JitLinkApi &jl = jitlink();
     nvJitLinkHandle lh = nullptr;
-    const char *lopts[] = {"-arch=sm_100a"};
-    if (!jl.ok || jl.create(&lh, 1, lopts) != NVJITLINK_SUCCESS) {
-        *msg = jl.ok ? "nvJitLinkCreate failed" : "nvJitLink not found (set SKC_NVJITLINK)";
-        return SKC_ERR_UNSUPPORTED;
-    }
-    nvJitLinkResult lr = NVJITLINK_SUCCESS;
-    for (size_t i = 0; i < objs.size() && lr == NVJITLINK_SUCCESS; ++i) {
-        const std::string name = "m" + std::to_string(i);
-        lr = jl.add_data(lh, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(), name.c_str());
-    }
-    if (lr == NVJITLINK_SUCCESS) lr = jl.complete(lh);
-    if (lr != NVJITLINK_SUCCESS) {
+    const std::string opt2 = std::string(opt) + " --disable-optimizer-constants";
+    for (int attempt = 0;; ++attempt) {
+        const char *o_used = attempt ? opt2.c_str() : opt;
+        std::vector<std::vector<char>> objs(mods.size());
+        std::vector<std::string> errs(mods.size());
+        std::atomic<size_t> next{0};
+        std::atomic<bool> bad{false};
+        unsigned nth = std::max(1u, std::thread::hardware_concurrency());
+        if (const char *e = std::getenv("SKC_JIT_THREADS")) nth = unsigned(std::max(1, std::atoi(e)));
+        nth = std::min<unsigned>(nth, unsigned(mods.size()));
+        // biggest modules first
+        std::vector<size_t> order(mods.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+        std::sort(order.begin(), order.end(),
+                  [&](size_t a, size_t b) { return mods[a].size() > mods[b].size(); });
+        auto work = [&]() {
+            for (;;) {
+                const size_t i = next.fetch_add(1);
+                if (i >= order.size() || bad.load()) return;
+                const size_t m = order[i];
+                if (!compile_ptx(mods[m], o_used, jp->maxreg, objs[m], &errs[m])) bad.store(true);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work);
+        work();
+        for (auto &t : pool) t.join();
+        for (const auto &e : errs)
+            if (!e.empty()) {
+                *msg = e;
+                return SKC_ERR_UNSUPPORTED;
+            }
+        // link
+        const char *lopts[] = {"-arch=sm_100a"};
+        if (!jl.ok || jl.create(&lh, 1, lopts) != NVJITLINK_SUCCESS) {
+            *msg = jl.ok ? "nvJitLinkCreate failed" : "nvJitLink not found (set SKC_NVJITLINK)";
+            return SKC_ERR_UNSUPPORTED;
+        }
+        nvJitLinkResult lr = NVJITLINK_SUCCESS;
+        for (size_t i = 0; i < objs.size() && lr == NVJITLINK_SUCCESS; ++i) {
+            const std::string name = "m" + std::to_string(i);
+            lr = jl.add_data(lh, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(), name.c_str());
+        }
+        if (lr == NVJITLINK_SUCCESS) lr = jl.complete(lh);
+        if (lr == NVJITLINK_SUCCESS) break;
         size_t n = 0;
         jl.log_size(lh, &n);
         std::string log(n, '\0');
         if (n) jl.log(lh, &log[0]);
         jl.destroy(&lh);
+        if (attempt == 0 && log.find("disable-optimizer-constants") != std::string::npos) continue;
         *msg = "nvJitLink failed (" + std::to_string(int(lr)) + "): " + log.substr(0, 800);
         return SKC_ERR_UNSUPPORTED;
     }
+    std::vector<std::string>().swap(mods);
     size_t n = 0;
     jl.cubin_size(lh, &n);
     jp->cubin.resize(n);

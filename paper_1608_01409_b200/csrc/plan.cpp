@@ -72,6 +72,7 @@ struct skc_plan {
     DirectParams dp{};
     double direct_waves = 0;  // smem wavefronts per nonzero per image (all bands)
     int max_ni = 4;           // images per CTA the direct kernel may stage (FC: 1)
+    int batch_hint = 256;     // images per launch the configuration is chosen for
     size_t smem = 0;
 
     // register-tiled kernel configuration (kernel == SKC_KERNEL_REGTILE)
@@ -107,6 +108,9 @@ namespace {
 
 constexpr int kDirectNW = 8;              // compute warps per CTA (+1 producer warp)
 constexpr size_t kStageTarget = 24 << 10;  // bytes per stage we aim for
+constexpr int kDirectSmallBatch = 16;      // batch hints below this: launch-time config model
+constexpr int kAutoJitMinBatch = 8;        // AUTO: compiled-weights kernel from this batch up
+constexpr int kDirectStages = 4;           // stages of the direct kernel's ring (sconv_direct.cu)
 constexpr size_t kSmemBudget = 112 << 10;  // per CTA, so that >= 2 CTAs fit an SM
 
 skc_status check_geometry(int K, int C, int R, int S, int H, int W, int stride, int pad,
@@ -184,7 +188,20 @@ skc_status configure_direct(skc_plan *p) {
     double best_cost = 1e300;
     const char *nb_env = std::getenv("SKC_DIRECT_BANDS");
     const int nb_force = nb_env ? std::atoi(nb_env) : 0;
+    // Small batches (batch_hint < kDirectSmallBatch): the per-image cost below ignores how
+    // many CTAs a launch has, and a batch-1 launch of a 256-image configuration runs a few
+    // dozen CTAs on 148 SMs.  There the candidates (band height, images per CTA, channels per
+    // warp M) are ranked by a launch-time model instead: CTAs = groups x channel blocks x
+    // bands x image groups in waves of 148 x (CTAs per SM by shared memory, at most 2); a
+    // CTA is latency-bound -- each warp walks its channels' nonzeros one after another at
+    // ~110 cycles each whatever the pixel slots T (B200, conv3 at batch 1-2:
+    // profiles/r02_small_batch.txt) -- plus its staged input and {w, off} stream at ~64 B/clk
+    // from L2, ~2000 cycles of setup, and a small charge per row band (more bands measured
+    // slower at equal waves).
+    const bool small = p->batch_hint < kDirectSmallBatch;
+    int best_M = 0;
     for (int NI = 1; NI <= p->max_ni; NI *= 2) {
+        if (small && NI > 1 && NI / 2 >= p->batch_hint) break;  // no empty image slots
         for (int nb = 1; nb <= Ho; ++nb) {
             if (nb_force > 0 && nb != std::min(nb_force, Ho)) continue;
             const int BH = (Ho + nb - 1) / nb;
@@ -205,12 +222,39 @@ skc_status configure_direct(skc_plan *p) {
                     T = std::max(T, band_slots(NI, IS, std::min(BH, Ho - b * BH), Wo, p->Wp,
                                                p->stride, nullptr));
                 if (T > 16) continue;
+                const bool bulk_ok = bulk_legal(p, NI, BH, BHin, nb, whole, CB, chan_stride, IS);
+                const int M0 = T <= 8 ? 4 : 2;
+                if (small) {
+                    const size_t smem_est = size_t(kDirectStages) * (size_t(IS) * NI * 4 + 4096);
+                    const int per_sm = std::max(1, int((227u << 10) / std::max<size_t>(1, smem_est)));
+                    // co-resident CTAs of these latency-bound launches slow each other about
+                    // as much as a second wave would: count waves of 148
+                    (void)per_sm;
+                    const double P = 148.0;
+                    const double nig = std::ceil(double(p->batch_hint) / NI);
+                    for (int M = M0; M >= 1; M /= 2) {
+                        const double blocks = std::ceil(double(p->Kg) / (kDirectNW * M)) * p->groups;
+                        const double ctas = blocks * nb * nig;
+                        const double nz_cta = double(p->colidx.size()) / blocks;
+                        const double staged = double(BHin) * p->Wp * p->Cg * NI * 4.0;
+                        const double copy = (bulk_ok ? staged / 64.0 : staged / 4.0 / 32.0 * 8.0) +
+                                            nz_cta * 8.0 / 64.0;
+                        const double walk = nz_cta / kDirectNW * 110.0;
+                        const double cost = std::ceil(ctas / P) * (walk + copy + 2000.0) + 500.0 * nb;
+                        if (cost < best_cost) {
+                            best_cost = cost; best_M = M;
+                            g.NI = NI; g.BH = BH; g.nbands = nb; g.BHin = BHin; g.whole = whole;
+                            g.CB = CB; g.chan_stride = chan_stride; g.img_stride = IS; p->T = T;
+                        }
+                    }
+                    continue;
+                }
                 // per nonzero and image: T loads + 1 broadcast per band (wavefront-cycles)
                 double cost = double(nb) * (T + 1) / NI + 1e-3 * NI + 1e-4 * nb;
-                if (!bulk_legal(p, NI, BH, BHin, nb, whole, CB, chan_stride, IS)) {
+                if (!bulk_ok) {
                     // cp.async fallback: ~8 cycles per 32 staged words, repeated by every
                     // channel block; expressed per nonzero of the layer
-                    const int M = T <= 8 ? 4 : 2;
+                    const int M = M0;
                     const double blocks = std::ceil(double(p->Kg) / (kDirectNW * M)) * p->groups;
                     const double words = double(nb) * BHin * p->Wp * p->C * blocks;
                     cost += words / 32.0 * 8.0 / std::max<double>(1.0, double(p->colidx.size()));
@@ -232,6 +276,7 @@ skc_status configure_direct(skc_plan *p) {
     g.bulk = bulk ? 1 : 0;
     p->NW = kDirectNW;
     p->M = p->T <= 8 ? 4 : (p->T <= 16 ? 2 : 1);
+    if (small && best_M > 0) p->M = std::min(p->M, best_M);
     // tuning overrides (benchmarks): SKC_DIRECT_NW (compute warps, 1..16), SKC_DIRECT_M
     if (const char *e = std::getenv("SKC_DIRECT_NW")) p->NW = std::max(1, std::min(16, std::atoi(e)));
     if (const char *e = std::getenv("SKC_DIRECT_M")) p->M = std::max(1, std::min(4, std::atoi(e)));
@@ -821,15 +866,28 @@ extern "C" {
 const char *skc_last_error(void) { return g_err.c_str(); }
 
 static skc_status pack_common(const float *w, int K, int C, int R, int S, int H, int W, int stride,
-                       int pad, int groups, int kernel, int max_ni, skc_plan **out);
+                       int pad, int groups, int kernel, int max_ni, int batch_hint, skc_plan **out);
+
+// The configuration's default batch: 256 (the benchmark batch), or SKC_JIT_NHINT.
+static int default_batch_hint() {
+    const char *e = std::getenv("SKC_JIT_NHINT");
+    return e ? std::max(1, std::atoi(e)) : 256;
+}
 
 skc_status skc_pack_csr_ex(const float *w, int K, int C, int R, int S, int H, int W,
                            int stride, int pad, int groups, int kernel, skc_plan **out) {
-    return pack_common(w, K, C, R, S, H, W, stride, pad, groups, kernel, 4, out);
+    return pack_common(w, K, C, R, S, H, W, stride, pad, groups, kernel, 4, default_batch_hint(), out);
+}
+
+skc_status skc_pack_csr_batch(const float *w, int K, int C, int R, int S, int H, int W,
+                              int stride, int pad, int groups, int kernel, int batch_hint,
+                              skc_plan **out) {
+    if (batch_hint < 1) return fail(SKC_ERR_ARG, "batch_hint %d < 1", batch_hint);
+    return pack_common(w, K, C, R, S, H, W, stride, pad, groups, kernel, 4, batch_hint, out);
 }
 
 static skc_status pack_common(const float *w, int K, int C, int R, int S, int H, int W, int stride,
-                       int pad, int groups, int kernel, int max_ni, skc_plan **out) {
+                       int pad, int groups, int kernel, int max_ni, int batch_hint, skc_plan **out) {
     if (!w || !out) return fail(SKC_ERR_ARG, "NULL weights or output pointer");
     *out = nullptr;
     if (kernel < SKC_KERNEL_AUTO || kernel > SKC_KERNEL_SPMDM)
@@ -844,6 +902,7 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
     p->Ho = (p->Hp - R) / stride + 1; p->Wo = (p->Wp - S) / stride + 1;
     p->Kg = K / groups; p->Cg = C / groups;
     p->max_ni = max_ni;
+    p->batch_hint = std::max(1, batch_hint);
 
     // a1: canonical CSR.  Row k scans (c_local, r, s) lexicographically; because r < Hp
     // and s < Wp the offset is strictly increasing in that order.
@@ -916,12 +975,23 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
     const char *nojit = std::getenv("SKC_NO_JIT");
     // (AUTO keeps single-image FC plans -- max_ni == 1 -- on the data-driven kernels: their
     // code would be millions of instructions for ~one CTA item per block)
+    // (AUTO also keeps small batches on them: a compiled layer's code is fetched cold by the
+    // few CTAs a small batch has, and the direct kernel with a small-batch configuration is
+    // faster below kAutoJitMinBatch images per launch, profiles/r02_small_batch.txt)
     if (kernel == SKC_KERNEL_JIT ||
-        (kernel == SKC_KERNEL_AUTO && max_ni > 1 && !(nojit && nojit[0] == '1'))) {
+        (kernel == SKC_KERNEL_AUTO && max_ni > 1 && p->batch_hint >= kAutoJitMinBatch &&
+         !(nojit && nojit[0] == '1'))) {
         const JitInput ji{K, C, R, S, p->Hp, p->Wp, p->Ho, p->Wo, stride, groups, p->Kg, p->Cg, pad,
                           p->rowptr.data(), p->colidx.data(), p->perm.data(), p->values.data()};
         std::string msg;
-        const int r = jit_configure(ji, max_ni == 1 ? 1 : 64, &p->jit, &msg);
+        // the configuration search at small batch hints picks code-heavy blocks (few channels
+        // each) whose cold code costs more than the model charges: below 64 images it
+        // configures for 32 (measured best at 8-32 images), from 64 up for 256 (the 64- and
+        // 128-image configurations measured no faster; profiles/r02_small_batch.txt)
+        // (SKC_JIT_NHINT, an experiment knob, is passed through unchanged)
+        int jit_hint = p->batch_hint < 64 ? 32 : 256;
+        if (max_ni == 1 || std::getenv("SKC_JIT_NHINT")) jit_hint = max_ni == 1 ? 256 : p->batch_hint;
+        const int r = jit_configure(ji, max_ni == 1 ? 1 : 64, jit_hint, &p->jit, &msg);
         if (r == SKC_OK) {
             p->kernel = SKC_KERNEL_JIT;
             p->image.assign(jit_image_bytes(p->jit), 0);   // lane tables, counters, staging
@@ -940,7 +1010,10 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
         }
     }
     RtCandidate best_rt;
-    if (kernel != SKC_KERNEL_DIRECT) {
+    // (small batches: the register-tiled kernel's configurations are per-image ones; AUTO
+    // takes the direct kernel's launch-time configuration there)
+    const bool small_auto = kernel == SKC_KERNEL_AUTO && p->batch_hint < kAutoJitMinBatch;
+    if (kernel != SKC_KERNEL_DIRECT && !small_auto) {
         RegtileShape shapes[32];
         const int ns = std::min(32, regtile_shapes(shapes, 32));
         // SKC_RT_SHAPE="R,S,TY,TX,M" restricts the search to one shape (tuning/benchmarks)
@@ -1008,7 +1081,7 @@ skc_status skc_pack_fc(const float *w, int M, int K, int B, int kernel, skc_plan
     int rows = 1;
     if (const char *e = std::getenv("SKC_FC_ROWS")) rows = std::max(1, std::atoi(e));
     if (B % rows) rows = 1;
-    return pack_common(w, M, K, 1, 1, rows, B / rows, 1, 0, 1, kernel, 1, out);
+    return pack_common(w, M, K, 1, 1, rows, B / rows, 1, 0, 1, kernel, 1, default_batch_hint(), out);
 }
 
 skc_status skc_plan_info(const skc_plan *p, skc_info *info) {

@@ -152,7 +152,7 @@ struct JitInfo {
 };
 struct JitPlan;
 // Pick the tile / channel-block / staging configuration (host, cheap; no code generated).
-int jit_configure(const JitInput &in, int max_ni, JitPlan **out, std::string *msg);
+int jit_configure(const JitInput &in, int max_ni, int batch_hint, JitPlan **out, std::string *msg);
 // Generate + compile + link the code (host; thread pool; on-disk cache).
 int jit_compile(JitPlan *jp, std::string *msg);
 // device image of the plan's kernel-private tables (lane tables, scheduling counters, raw

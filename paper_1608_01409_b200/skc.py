@@ -24,7 +24,7 @@ STATUS = {0: "SKC_OK", -1: "SKC_ERR_ARG", -2: "SKC_ERR_GEOMETRY", -3: "SKC_ERR_N
           -7: "SKC_ERR_STATE", -8: "SKC_ERR_CUDA"}
 
 # Every symbol include/skc.h declares (checked by tests/test_abi.py).
-EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_plan_info", "skc_plan_csr", "skc_plan_perm",
+EXPORTS = ("skc_pack_csr", "skc_pack_csr_ex", "skc_pack_csr_batch", "skc_plan_info", "skc_plan_csr", "skc_plan_perm",
            "skc_plan_upload", "skc_pad_input", "skc_sparse_conv_forward", "skc_forward_host",
            "skc_layout_offset", "skc_plan_destroy", "skc_last_error", "skc_model_layer_cost",
            "skc_model_project", "skc_model_window", "skc_bench_ffma", "skc_bench_lds",
@@ -95,6 +95,7 @@ def lib():
         sig = {
             "skc_pack_csr": [_P] + [_I] * 9 + [ctypes.POINTER(_P)],
             "skc_pack_csr_ex": [_P] + [_I] * 10 + [ctypes.POINTER(_P)],
+            "skc_pack_csr_batch": [_P] + [_I] * 11 + [ctypes.POINTER(_P)],
             "skc_plan_info": [_P, ctypes.POINTER(skc_info)],
             "skc_plan_verify": [_P],
             "skc_plan_compile": [_P],
@@ -216,13 +217,18 @@ class Plan:
 
 # ------------------------------------------------------------------ C-ABI mirrors
 def skc_pack_csr(w: np.ndarray, H: int, W: int, stride: int = 1, pad: int = 0, groups: int = 1,
-                 kernel: int = SKC_KERNEL_AUTO) -> Plan:
-    """a1: pruned dense weights float32 [K, C/g, R, S] (host) -> Plan."""
+                 kernel: int = SKC_KERNEL_AUTO, batch_hint: int = None) -> Plan:
+    """a1: pruned dense weights float32 [K, C/g, R, S] (host) -> Plan, configured for
+    batch_hint images per forward call (None: skc_pack_csr_ex's default, 256)."""
     w = np.ascontiguousarray(w, dtype=np.float32)
     K, Cg, R, S = w.shape
     h = _P()
-    _check(lib().skc_pack_csr_ex(w.ctypes.data, K, Cg * groups, R, S, H, W, stride, pad, groups,
-                                 kernel, ctypes.byref(h)))
+    if batch_hint is None:
+        _check(lib().skc_pack_csr_ex(w.ctypes.data, K, Cg * groups, R, S, H, W, stride, pad, groups,
+                                     kernel, ctypes.byref(h)))
+    else:
+        _check(lib().skc_pack_csr_batch(w.ctypes.data, K, Cg * groups, R, S, H, W, stride, pad,
+                                        groups, kernel, int(batch_hint), ctypes.byref(h)))
     return Plan(h.value)
 
 
@@ -444,8 +450,8 @@ class SparseConv2d:
 
     @classmethod
     def from_dense(cls, w: np.ndarray, H: int, W: int, stride=1, pad=0, groups=1,
-                   kernel=SKC_KERNEL_AUTO, device="cuda"):
-        plan = skc_pack_csr(w, H, W, stride, pad, groups, kernel)
+                   kernel=SKC_KERNEL_AUTO, device="cuda", batch_hint=None):
+        plan = skc_pack_csr(w, H, W, stride, pad, groups, kernel, batch_hint)
         plan.upload(device)
         return cls(plan, plan.info())
 

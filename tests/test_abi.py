@@ -205,6 +205,39 @@ def test_plan_verify_random(L):
     assert n_rt >= 20
 
 
+def test_batch_hint_configurations(L):
+    """skc_pack_csr_batch: the configuration follows the batch the plan is packed for (DESIGN.md
+    Sec. 7.5): AUTO takes the direct kernel below 8 images per call and the compiled-weights
+    kernel from 8 up; a batch hint never changes the canonical CSR (bit-exact against the
+    independent packer for every hint); small-batch direct configurations stage no more images
+    per CTA than the batch has and pass the plan's static self-check on random geometries."""
+    cfg = wl.CONFIGS[2]
+    L = cfg.layers[1]
+    w = wl.gen_weights(2, 1, L)
+    with pytest.raises(skc.SkcError) as e:
+        skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_AUTO, 0)
+    assert e.value.status == -1
+    ref = ref_pack(w, L.H, L.W, L.pad, L.groups)
+    for hint, kern in ((1, skc.SKC_KERNEL_DIRECT), (2, skc.SKC_KERNEL_DIRECT), (7, skc.SKC_KERNEL_DIRECT),
+                       (8, skc.SKC_KERNEL_JIT), (256, skc.SKC_KERNEL_JIT), (4096, skc.SKC_KERNEL_JIT)):
+        plan = skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_AUTO, hint)
+        info = plan.info()
+        assert info["kernel"] == kern, (hint, info["kernel"])
+        assert info["images_per_cta"] <= max(2, hint) or kern == skc.SKC_KERNEL_JIT
+        assert_pack_equal(plan, ref)
+        skc.skc_plan_verify(plan)
+    rng = np.random.default_rng(23)
+    for it in range(60):
+        layer = wl.random_layer(rng, max_c=24, max_hw=30, rs=(1, 3, 5), groups=(1, 2))
+        w, _ = wl.random_tensors(rng, layer, 1)
+        for hint in (1, 3):
+            plan = skc.skc_pack_csr(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                    skc.SKC_KERNEL_AUTO, hint)
+            assert plan.info()["kernel"] == skc.SKC_KERNEL_DIRECT
+            assert plan.info()["images_per_cta"] <= hint + (hint % 2)
+            skc.skc_plan_verify(plan)
+
+
 def test_library_never_allocates_device_memory():
     """skc.h: libskc never allocates device memory -- PyTorch owns every buffer (workspace,
     activations, tuning scratch).  No allocation call may appear in the library's sources."""
