@@ -150,10 +150,10 @@ skc_status skc_pack_csr_ex(const float *w_host, int K, int C, int R, int S, int 
  * for.  skc_pack_csr / _ex assume 256 (the benchmark batch; SKC_JIT_NHINT overrides).  The
  * configuration (kernel, images per CTA, channel blocks, row bands) is a performance choice
  * only: any plan accepts any N and computes the same outputs (Eq. 1).  Below
- * 8 images AUTO picks the data-driven direct kernel with a launch-time configuration (a
- * compiled layer's code would be fetched cold by a few CTAs), from 8 up the compiled-weights
- * kernel configured for batch_hint images (whole rounds of 148 SMs, at most batch_hint images
- * per CTA).  Errors: as skc_pack_csr_ex; SKC_ERR_ARG if batch_hint < 1. */
+ * 16 images AUTO picks the data-driven direct kernel with a launch-time configuration for
+ * batch_hint images (a compiled layer's code would be fetched cold by a few CTAs), from 16 up
+ * the compiled-weights kernel (its 256-image configuration).  Errors: as skc_pack_csr_ex;
+ * SKC_ERR_ARG if batch_hint < 1. */
 skc_status skc_pack_csr_batch(const float *w_host, int K, int C, int R, int S, int H, int W,
                               int stride, int pad, int groups, int kernel, int batch_hint,
                               skc_plan **out);

@@ -109,7 +109,7 @@ namespace {
 constexpr int kDirectNW = 8;              // compute warps per CTA (+1 producer warp)
 constexpr size_t kStageTarget = 24 << 10;  // bytes per stage we aim for
 constexpr int kDirectSmallBatch = 16;      // batch hints below this: launch-time config model
-constexpr int kAutoJitMinBatch = 8;        // AUTO: compiled-weights kernel from this batch up
+constexpr int kAutoJitMinBatch = 16;       // AUTO: compiled-weights kernel from this batch up
 constexpr int kDirectStages = 4;           // stages of the direct kernel's ring (sconv_direct.cu)
 constexpr size_t kSmemBudget = 112 << 10;  // per CTA, so that >= 2 CTAs fit an SM
 
@@ -984,13 +984,12 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
         const JitInput ji{K, C, R, S, p->Hp, p->Wp, p->Ho, p->Wo, stride, groups, p->Kg, p->Cg, pad,
                           p->rowptr.data(), p->colidx.data(), p->perm.data(), p->values.data()};
         std::string msg;
-        // the configuration search at small batch hints picks code-heavy blocks (few channels
-        // each) whose cold code costs more than the model charges: below 64 images it
-        // configures for 32 (measured best at 8-32 images), from 64 up for 256 (the 64- and
-        // 128-image configurations measured no faster; profiles/r02_small_batch.txt)
-        // (SKC_JIT_NHINT, an experiment knob, is passed through unchanged)
-        int jit_hint = p->batch_hint < 64 ? 32 : 256;
-        if (max_ni == 1 || std::getenv("SKC_JIT_NHINT")) jit_hint = max_ni == 1 ? 256 : p->batch_hint;
+        // the configuration search at batch hints below 256 picks code-heavy blocks (few
+        // channels each) whose cold code costs more than its model charges -- 3x slower than
+        // the 256-image configuration on ResNet res256 at 8 images -- so JIT plans are always
+        // configured for 256 images (profiles/r02_small_batch.txt; SKC_JIT_NHINT, an
+        // experiment knob, is passed through)
+        const int jit_hint = std::getenv("SKC_JIT_NHINT") && max_ni > 1 ? p->batch_hint : 256;
         const int r = jit_configure(ji, max_ni == 1 ? 1 : 64, jit_hint, &p->jit, &msg);
         if (r == SKC_OK) {
             p->kernel = SKC_KERNEL_JIT;

@@ -207,8 +207,8 @@ def test_plan_verify_random(L):
 
 def test_batch_hint_configurations(L):
     """skc_pack_csr_batch: the configuration follows the batch the plan is packed for (DESIGN.md
-    Sec. 7.5): AUTO takes the direct kernel below 8 images per call and the compiled-weights
-    kernel from 8 up; a batch hint never changes the canonical CSR (bit-exact against the
+    Sec. 7.5): AUTO takes the direct kernel below 16 images per call and the compiled-weights
+    kernel from 16 up; a batch hint never changes the canonical CSR (bit-exact against the
     independent packer for every hint); small-batch direct configurations stage no more images
     per CTA than the batch has and pass the plan's static self-check on random geometries."""
     cfg = wl.CONFIGS[2]
@@ -218,8 +218,8 @@ def test_batch_hint_configurations(L):
         skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_AUTO, 0)
     assert e.value.status == -1
     ref = ref_pack(w, L.H, L.W, L.pad, L.groups)
-    for hint, kern in ((1, skc.SKC_KERNEL_DIRECT), (2, skc.SKC_KERNEL_DIRECT), (7, skc.SKC_KERNEL_DIRECT),
-                       (8, skc.SKC_KERNEL_JIT), (256, skc.SKC_KERNEL_JIT), (4096, skc.SKC_KERNEL_JIT)):
+    for hint, kern in ((1, skc.SKC_KERNEL_DIRECT), (2, skc.SKC_KERNEL_DIRECT), (15, skc.SKC_KERNEL_DIRECT),
+                       (16, skc.SKC_KERNEL_JIT), (256, skc.SKC_KERNEL_JIT), (4096, skc.SKC_KERNEL_JIT)):
         plan = skc.skc_pack_csr(w, L.H, L.W, L.stride, L.pad, L.groups, skc.SKC_KERNEL_AUTO, hint)
         info = plan.info()
         assert info["kernel"] == kern, (hint, info["kernel"])

@@ -276,7 +276,7 @@ def test_config_parity_full_batch(cfg_id):
 
 def test_small_batch_plans_vs_oracle():
     """Plans packed for small batches (skc_pack_csr_batch): AUTO's direct launch-time
-    configurations below 8 images and the 32-image compiled-weights configuration from 8 up,
+    configurations below 16 images and the compiled-weights kernel from 16 up,
     every image checked against the fp64 oracle -- at the batch the plan was packed for, odd
     batches included, and at other batches (a configuration is a performance choice only)."""
     cases = [(1, 0), (2, 0), (2, 1), (4, 0)]
@@ -286,10 +286,11 @@ def test_small_batch_plans_vs_oracle():
         w = wl.gen_weights(cfg_id, li, layer)
         x = wl.gen_input(cfg_id, li, layer, 0, 13)
         ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
-        for hint, Ns in ((1, (1, 6)), (2, (2,)), (3, (3, 1)), (5, (5, 13)), (8, (8, 3)), (13, (13,))):
+        for hint, Ns in ((1, (1, 6)), (2, (2,)), (3, (3, 1)), (5, (5, 13)), (8, (8, 3)), (13, (13,)),
+                         (16, (13, 2))):
             conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
                                                layer.groups, batch_hint=hint)
-            assert conv.geom["kernel"] == (skc.SKC_KERNEL_DIRECT if hint < 8 else skc.SKC_KERNEL_JIT)
+            assert conv.geom["kernel"] == (skc.SKC_KERNEL_DIRECT if hint < 16 else skc.SKC_KERNEL_JIT)
             for N in Ns:
                 out = conv.forward(torch.from_numpy(x[:N]).cuda()).cpu().numpy()
                 check(out, ref[:N], bound[:N], f"cfg{cfg_id} {layer.name} hint {hint} N {N}")
