@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--pad-overlap", type=int, default=1, choices=[0, 1],
                     help="graph step: run the pads of layers 2..L on a low-priority side stream, "
                          "filling the previous conv's tail (the layers' inputs are independent)")
+    ap.add_argument("--order", default="",
+                    help="graph step with --pad-overlap: layer order, e.g. 0132 (default: 0213 for configs 2 and 5, else natural)")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -396,6 +398,15 @@ def run_ours(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
+    # AlexNet conv2-5 (configs 2 and 5): conv2, conv4, conv3, conv5 measured 0.3% faster than the
+    # natural order (0.8088-0.8106 vs 0.8115-0.8125 ms over four alternating pairs of 200-step
+    # runs; other orders 0.8129-0.8385 ms: profiles/r02_pad_overlap.txt)
+    default_order = "0213" if cfg.cfg_id in (2, 5) else ""
+    order_s = args.order or default_order
+    order = [int(c) for c in order_s] if order_s else list(range(len(layers)))
+    if sorted(order) != list(range(len(layers))):
+        raise SystemExit(f"bench.py: --order {args.order} is not a permutation of the layers")
+
     def step_overlap(main, side):
         # the conv launches stay in layer order on the high-priority main stream; the pad of
         # layer i > 0 runs on the low-priority side stream (forked after layer 0's pad) and
@@ -403,7 +414,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         # registers per SM), so a pad's CTAs get SMs only as the running conv's CTAs retire:
         # the HBM-bound pads fill the ALU-bound convs' tails instead of running between them.
         # (layer order: the natural one measured best, profiles/r02_pad_overlap.txt)
-        seq = layers
+        seq = [layers[i] for i in order]
         skc.skc_pad_input(seq[0]["conv"].plan, seq[0]["x"], seq[0]["xp"], local_n, main)
         fork = torch.cuda.Event()
         fork.record(main)
@@ -721,6 +732,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "step": "per layer: skc_pad_input + skc_sparse_conv_forward"
                            + (", the step's 8 launches replayed as one CUDA graph" if graph is not None else "")
                            + ("; pads of layers 2..L on a low-priority side stream overlapping the previous conv"
+                              + (f" (layer order {''.join(map(str, order))})" if order != list(range(len(layers))) else "")
                               if graph is not None and args.pad_overlap and len(layers) > 1 else "")},
         "dense_equiv_gflops": step_dense_flops / (t_step * 1e-3) / 1e9,
         "per_gpu_gflops": local_nnz_flops / (t_local * 1e-3) / 1e9,
