@@ -841,6 +841,12 @@ std::string emit_block(const JitPlan &jp, int b, const std::vector<int> &ks,
             o("mul.wide.u32 %%rd6, %%r16, %d;", tx);
             o("add.u64 %%rdp%d, %%rdp%d, %%rd6;", i, i);
         }
+        if (std::getenv("SKC_JIT_NOSTORE")) {
+            // measurement only: the stores stay in the code (so nothing is dead) but are
+            // predicated off by a runtime-false predicate (relu flag == 77): no output traffic
+            o("setp.eq.u32 %%p9, %%r4, 77;");
+            for (int i = 0; i < 2 * T; ++i) o("and.pred %%pe%d, %%pe%d, %%p9;", i, i);
+        }
         o("@%%p1 bra $EPI_B;");
         for (int relu = 0; relu < 2; ++relu) {
             o("$EPI_%c:", relu ? 'R' : 'N');
