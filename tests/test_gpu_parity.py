@@ -297,6 +297,29 @@ def test_small_batch_plans_vs_oracle():
             del conv
 
 
+def test_small_batch_random_geometries():
+    """Direct small-batch configurations (AUTO below 16 images) on 120 random layers (strides,
+    groups, 1x1 to 5x5, ragged sizes, empty channels) at the batch they were packed for and at
+    another one, every output against the fp64 oracle."""
+    rng = np.random.default_rng(31)
+    worst = 0.0
+    for it in range(120):
+        layer = wl.random_layer(rng, max_c=32, max_hw=20, rs=(1, 2, 3, 5), groups=(1, 2, 4))
+        hint = int(rng.integers(1, 16))
+        w, x = wl.random_tensors(rng, layer, hint + 2)
+        if it % 7 == 0:
+            w[rng.integers(0, layer.K)] = 0.0
+        conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                           layer.groups, batch_hint=hint)
+        assert conv.geom["kernel"] == skc.SKC_KERNEL_DIRECT
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        for N in (hint, hint + 2):
+            out = conv.forward(torch.from_numpy(x[:N]).cuda()).cpu().numpy()
+            worst = max(worst, check(out, ref[:N], bound[:N], f"it{it} {layer} hint {hint} N {N}"))
+        del conv
+    print("max err/bound", worst)
+
+
 def test_config5_sharded_parity():
     """BASELINE.json configs[4]: config 2's layers at batch 4096, sharded over 8 GPUs.  On
     one GPU: the whole batch, and each of the 8 shards run separately (as the 8 ranks would,
