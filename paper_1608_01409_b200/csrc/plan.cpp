@@ -1038,6 +1038,13 @@ static skc_status pack_common(const float *w, int K, int C, int R, int S, int H,
         }
     }
     st = configure_direct(p);
+    if (small_auto && st != SKC_OK) {
+        // no small-batch direct configuration (e.g. a row wider than the kernel's pixel
+        // slots): the configuration for kAutoJitMinBatch images, whatever the kernel
+        delete p;
+        return pack_common(w, K, C, R, S, H, W, stride, pad, groups, kernel, max_ni,
+                           kAutoJitMinBatch, out);
+    }
     if (kernel == SKC_KERNEL_REGTILE && best_rt.cost >= 1e300) {
         delete p;
         return fail(SKC_ERR_UNSUPPORTED, "no register-tile shape for R=%d S=%d stride=%d "
