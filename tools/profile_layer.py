@@ -22,13 +22,15 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kernel", default="auto", choices=["auto", "direct", "regtile"])
+    ap.add_argument("--batch-hint", type=int, default=0, help="plan configured for this batch")
     a = ap.parse_args()
     cfg = wl.CONFIGS[a.config]
     L = cfg.layers[a.layer]
     N = a.batch or cfg.batch
     kern = {"auto": 0, "direct": 1, "regtile": 2}[a.kernel]
     w = wl.gen_weights(a.config, a.layer, L)
-    conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kern)
+    conv = skc.SparseConv2d.from_dense(w, L.H, L.W, L.stride, L.pad, L.groups, kern,
+                                       batch_hint=a.batch_hint or None)
     x = torch.from_numpy(wl.gen_input(a.config, a.layer, L, 0, N)).cuda()
     xp = torch.empty(conv.padded_shape(N), device="cuda")
     out = torch.empty(conv.out_shape(N), device="cuda")
