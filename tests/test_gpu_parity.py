@@ -320,6 +320,30 @@ def test_small_batch_random_geometries():
     print("max err/bound", worst)
 
 
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_large_and_stem_geometries(kernel):
+    """Network layers outside the BASELINE configs, at full size: the ResNet stem (3 -> 64,
+    224x224, 7x7, stride 2, pad 3), AlexNet conv1 (3 -> 96, 227x227, 11x11, stride 4), a
+    112x112 3x3 layer (many row bands), and a 1x1 projection with stride 2 -- odd channel
+    counts and planes (no 16-byte TMA runs: AUTO falls back to the data-driven kernels), large
+    strides and kernels, every output of 2 images against the fp64 oracle."""
+    rng = np.random.default_rng(41)
+    layers = [wl.Layer("resnet_stem", 64, 3, 224, 224, 7, 7, 2, 3, 1, 0.5, 1.0),
+              wl.Layer("alexnet_conv1", 96, 3, 227, 227, 11, 11, 4, 0, 1, 0.5, 1.0),
+              wl.Layer("c64_112", 64, 64, 112, 112, 3, 3, 1, 1, 1, 0.7, 1.0),
+              wl.Layer("proj_s2", 128, 64, 56, 56, 1, 1, 2, 0, 1, 0.7, 1.0)]
+    for layer in layers:
+        w, x = wl.random_tensors(rng, layer, 2)
+        try:
+            out, conv = run_gpu(w, x, layer, kernel)
+        except skc.SkcError as e:  # a forced kernel may not tile a shape; AUTO must
+            assert kernel != skc.SKC_KERNEL_AUTO and e.status == -5, (layer.name, e)
+            continue
+        ref, bound = oracle.conv2d_fp64(x, w, layer.stride, layer.pad, layer.groups)
+        check(out, ref, bound, f"{layer.name} kernel {conv.geom['kernel']}")
+        del conv
+
+
 def test_config5_sharded_parity():
     """BASELINE.json configs[4]: config 2's layers at batch 4096, sharded over 8 GPUs.  On
     one GPU: the whole batch, and each of the 8 shards run separately (as the 8 ranks would,
