@@ -110,7 +110,6 @@ constexpr int kDirectNW = 8;              // compute warps per CTA (+1 producer 
 constexpr size_t kStageTarget = 24 << 10;  // bytes per stage we aim for
 constexpr int kDirectSmallBatch = 16;      // batch hints below this: launch-time config model
 constexpr int kAutoJitMinBatch = 16;       // AUTO: compiled-weights kernel from this batch up
-constexpr int kDirectStages = 4;           // stages of the direct kernel's ring (sconv_direct.cu)
 constexpr size_t kSmemBudget = 112 << 10;  // per CTA, so that >= 2 CTAs fit an SM
 
 skc_status check_geometry(int K, int C, int R, int S, int H, int W, int stride, int pad,
@@ -225,11 +224,8 @@ skc_status configure_direct(skc_plan *p) {
                 const bool bulk_ok = bulk_legal(p, NI, BH, BHin, nb, whole, CB, chan_stride, IS);
                 const int M0 = T <= 8 ? 4 : 2;
                 if (small) {
-                    const size_t smem_est = size_t(kDirectStages) * (size_t(IS) * NI * 4 + 4096);
-                    const int per_sm = std::max(1, int((227u << 10) / std::max<size_t>(1, smem_est)));
                     // co-resident CTAs of these latency-bound launches slow each other about
                     // as much as a second wave would: count waves of 148
-                    (void)per_sm;
                     const double P = 148.0;
                     const double nig = std::ceil(double(p->batch_hint) / NI);
                     for (int M = M0; M >= 1; M /= 2) {
