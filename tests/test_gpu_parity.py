@@ -344,6 +344,35 @@ def test_large_and_stem_geometries(kernel):
         del conv
 
 
+@pytest.mark.parametrize("kernel", [skc.SKC_KERNEL_AUTO, skc.SKC_KERNEL_DIRECT])
+def test_beyond_2gib_offsets(kernel):
+    """Maximum sizes: config 2's conv3 at 10240 images -- a 2.36 GB padded input and a 2.66 GB
+    output, so image offsets pass 2^31 bytes in both -- pad + conv through the C-ABI, then
+    sampled images (first, last, both sides of the 2 GiB boundaries, random) against the
+    oracle."""
+    layer = wl.CONFIGS[2].layers[1]
+    N = 10240
+    w = wl.gen_weights(2, 1, layer)
+    conv = skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad, layer.groups,
+                                       kernel)
+    x = torch.empty((N, layer.C, layer.H, layer.W), device="cuda")
+    for n0 in range(0, N, 256):  # the seeded generator, in slices
+        x[n0:n0 + 256] = torch.from_numpy(wl.gen_input(2, 1, layer, n0, n0 + 256))
+    out = conv.forward(x)
+    torch.cuda.synchronize()
+    edges = [(1 << 31) // (layer.K * layer.Ho * layer.Wo * 4),                 # output
+             (1 << 31) // (layer.C * (layer.H + 2 * layer.pad) * (layer.W + 2 * layer.pad) * 4)]
+    assert all(e + 1 < N for e in edges)
+    rng = np.random.default_rng(5)
+    idx = sorted({0, N - 1, *[e + d for e in edges for d in (-1, 0, 1)],
+                  *map(int, rng.integers(0, N, 3))})
+    xs = x[idx].cpu().numpy()
+    ref, bound = oracle.conv2d_fp64(xs, w, layer.stride, layer.pad, layer.groups)
+    check(out[idx].cpu().numpy(), ref, bound, f"N={N} images {idx} kernel {conv.geom['kernel']}")
+    del x, out, conv
+    torch.cuda.empty_cache()
+
+
 def test_config5_sharded_parity():
     """BASELINE.json configs[4]: config 2's layers at batch 4096, sharded over 8 GPUs.  On
     one GPU: the whole batch, and each of the 8 shards run separately (as the 8 ranks would,
