@@ -373,6 +373,37 @@ def test_beyond_2gib_offsets(kernel):
     torch.cuda.empty_cache()
 
 
+def test_concurrent_streams_separate_workspaces():
+    """skc.h thread-safety contract: launches that use different workspaces may overlap.  The
+    four AlexNet layers, plus a second upload of conv3's plan (its own workspace: the work-item
+    counter and the first-item claim table), run at the same time on five streams, repeated;
+    every output is bitwise equal to the same launch run alone."""
+    cfg = wl.CONFIGS[2]
+    N = 64
+    convs, xs = [], []
+    for li, layer in enumerate(cfg.layers):
+        w = wl.gen_weights(2, li, layer)
+        convs.append(skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                                 layer.groups))
+        xs.append(torch.from_numpy(wl.gen_input(2, li, layer, 0, N)).cuda())
+        if li == 1:
+            convs.append(skc.SparseConv2d.from_dense(w, layer.H, layer.W, layer.stride, layer.pad,
+                                                     layer.groups))
+            xs.append(torch.from_numpy(wl.gen_input(2, li, layer, N, 2 * N)).cuda())
+    alone = [c.forward(x) for c, x in zip(convs, xs)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in convs]
+    for rep in range(5):
+        outs = [None] * len(convs)
+        for i, (c, x, st) in enumerate(zip(convs, xs, streams)):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                outs[i] = c.forward(x, stream=st)
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(zip(alone, outs)):
+            assert torch.equal(a.view(torch.int32), b.view(torch.int32)), (rep, i)
+
+
 def test_config5_sharded_parity():
     """BASELINE.json configs[4]: config 2's layers at batch 4096, sharded over 8 GPUs.  On
     one GPU: the whole batch, and each of the 8 shards run separately (as the 8 ranks would,
